@@ -1,0 +1,192 @@
+/*
+ * tdb.h - C ABI of the B200-native lag-block assembly + block Hessenberg matvec
+ * for the space-time Galerkin TDBIE (arXiv:1503.07221).
+ *
+ * Every entry point returns int: TDB_OK (0) or a negative TDB_E* code;
+ * tdb_last_error() gives a thread-local message.  No C++ exceptions and no
+ * torch types cross this boundary; arrays are plain pointers + sizes, all
+ * float64 C-contiguous unless stated.  Pointers named *_dev are device
+ * pointers; all others are host pointers owned by the caller.
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/tdbem/):
+ *   tdb_pair_block_contributions  <- _kernels/__init__.py:7-9,32
+ *                                    (_core.pyx:81-193, _fallback.py:239-274)
+ *   tdb_system_assemble           <- block_system.py:228-275 assemble_system
+ *                                    + assembly.py:240-306 assemble_subblocks
+ *   tdb_system_copy_family        <- the CSR lists of BlockHessenbergMatrix
+ *                                    .unique_blocks (block_system.py:145)
+ *   tdb_matvec (+ plan)           <- block_system.py:180-216 matvec(x, rows, cols)
+ */
+#ifndef TDB_H_
+#define TDB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TDB_ABI_VERSION 1
+
+enum {
+  TDB_OK = 0,
+  TDB_E_INVALID = -1,   /* bad argument / shape (ValueError) */
+  TDB_E_CUDA = -2,      /* CUDA runtime failure (RuntimeError) */
+  TDB_E_NOMEM = -3,     /* device allocation failed (MemoryError) */
+  TDB_E_NODEVICE = -4,  /* no CUDA device visible (RuntimeError) */
+  TDB_E_UNSUPPORTED = -5
+};
+
+/* Packed psi / psi~ tables of one block position (assembly.py:68-127 PsiPack).
+ * nt = 2 (p+1)^2 tables, index t = (m2 (p+1) + m1) * 2 + {0: psi, 1: psi~}.
+ * coeffs is (nt, max_nsub, deg+1). */
+typedef struct TdbPsiPack {
+  int32_t p;
+  int32_t deg;
+  int32_t max_nsub;
+  int32_t reserved;
+  double delta;
+  const double* lo;       /* (nt,) */
+  const double* width;    /* (nt,) */
+  const int64_t* nsub;    /* (nt,) */
+  const double* coeffs;   /* (nt, max_nsub, deg+1) */
+  const double* sp;       /* (nt,) sign for a >= 0 (folded tables) */
+  const double* sn;       /* (nt,) sign for a < 0 */
+  const uint8_t* fold;    /* (nt,) */
+  const uint8_t* active;  /* (nt,) */
+} TdbPsiPack;
+
+/* Drop-in for tdbem._kernels.pair_block_contributions.
+ * cx, cy (npair,3,3) chart corners; a2x, a2y, ndot (npair,); curly, curlx
+ * (npair,3,3); xhat, yhat (nq,2); wq (nq,).  out (npair,p+1,p+1,3,3) is
+ * written (not accumulated): out[P,m2,m1,a,b] = contribution of pair P to
+ * sub-block (m2,m1) at (row = y chart vertex a, col = x chart vertex b).
+ * Host pointers; the call copies to the current device and synchronises. */
+int tdb_pair_block_contributions(const double* cx, const double* cy,
+                                 const double* a2x, const double* a2y,
+                                 const double* ndot, const double* curly,
+                                 const double* curlx, const double* xhat,
+                                 const double* yhat, const double* wq,
+                                 int64_t npair, int64_t nq,
+                                 const TdbPsiPack* pack, double* out);
+
+/* ---- device-resident system ------------------------------------------- */
+
+typedef struct TdbMesh {
+  int64_t num_vertices;
+  int64_t num_triangles;
+  const double* corners;   /* (E,3,3) */
+  const double* a2;        /* (E,) twice the triangle area */
+  const double* normals;   /* (E,3) */
+  const double* curls;     /* (E,3,3) n x grad(hat_a) */
+  const int64_t* triangles;/* (E,3) */
+  const int64_t* star_off; /* (V+1,) vertex -> triangles CSR, ascending ids */
+  const int64_t* star_ids; /* (3E,) */
+} TdbMesh;
+
+/* One table family = all canonical block positions sharing (ansatz kind,
+ * test kind): identical tables, only delta differs.  Positions
+ * are listed in lag order so that slo and shi are non-decreasing. */
+typedef struct TdbFamily {
+  int32_t npos;
+  int32_t reserved;
+  const double* delta;     /* (npos,) canonical_origin(it) - canonical_origin(kt) */
+  const double* slo;       /* (npos,) psi_support lower end */
+  const double* shi;       /* (npos,) psi_support upper end */
+  TdbPsiPack pack;         /* delta field ignored */
+} TdbFamily;
+
+typedef struct TdbRule {
+  int64_t nq;
+  const double* xhat;      /* (nq,2) */
+  const double* yhat;      /* (nq,2) */
+  const double* w;         /* (nq,) */
+} TdbRule;
+
+enum { TDB_CASE_REGULAR = 0, TDB_CASE_COINCIDENT = 1, TDB_CASE_EDGE = 2, TDB_CASE_VERTEX = 3 };
+
+typedef struct TdbAssemblyDesc {
+  int32_t p;
+  int32_t num_families;
+  const TdbFamily* families;
+  TdbRule rules[4];        /* indexed by TDB_CASE_* */
+} TdbAssemblyDesc;
+
+typedef struct TdbStats {
+  int64_t units;           /* admissible (pair, position) units */
+  int64_t items;           /* warp work items of the quadrature kernel */
+  int64_t n_in;            /* (unit, point) evaluations inside the table support */
+  int64_t n_geom;          /* rule points whose geometry was evaluated */
+  int64_t nnz_total;       /* stored entries over all families */
+  double ms_plan;          /* pair bounds + admissible ranges + scans */
+  double ms_quad;          /* quadrature kernel(s) */
+  double ms_finalize;      /* singular item reduction */
+  double ms_pattern;       /* CSR pattern + compensated gather */
+  double ms_total;
+} TdbStats;
+
+typedef struct TdbContext TdbContext;
+typedef struct TdbSystem TdbSystem;
+
+int tdb_abi_version(void);
+const char* tdb_last_error(void);
+int tdb_device_count(int* count);
+
+int tdb_ctx_create(int device, TdbContext** out);
+int tdb_ctx_destroy(TdbContext* ctx);
+/* stream used by all stream-ordered calls on this context (0 = legacy default) */
+int tdb_ctx_set_stream(TdbContext* ctx, void* cuda_stream);
+
+/* Assemble every family's blocks into device memory (host inputs). */
+int tdb_system_assemble(TdbContext* ctx, const TdbMesh* mesh,
+                        const TdbAssemblyDesc* desc, TdbSystem** out);
+int tdb_system_destroy(TdbSystem* sys);
+int tdb_system_stats(const TdbSystem* sys, TdbStats* out);
+/* nnz of family f (stored pattern incl. explicit zeros) */
+int tdb_system_family_nnz(const TdbSystem* sys, int32_t f, int64_t* nnz);
+/* D2H copy of family f: indptr (npos*M+1,) int64 with rows (s, j);
+ * indices (nnz,) int32 columns; data (nnz,(p+1)^2) */
+int tdb_system_copy_family(const TdbSystem* sys, int32_t f, int64_t* indptr,
+                           int32_t* indices, double* data);
+/* Device pointers of family f (valid until tdb_system_destroy). */
+int tdb_system_family_device(const TdbSystem* sys, int32_t f,
+                             const int64_t** indptr_dev,
+                             const int32_t** indices_dev,
+                             const double** data_dev);
+
+
+/* ---- block Hessenberg matvec (block_system.py:180-216) ------------------
+ * A matvec plan fixes the inclusive 1-based block ranges rows = [rlo, rhi],
+ * cols = [clo, chi] and the list of "terms": one per stored (family f,
+ * position s) that any logical block position (kt, it) in range resolves to,
+ * with d = kt - it constant per term and a bitmask over kt (bit kt-1 of
+ * word (kt-1)/32) of the logical positions that are structurally non-zero
+ * (is_zero_position, block_system.py:153-160, evaluated by the caller).
+ * Vectors are time-major as in the reference: entry ((k-1)(p+1)+m)*M + j
+ * relative to the range start.  tdb_matvec is stream-ordered on the
+ * context's stream and deterministic (fixed summation order). */
+typedef struct TdbMatvecDesc {
+  int32_t N;
+  int32_t rlo, rhi, clo, chi;
+  int32_t nterms;
+  int32_t words;            /* mask words per term = ceil(N / 32) */
+  int32_t reserved;
+  const int32_t* term_family;
+  const int32_t* term_pos;
+  const int32_t* term_d;
+  const uint32_t* term_mask; /* (nterms, words) */
+} TdbMatvecDesc;
+
+typedef struct TdbMatvecPlan TdbMatvecPlan;
+
+int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* desc, TdbMatvecPlan** out);
+int tdb_matvec_plan_destroy(TdbMatvecPlan* plan);
+/* y_dev[(rhi-rlo+1)(p+1)M] = A[rows, cols] x_dev[(chi-clo+1)(p+1)M] (device pointers) */
+int tdb_matvec(TdbMatvecPlan* plan, const double* x_dev, double* y_dev);
+/* canonical stored bytes and logical flops of one application of this plan */
+int tdb_matvec_plan_work(const TdbMatvecPlan* plan, double* algorithmic_bytes, double* flops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TDB_H_ */

@@ -1,0 +1,351 @@
+"""Galerkin assembly of block positions on the GPU (host orchestration).
+
+Reference interface (``tdbem.assembly``, /root/reference/pkg/src/tdbem/assembly.py):
+  QuadratureConfig      :52-65
+  PsiPack / .build      :68-127
+  classify_pair         :130-152
+  assemble_subblocks    :240-306   -> device all-lags assembly of one position
+  assemble_block        :309-311
+Entries are
+    (n_x.n_y)/(4 pi |x-y|) phi_j(y) phi_l(x) psi(|x-y|)
+  + (curl phi_j(y) . curl phi_l(x))/(4 pi |x-y|) psi~(|x-y|)
+rows j = y (test) vertex, columns l = x (ansatz) vertex.
+
+All quadrature runs in libtdb.so (csrc/tdb_assembly.cu); this module only
+builds the small host-side plan (positions grouped into table families, the
+reference rules, n_rad) and converts device CSR to scipy on request.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+from .kernel_weights import PrototypeTables, is_zero_pair, psi_support, tables_for
+from .mesh import SurfaceMesh, touching_pairs
+from .quadrature import Q_REG, Q_SING, n_rad_for, pair_rule_regular, singular_rule
+from .temporal_basis import TimeGrid, canonical_origin, timestep_kind
+
+__all__ = [
+    "QuadratureConfig",
+    "PsiPack",
+    "classify_pair",
+    "assemble_subblocks",
+    "assemble_block",
+    "AssemblyPlan",
+    "build_plan",
+    "DeviceAssembly",
+]
+
+CASES = ("regular", "coincident", "edge", "vertex")
+
+
+@dataclass(frozen=True)
+class QuadratureConfig:
+    """q_reg x q_reg collapsed Gauss per triangle for separated pairs; q_sing
+    tensor Gauss with n_rad x n_ang panels for touching pairs (n_rad=None:
+    min(8, ceil(3 rmax/dt)) from the touching pairs' largest corner distance)."""
+
+    q_reg: int = Q_REG
+    q_sing: int = Q_SING
+    n_rad: int | None = None
+
+
+@dataclass
+class PsiPack:
+    """Packed tables of one block position; t = (m2 (p+1) + m1) * 2 + {0: psi, 1: psi~}."""
+
+    p: int
+    delta: float
+    lo: np.ndarray
+    width: np.ndarray
+    nsub: np.ndarray
+    coeffs: np.ndarray
+    sp: np.ndarray
+    sn: np.ndarray
+    fold: np.ndarray
+    active: np.ndarray
+
+    @classmethod
+    def build(cls, tables: PrototypeTables, grid: TimeGrid, kt: int, it: int) -> "PsiPack":
+        p = grid.p
+        ki, kk = timestep_kind(grid, it), timestep_kind(grid, kt)
+        nt = 2 * (p + 1) ** 2
+        entries = []
+        for m2 in range(p + 1):
+            for m1 in range(p + 1):
+                for tilde in (False, True):
+                    entries.append(tables.resolve(tilde, ki, kk, m1, m2))
+        max_nsub = max([1] + [e[0].n_sub for e in entries if e[0] is not None])
+        pack = cls(
+            p=p,
+            delta=canonical_origin(grid, it) - canonical_origin(grid, kt),
+            lo=np.zeros(nt), width=np.ones(nt), nsub=np.ones(nt, dtype=np.int64),
+            coeffs=np.zeros((nt, max_nsub, tables.deg + 1)),
+            sp=np.ones(nt), sn=np.ones(nt),
+            fold=np.zeros(nt, dtype=np.uint8), active=np.zeros(nt, dtype=np.uint8),
+        )
+        for t, (tbl, s_pos, s_neg, fold) in enumerate(entries):
+            if tbl is None:
+                continue
+            pack.active[t] = 1
+            pack.lo[t], pack.width[t], pack.nsub[t] = tbl.lo, tbl.width, tbl.n_sub
+            pack.coeffs[t, : tbl.n_sub] = tbl.coeffs
+            pack.sp[t], pack.sn[t] = s_pos, s_neg
+            pack.fold[t] = 1 if fold else 0
+        return pack
+
+    def to_c(self, keep: list) -> _lib.TdbPsiPack:
+        """C view of the pack; arrays appended to `keep` stay alive with it."""
+        arrs = dict(
+            lo=_lib.f64(self.lo), width=_lib.f64(self.width),
+            nsub=np.ascontiguousarray(self.nsub, dtype=np.int64),
+            coeffs=_lib.f64(self.coeffs), sp=_lib.f64(self.sp), sn=_lib.f64(self.sn),
+            fold=np.ascontiguousarray(self.fold, dtype=np.uint8),
+            active=np.ascontiguousarray(self.active, dtype=np.uint8),
+        )
+        keep.append(arrs)
+        c = _lib.TdbPsiPack()
+        c.p = self.p
+        c.deg = arrs["coeffs"].shape[2] - 1
+        c.max_nsub = arrs["coeffs"].shape[1]
+        c.delta = float(self.delta)
+        c.lo, c.width = _lib.ptr(arrs["lo"]), _lib.ptr(arrs["width"])
+        c.nsub = _lib.ptr(arrs["nsub"], _lib.C.c_int64)
+        c.coeffs = _lib.ptr(arrs["coeffs"])
+        c.sp, c.sn = _lib.ptr(arrs["sp"]), _lib.ptr(arrs["sn"])
+        c.fold = _lib.ptr(arrs["fold"], _lib.C.c_uint8)
+        c.active = _lib.ptr(arrs["active"], _lib.C.c_uint8)
+        return c
+
+
+def classify_pair(mesh: SurfaceMesh, ex: int, ey: int):
+    """(case, lx, ly): shared vertices first in ascending global order."""
+    if ex == ey:
+        return "coincident", (0, 1, 2), (0, 1, 2)
+    tx = [int(v) for v in mesh.triangles[ex]]
+    ty = [int(v) for v in mesh.triangles[ey]]
+    shared = sorted(set(tx) & set(ty))
+    if not shared:
+        return "regular", (0, 1, 2), (0, 1, 2)
+
+    def lead(t):
+        first = [t.index(g) for g in shared]
+        return tuple(first + [a for a in range(3) if a not in first])
+
+    return ("edge" if len(shared) == 2 else "vertex"), lead(tx), lead(ty)
+
+
+# ---------------------------------------------------------------------------
+# plan: positions grouped into table families
+# ---------------------------------------------------------------------------
+@dataclass
+class Family:
+    kinds: tuple          # (kind_i, kind_k)
+    positions: list       # [(kt, it)] in lag order
+    delta: np.ndarray
+    slo: np.ndarray
+    shi: np.ndarray
+    pack: PsiPack
+
+
+@dataclass
+class AssemblyPlan:
+    grid: TimeGrid
+    families: list
+    where: dict           # (kt, it) -> (family index, s)
+    rules: dict           # case -> (xhat, yhat, w)
+    n_rad: dict           # case -> n_rad used
+
+
+def _touching_tmax(mesh: SurfaceMesh):
+    """Largest corner distance of every touching pair, per case (mesh.py:366-369)."""
+    out = {}
+    for case, (ex, ey, _, _) in touching_pairs(mesh).items():
+        if len(ex) == 0:
+            out[case] = np.zeros(0)
+            continue
+        diff = mesh.corners[ex][:, :, None, :] - mesh.corners[ey][:, None, :, :]
+        out[case] = np.linalg.norm(diff, axis=3).max(axis=(1, 2))
+    return out
+
+
+def build_plan(mesh: SurfaceMesh, grid: TimeGrid, tables: PrototypeTables, positions,
+               config: QuadratureConfig = QuadratureConfig()) -> AssemblyPlan:
+    groups: dict = {}
+    for kt, it in positions:
+        if is_zero_pair(grid, kt, it):
+            continue
+        key = (timestep_kind(grid, it), timestep_kind(grid, kt))
+        groups.setdefault(key, []).append((kt, it))
+    families = []
+    where = {}
+    for key in sorted(groups):
+        pos = groups[key]
+        d = np.array([canonical_origin(grid, it) - canonical_origin(grid, kt) for kt, it in pos])
+        order = np.argsort(-d, kind="stable")
+        pos = [pos[i] for i in order]
+        sup = np.array([psi_support(grid, kt, it) for kt, it in pos]).reshape(-1, 2)
+        slo, shi = sup[:, 0].copy(), sup[:, 1].copy()
+        if np.any(np.diff(slo) < 0) or np.any(np.diff(shi) < 0):
+            raise AssertionError(f"family {key}: supports not monotone in lag order")
+        pack = PsiPack.build(tables, grid, pos[0][0], pos[0][1])
+        if not np.all(pack.active):
+            continue  # unreachable variant (e.g. last/first): identically zero
+        f = len(families)
+        families.append(Family(key, pos, d[order], slo, shi, pack))
+        for s, ktit in enumerate(pos):
+            where[ktit] = (f, s)
+
+    rules = {"regular": pair_rule_regular(config.q_reg)}
+    n_rad = {}
+    tmax = _touching_tmax(mesh) if families else {}
+    all_slo = np.concatenate([f.slo for f in families]) if families else np.zeros(0)
+    for case in CASES[1:]:
+        if config.n_rad is not None:
+            nr = config.n_rad
+        else:
+            tm = tmax.get(case, np.zeros(0))
+            vals = set()
+            # rmax of the case at every position where any pair of it is admissible
+            # (touching pairs have tmin = 0, so admissible iff slo <= tmax)
+            for s in np.unique(all_slo):
+                adm = tm[tm >= s]
+                if len(adm):
+                    vals.add(n_rad_for(float(adm.max()), grid.dt))
+            if len(vals) > 1:
+                raise NotImplementedError(f"{case}: n_rad varies across positions {vals}")
+            nr = vals.pop() if vals else 1
+        n_rad[case] = nr
+        rules[case] = singular_rule(case, config.q_sing, nr, 2 if nr > 1 else 1)
+    return AssemblyPlan(grid, families, where, rules, n_rad)
+
+
+def _mesh_c(mesh: SurfaceMesh, keep: list) -> _lib.TdbMesh:
+    off, ids = mesh.star_csr
+    arrs = dict(
+        corners=_lib.f64(mesh.corners), a2=_lib.f64(2.0 * mesh.areas), normals=_lib.f64(mesh.normals),
+        curls=_lib.f64(mesh.curls), tri=np.ascontiguousarray(mesh.triangles, dtype=np.int64),
+        off=np.ascontiguousarray(off, dtype=np.int64), ids=np.ascontiguousarray(ids, dtype=np.int64),
+    )
+    keep.append(arrs)
+    m = _lib.TdbMesh()
+    m.num_vertices, m.num_triangles = mesh.num_vertices, mesh.num_triangles
+    m.corners, m.a2 = _lib.ptr(arrs["corners"]), _lib.ptr(arrs["a2"])
+    m.normals, m.curls = _lib.ptr(arrs["normals"]), _lib.ptr(arrs["curls"])
+    I64 = _lib.C.c_int64
+    m.triangles = _lib.ptr(arrs["tri"], I64)
+    m.star_off = _lib.ptr(arrs["off"], I64)
+    m.star_ids = _lib.ptr(arrs["ids"], I64)
+    return m
+
+
+class DeviceAssembly:
+    """Owner of a device-resident assembled system (TdbSystem handle)."""
+
+    def __init__(self, mesh: SurfaceMesh, plan: AssemblyPlan, ctx: _lib.Context | None = None):
+        self.mesh = mesh
+        self.plan = plan
+        self.ctx = ctx or _lib.default_context()
+        self.M = mesh.num_vertices
+        self.p = plan.grid.p
+        self.handle = None
+        keep: list = []
+        fams = (_lib.TdbFamily * max(1, len(plan.families)))()
+        for i, f in enumerate(plan.families):
+            arr = dict(delta=_lib.f64(f.delta), slo=_lib.f64(f.slo), shi=_lib.f64(f.shi))
+            keep.append(arr)
+            fams[i].npos = len(f.positions)
+            fams[i].delta, fams[i].slo, fams[i].shi = (_lib.ptr(arr[k]) for k in ("delta", "slo", "shi"))
+            fams[i].pack = f.pack.to_c(keep)
+        desc = _lib.TdbAssemblyDesc()
+        desc.p = self.p
+        desc.num_families = len(plan.families)
+        desc.families = fams
+        for c, case in enumerate(CASES):
+            xh, yh, w = (_lib.f64(a) for a in plan.rules[case])
+            keep.append((xh, yh, w))
+            desc.rules[c].nq = len(w)
+            desc.rules[c].xhat, desc.rules[c].yhat, desc.rules[c].w = _lib.ptr(xh), _lib.ptr(yh), _lib.ptr(w)
+        self.num_families = len(plan.families)
+        if self.num_families == 0:
+            return
+        h = _lib.C.c_void_p()
+        _lib.check(_lib.LIB.tdb_system_assemble(self.ctx.handle, _lib.C.byref(_mesh_c(mesh, keep)),
+                                                _lib.C.byref(desc), _lib.C.byref(h)), "system_assemble")
+        self.handle = h
+
+    def stats(self) -> dict:
+        if self.handle is None:
+            return {}
+        st = _lib.TdbStats()
+        _lib.check(_lib.LIB.tdb_system_stats(self.handle, _lib.C.byref(st)), "system_stats")
+        return st.as_dict()
+
+    def family_arrays(self, f: int):
+        """(indptr (npos*M+1,), indices (nnz,), data (nnz, (p+1)^2)) of family f on the host."""
+        nnz = _lib.C.c_int64()
+        _lib.check(_lib.LIB.tdb_system_family_nnz(self.handle, f, _lib.C.byref(nnz)), "family_nnz")
+        npos = len(self.plan.families[f].positions)
+        indptr = np.empty(npos * self.M + 1, dtype=np.int64)
+        indices = np.empty(max(1, nnz.value), dtype=np.int32)
+        data = np.empty((max(1, nnz.value), (self.p + 1) ** 2))
+        _lib.check(_lib.LIB.tdb_system_copy_family(
+            self.handle, f, _lib.ptr(indptr, _lib.C.c_int64), _lib.ptr(indices, _lib.C.c_int32),
+            _lib.ptr(data)), "copy_family")
+        return indptr, indices[: nnz.value], data[: nnz.value]
+
+    def family_device(self, f: int):
+        a, b, c = _lib.C.c_void_p(), _lib.C.c_void_p(), _lib.C.c_void_p()
+        _lib.check(_lib.LIB.tdb_system_family_device(self.handle, f, _lib.C.byref(a), _lib.C.byref(b),
+                                                     _lib.C.byref(c)), "family_device")
+        return a.value, b.value, c.value
+
+    def position_blocks(self, kt: int, it: int, _cache: dict | None = None):
+        """Nested (p+1) x (p+1) list of scipy CSR blocks of position (kt, it)."""
+        np1 = self.p + 1
+        m = self.M
+        loc = self.plan.where.get((kt, it))
+        if loc is None or self.handle is None:
+            return [[sp.csr_matrix((m, m)) for _ in range(np1)] for _ in range(np1)]
+        f, s = loc
+        if _cache is not None and f in _cache:
+            indptr, indices, data = _cache[f]
+        else:
+            indptr, indices, data = self.family_arrays(f)
+            if _cache is not None:
+                _cache[f] = (indptr, indices, data)
+        lo, hi = indptr[s * m], indptr[(s + 1) * m]
+        ip = indptr[s * m : (s + 1) * m + 1] - lo
+        out = []
+        for m2 in range(np1):
+            row = []
+            for m1 in range(np1):
+                vals = data[lo:hi, m2 * np1 + m1].copy()
+                row.append(sp.csr_matrix((vals, indices[lo:hi].copy(), ip.copy()), shape=(m, m)))
+            out.append(row)
+        return out
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            _lib.LIB.tdb_system_destroy(h)
+            self.handle = None
+
+
+def assemble_subblocks(mesh: SurfaceMesh, grid: TimeGrid, tables: PrototypeTables, kt: int, it: int,
+                       config: QuadratureConfig = QuadratureConfig()):
+    """All (p+1) x (p+1) CSR sub-blocks of block position (kt, it) (device assembly)."""
+    if tables is None:
+        tables = tables_for(grid)
+    plan = build_plan(mesh, grid, tables, [(kt, it)], config)
+    dev = DeviceAssembly(mesh, plan)
+    return dev.position_blocks(kt, it)
+
+
+def assemble_block(mesh, grid, tables, kt, it, m2, m1, config=QuadratureConfig()):
+    return assemble_subblocks(mesh, grid, tables, kt, it, config)[m2][m1]

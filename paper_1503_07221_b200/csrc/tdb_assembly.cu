@@ -1,0 +1,1058 @@
+// All-lags assembly of the canonical block positions (sm_100a, FP64 SIMT).
+//
+// Replaces block_system.assemble_system (/root/reference/pkg/src/tdbem/
+// block_system.py:228-275) and assembly.assemble_subblocks (assembly.py:240-306).
+//
+// Pipeline (one stream, everything device resident):
+//   1. k_plan_pairs     every ordered triangle pair (ex, ey): exact distance
+//                       bounds tmin/tmax (mesh.py:357-391), touching case, and
+//                       per table family the contiguous range of admissible
+//                       positions (assembly.py:167-184 block_pattern test
+//                       tmin <= shi && tmax >= slo).  Nothing E x E on the host.
+//   2. scans            partial-slot base per pair, work-item base per pair.
+//   3. k_quad<P>        one warp per work item = (pair, 256 rule points).  The
+//                       pair's geometry (r, weight) is computed once per point
+//                       and reused for every admissible lag of every family
+//                       ("pair owns all lags"); per lag the in-support points are
+//                       compacted with ballots, the psi/psi~ tables (shared
+//                       memory) are evaluated with Clenshaw and the 10 (p+1)^2
+//                       accumulators S[a][b], s are reduced across the warp.
+//   4. k_sing_finalize  singular pairs span many items: their partials are
+//                       summed in item order (deterministic).
+//   5. k_pattern_*      CTA per (family, test vertex j): the CSR row pattern of
+//                       every position of the family from bitmaps, then each
+//                       entry (j, l) gathers its contributions over
+//                       ey in star(j), ex in star(l) in the reference's canonical
+//                       order (case, ex, ey) with Kahan summation
+//                       (assembly.py:187-214) -> bit-reproducible values.
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "tdb_common.cuh"
+#include "tdb_internal.h"
+
+namespace tdb {
+
+// ---------------------------------------------------------------------------
+// geometry primitives (restating mesh.py:286-354)
+// ---------------------------------------------------------------------------
+struct V3 {
+  double x, y, z;
+};
+__device__ __forceinline__ V3 sub(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+
+__device__ double seg_seg(V3 p0, V3 p1, V3 q0, V3 q1) {
+  V3 d1 = sub(p1, p0), d2 = sub(q1, q0), r = sub(p0, q0);
+  double a = dot(d1, d1), e = dot(d2, d2), b = dot(d1, d2), c = dot(d1, r), f = dot(d2, r);
+  double den = a * e - b * b;
+  double as = a > 0 ? a : 1.0, es = e > 0 ? e : 1.0;
+  double s = den > 0.0 ? clip01((b * f - c * e) / den) : 0.0;
+  double t = (b * s + f) / es;
+  if (t < 0.0) s = clip01(-c / as);
+  else if (t > 1.0) s = clip01((b - c) / as);
+  t = e > 0.0 ? clip01(t) : 0.0;
+  s = a > 0.0 ? s : 0.0;
+  V3 d = {p0.x + s * d1.x - (q0.x + t * d2.x), p0.y + s * d1.y - (q0.y + t * d2.y),
+          p0.z + s * d1.z - (q0.z + t * d2.z)};
+  return sqrt(dot(d, d));
+}
+
+__device__ double pt_seg(V3 p, V3 a, V3 b) {
+  V3 ab = sub(b, a);
+  double den = dot(ab, ab);
+  double t = dot(sub(p, a), ab) / (den > 0 ? den : 1.0);
+  t = den > 0.0 ? clip01(t) : 0.0;
+  V3 d = {p.x - a.x - t * ab.x, p.y - a.y - t * ab.y, p.z - a.z - t * ab.z};
+  return sqrt(dot(d, d));
+}
+
+__device__ double pt_tri(V3 p, V3 v0, V3 v1, V3 v2) {
+  V3 e0 = sub(v1, v0), e1 = sub(v2, v0);
+  V3 n = {e0.y * e1.z - e0.z * e1.y, e0.z * e1.x - e0.x * e1.z, e0.x * e1.y - e0.y * e1.x};
+  double nn = dot(n, n);
+  V3 w = sub(p, v0);
+  double dplane = fabs(dot(w, n)) / sqrt(nn > 0 ? nn : 1.0);
+  double d00 = dot(e0, e0), d01 = dot(e0, e1), d11 = dot(e1, e1), d20 = dot(w, e0), d21 = dot(w, e1);
+  double den = d00 * d11 - d01 * d01;
+  double dens = den > 0 ? den : 1.0;
+  double u = (d11 * d20 - d01 * d21) / dens, v = (d00 * d21 - d01 * d20) / dens;
+  bool inside = u >= 0.0 && v >= 0.0 && u + v <= 1.0 && den > 0.0 && nn > 0.0;
+  if (inside) return dplane;
+  return fmin(fmin(pt_seg(p, v0, v1), pt_seg(p, v1, v2)), pt_seg(p, v2, v0));
+}
+
+__device__ __forceinline__ V3 corner(const double* __restrict__ corners, int e, int a) {
+  const double* c = corners + 9 * (long long)e + 3 * a;
+  return {c[0], c[1], c[2]};
+}
+
+// Touching case of (ex, ey) and the chart permutations (assembly.py:130-152):
+// shared vertices first, in ascending global order; the rest in local order.
+__device__ __forceinline__ int pair_topology(const int* __restrict__ tri, int ex, int ey,
+                                             int lx[3], int ly[3]) {
+  const int tx[3] = {tri[3 * ex], tri[3 * ex + 1], tri[3 * ex + 2]};
+  const int ty[3] = {tri[3 * ey], tri[3 * ey + 1], tri[3 * ey + 2]};
+  lx[0] = 0; lx[1] = 1; lx[2] = 2;
+  ly[0] = 0; ly[1] = 1; ly[2] = 2;
+  if (ex == ey) return TDB_CASE_COINCIDENT;
+  int sh[3], ns = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    bool hit = false;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) hit |= (tx[a] == ty[b]);
+    if (hit) sh[ns++] = tx[a];
+  }
+  if (ns == 0) return TDB_CASE_REGULAR;
+  // sort shared global ids ascending (ns <= 3)
+  for (int i = 1; i < ns; ++i)
+    for (int k = i; k > 0 && sh[k - 1] > sh[k]; --k) {
+      int t = sh[k]; sh[k] = sh[k - 1]; sh[k - 1] = t;
+    }
+  int px = 0, py = 0;
+  bool usedx[3] = {false, false, false}, usedy[3] = {false, false, false};
+  for (int i = 0; i < ns; ++i) {
+    for (int a = 0; a < 3; ++a)
+      if (tx[a] == sh[i]) { lx[px++] = a; usedx[a] = true; }
+    for (int a = 0; a < 3; ++a)
+      if (ty[a] == sh[i]) { ly[py++] = a; usedy[a] = true; }
+  }
+  for (int a = 0; a < 3; ++a) {
+    if (!usedx[a]) lx[px++] = a;
+    if (!usedy[a]) ly[py++] = a;
+  }
+  return ns == 2 ? TDB_CASE_EDGE : TDB_CASE_VERTEX;
+}
+
+__device__ __forceinline__ int shared_count(const int* __restrict__ tri, int ex, int ey) {
+  if (ex == ey) return 3;
+  int n = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) n += (tri[3 * ex + a] == tri[3 * ey + b]);
+  return n;
+}
+
+__device__ __forceinline__ int case_of(const int* __restrict__ tri, int ex, int ey) {
+  if (ex == ey) return TDB_CASE_COINCIDENT;
+  int n = shared_count(tri, ex, ey);
+  return n == 0 ? TDB_CASE_REGULAR : (n == 2 ? TDB_CASE_EDGE : TDB_CASE_VERTEX);
+}
+
+// ---------------------------------------------------------------------------
+// 1. plan: bounds, admissible ranges, unit counts
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int first_geq(const double* __restrict__ a, int n, double v) {
+  int lo = 0, hi = n;  // first index with a[i] >= v
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] >= v) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+__device__ __forceinline__ int last_leq(const double* __restrict__ a, int n, double v) {
+  int lo = 0, hi = n;  // first index with a[i] > v, minus one
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] > v) hi = mid; else lo = mid + 1;
+  }
+  return lo - 1;
+}
+
+struct PlanArgs {
+  int E, F;
+  const double* corners;
+  const int* tri;
+  const FamDev* fams;
+  int nitems_case[4];
+  FRange* frange;           // [F][E*E]
+  int* units;               // [E*E]
+  long long* slots;         // [E*E] -> exclusive scan -> pair_base
+  long long* nitems;        // [E*E] -> exclusive scan -> item_base
+  unsigned char* pcase;     // [E*E]
+};
+
+__global__ void k_plan_pairs(PlanArgs a) {
+  const long long E2 = (long long)a.E * a.E;
+  for (long long P = blockIdx.x * (long long)blockDim.x + threadIdx.x; P < E2;
+       P += (long long)gridDim.x * blockDim.x) {
+    const int ey = (int)(P / a.E), ex = (int)(P % a.E);
+    V3 A[3], B[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      A[k] = corner(a.corners, ex, k);
+      B[k] = corner(a.corners, ey, k);
+    }
+    double dmax = 0.0, dmin = 1e300;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        V3 d = sub(A[i], B[k]);
+        double v = sqrt(dot(d, d));
+        dmax = fmax(dmax, v);
+        dmin = fmin(dmin, v);
+      }
+    const int cs = case_of(a.tri, ex, ey);
+    if (cs != TDB_CASE_REGULAR) {
+      dmin = 0.0;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          dmin = fmin(dmin, seg_seg(A[i], A[(i + 1) % 3], B[k], B[(k + 1) % 3]));
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        dmin = fmin(dmin, pt_tri(A[i], B[0], B[1], B[2]));
+        dmin = fmin(dmin, pt_tri(B[i], A[0], A[1], A[2]));
+      }
+    }
+    int units = 0;
+    for (int f = 0; f < a.F; ++f) {
+      const FamDev& fd = a.fams[f];
+      int s0 = first_geq(fd.shi, fd.npos, dmin);  // shi >= tmin
+      int s1 = last_leq(fd.slo, fd.npos, dmax);   // slo <= tmax
+      int cnt = s1 >= s0 ? s1 - s0 + 1 : 0;
+      FRange fr;
+      fr.foff = units;
+      fr.lo_cnt = (cnt > 0 ? s0 : 0) | (cnt << 16);
+      a.frange[(long long)f * E2 + P] = fr;
+      units += cnt;
+    }
+    a.units[P] = units;
+    a.pcase[P] = (unsigned char)cs;
+    const int ni = units > 0 ? a.nitems_case[cs] : 0;
+    a.slots[P] = (long long)units * ni;
+    a.nitems[P] = ni;
+  }
+}
+
+__global__ void k_fill_items(long long E2, const long long* __restrict__ item_base,
+                             const long long* __restrict__ item_end_excl_next,
+                             const int* __restrict__ units, const unsigned char* __restrict__ pcase,
+                             const int* nitems_case, int2* __restrict__ items) {
+  for (long long P = blockIdx.x * (long long)blockDim.x + threadIdx.x; P < E2;
+       P += (long long)gridDim.x * blockDim.x) {
+    if (units[P] == 0) continue;
+    const int ni = nitems_case[pcase[P]];
+    const long long b = item_base[P];
+    for (int i = 0; i < ni; ++i) items[b + i] = make_int2((int)P, i);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 3. quadrature kernel
+// ---------------------------------------------------------------------------
+struct QuadArgs {
+  int E;
+  int fam_begin, fam_count;
+  const FamDev* fams;
+  const double* blob;      // coefficients of the launch's families, concatenated
+  int blob_doubles;
+  int coef_in_smem;
+  const int* tri;
+  const double* corners;
+  const double* a2;
+  RuleDev rules[4];
+  const int2* items;
+  long long nitems;
+  unsigned long long* work;
+  const FRange* frange;
+  const long long* pair_base;
+  const int* units;
+  double* part;
+  unsigned long long* n_in;
+};
+
+constexpr int kQuadWarps = 16;
+constexpr int kNK = kChunk / 32;
+
+template <int P, bool SMEM_COEF>
+__global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
+  constexpr int NM = (P + 1) * (P + 1);
+  constexpr int NACC = 10 * NM;
+  extern __shared__ __align__(16) double smem[];
+  // layout: [fam descriptors][coef blob][per warp: r[256], c[256], list[256] bytes]
+  FamDev* sfam = reinterpret_cast<FamDev*>(smem);
+  double* sblob = smem + (sizeof(FamDev) * a.fam_count + 7) / 8;
+  double* swarp = sblob + (SMEM_COEF ? a.blob_doubles : 0);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* sr = swarp + wid * (2 * kChunk + kChunk / 8);
+  double* sc = sr + kChunk;
+  unsigned char* slist = reinterpret_cast<unsigned char*>(sc + kChunk);
+
+  {  // stage family descriptors and coefficients
+    const int nwords = (int)((sizeof(FamDev) * a.fam_count + 7) / 8);
+    const double* src = reinterpret_cast<const double*>(a.fams + a.fam_begin);
+    for (int i = threadIdx.x; i < nwords; i += blockDim.x) smem[i] = src[i];
+    if (SMEM_COEF)
+      for (int i = threadIdx.x; i < a.blob_doubles; i += blockDim.x) sblob[i] = a.blob[i];
+    __syncthreads();
+  }
+  const double* coef_base = SMEM_COEF ? sblob : a.blob;
+  const long long E2 = (long long)a.E * a.E;
+  unsigned long long my_in = 0;
+
+  while (true) {
+    long long it;
+    if (lane == 0) it = (long long)atomicAdd(a.work, 1ULL);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= a.nitems) break;
+    const int2 item = a.items[it];
+    const int Pp = item.x, isub = item.y;
+    const int ey = Pp / a.E, ex = Pp % a.E;
+    int lx[3], ly[3];
+    const int cs = pair_topology(a.tri, ex, ey, lx, ly);
+    const RuleDev& R = a.rules[cs];
+    const long long q0 = (long long)isub * kChunk;
+    const int nq = (int)min((long long)kChunk, R.nq - q0);
+    const V3 X0 = corner(a.corners, ex, lx[0]), X1 = corner(a.corners, ex, lx[1]),
+             X2 = corner(a.corners, ex, lx[2]);
+    const V3 Y0 = corner(a.corners, ey, ly[0]), Y1 = corner(a.corners, ey, ly[1]),
+             Y2 = corner(a.corners, ey, ly[2]);
+    const V3 e1 = sub(X1, X0), e2 = sub(X2, X1), f1 = sub(Y1, Y0), f2 = sub(Y2, Y1);
+    const double scale = kInv4Pi * a.a2[ex] * a.a2[ey];
+    double rk[kNK];
+#pragma unroll
+    for (int k = 0; k < kNK; ++k) {
+      const int q = lane + 32 * k;
+      double r = 1e300, c = 0.0;
+      if (q < nq) {
+        const long long g = q0 + q;
+        const double x1 = R.x1[g], x2 = R.x2[g], y1 = R.y1[g], y2 = R.y2[g];
+        const double dx = (X0.x + x1 * e1.x + x2 * e2.x) - (Y0.x + y1 * f1.x + y2 * f2.x);
+        const double dy = (X0.y + x1 * e1.y + x2 * e2.y) - (Y0.y + y1 * f1.y + y2 * f2.y);
+        const double dz = (X0.z + x1 * e1.z + x2 * e2.z) - (Y0.z + y1 * f1.z + y2 * f2.z);
+        r = sqrt(dx * dx + dy * dy + dz * dz);
+        c = scale * R.w[g] / r;
+      }
+      rk[k] = r;
+      sr[q] = r;
+      sc[q] = c;
+    }
+    __syncwarp();
+    const int nunits = a.units[Pp];
+    const long long slot0 = a.pair_base[Pp] + (long long)isub * nunits;
+
+    for (int fi = 0; fi < a.fam_count; ++fi) {
+      const int fglob = a.fam_begin + fi;
+      const FRange fr = a.frange[(long long)fglob * E2 + Pp];
+      const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
+      if (cnt == 0) continue;
+      const FamDev& fd = sfam[fi];
+      const double* cf = coef_base + fd.coeff_off;
+      const int tstride = fd.nsub * (kDeg + 1);
+      for (int si = 0; si < cnt; ++si) {
+        const int s = s_lo + si;
+        const double delta = fd.delta[s];
+        // ballot compaction of the in-support points
+        int total = 0;
+#pragma unroll
+        for (int k = 0; k < kNK; ++k) {
+          const double av = rk[k] + delta;
+          const bool act = (av >= fd.amin) && (av <= fd.amax);
+          const unsigned m = __ballot_sync(0xffffffffu, act);
+          if (act) slist[total + __popc(m & ((1u << lane) - 1u))] = (unsigned char)(lane + 32 * k);
+          total += __popc(m);
+        }
+        __syncwarp();
+        my_in += total;
+        double acc[NACC];
+#pragma unroll
+        for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
+        for (int i = lane; i < total; i += 32) {
+          const int q = slist[i];
+          const double r = sr[q], c = sc[q];
+          const long long g = q0 + q;
+          const double x1 = R.x1[g], x2 = R.x2[g], y1 = R.y1[g], y2 = R.y2[g];
+          const double av = r + delta;
+          const double aa = fd.fold ? fabs(av) : av;
+          double x;
+          const int idx = cheb_locate(aa, fd.lo, fd.w, fd.inv_w, fd.nsub, x);
+          const bool neg = av < 0.0;
+          const double shx0 = 1.0 - x1, shx1 = x1 - x2;
+          const double shy0 = 1.0 - y1, shy1 = y1 - y2;
+#pragma unroll
+          for (int m = 0; m < NM; ++m) {
+            const double* c0 = cf + (2 * m) * tstride + idx * (kDeg + 1);
+            const double* c1 = c0 + tstride;
+            double v0, v1;
+            clenshaw2<kDeg>(c0, c1, x, x, v0, v1);
+            if (fd.fold) {
+              v0 *= neg ? fd.sn[2 * m] : fd.sp[2 * m];
+              v1 *= neg ? fd.sn[2 * m + 1] : fd.sp[2 * m + 1];
+            }
+            const double cp = c * v0;
+            const double u0 = cp * shy0, u1 = cp * shy1, u2 = cp * y2;
+            double* S = acc + 10 * m;
+            S[0] = fma(u0, shx0, S[0]);
+            S[1] = fma(u0, shx1, S[1]);
+            S[2] = fma(u0, x2, S[2]);
+            S[3] = fma(u1, shx0, S[3]);
+            S[4] = fma(u1, shx1, S[4]);
+            S[5] = fma(u1, x2, S[5]);
+            S[6] = fma(u2, shx0, S[6]);
+            S[7] = fma(u2, shx1, S[7]);
+            S[8] = fma(u2, x2, S[8]);
+            S[9] = fma(c, v1, S[9]);
+          }
+        }
+        double outv = 0.0;
+#pragma unroll
+        for (int k = 0; k < NACC; ++k) {
+          const double v = warp_allsum(acc[k]);
+          outv = (lane == (k & 31)) ? v : outv;
+          if ((k & 31) == 31 || k == NACC - 1) {
+            const int kb = k & ~31;
+            if (lane < NACC - kb && lane <= (k & 31))
+              a.part[(slot0 + fr.foff + si) * NACC + kb + lane] = outv;
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+  if (lane == 0) atomicAdd(a.n_in, my_in);
+}
+
+// ---------------------------------------------------------------------------
+// 4. singular pairs: sum item partials into item 0 (item order, deterministic)
+// ---------------------------------------------------------------------------
+__global__ void k_finalize_items(long long E2, const int* __restrict__ units,
+                                 const unsigned char* __restrict__ pcase,
+                                 const long long* __restrict__ pair_base, const int* nitems_case,
+                                 int nacc, double* __restrict__ part) {
+  for (long long Pp = blockIdx.x; Pp < E2; Pp += gridDim.x) {
+    const int ni = nitems_case[pcase[Pp]];
+    const int U = units[Pp];
+    if (ni <= 1 || U == 0) continue;
+    const long long base = pair_base[Pp];
+    const int n = U * nacc;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      double s = 0.0;
+      for (int i = 0; i < ni; ++i) s += part[(base + (long long)i * U) * nacc + t];
+      part[base * nacc + t] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 5. CSR pattern (bitmaps) and compensated gather of the values
+// ---------------------------------------------------------------------------
+struct PatternArgs {
+  int E, M, f, npos;
+  int s_begin, s_count;   // position chunk handled by this launch
+  int words;              // ceil(M / 32)
+  const int* tri;
+  const int* star_off;
+  const int* star_ids;
+  const FRange* frange;   // this family's slice [E*E]
+  long long* row_count;   // [npos * M]
+  // fill phase
+  const int64_t* indptr;
+  int32_t* indices;
+  double* data;
+  const long long* pair_base;
+  const double* part;
+  const double* normals;
+  const double* curls;
+  int nacc, nm;
+};
+
+__device__ void build_bitmaps(const PatternArgs& a, int j, unsigned* bm) {
+  const int nwords = a.s_count * a.words;
+  for (int i = threadIdx.x; i < nwords; i += blockDim.x) bm[i] = 0u;
+  __syncthreads();
+  const long long E2 = (long long)a.E * a.E;
+  (void)E2;
+  for (int k = a.star_off[j]; k < a.star_off[j + 1]; ++k) {
+    const int ey = a.star_ids[k];
+    const FRange* row = a.frange + (long long)ey * a.E;
+    for (int ex = threadIdx.x; ex < a.E; ex += blockDim.x) {
+      const FRange fr = row[ex];
+      const int cnt = fr.lo_cnt >> 16;
+      if (cnt == 0) continue;
+      const int s_lo = fr.lo_cnt & 0xffff;
+      const int lo = max(s_lo, a.s_begin), hi = min(s_lo + cnt, a.s_begin + a.s_count);
+      if (lo >= hi) continue;
+      const int l0 = a.tri[3 * ex], l1 = a.tri[3 * ex + 1], l2 = a.tri[3 * ex + 2];
+      for (int s = lo; s < hi; ++s) {
+        unsigned* b = bm + (s - a.s_begin) * a.words;
+        atomicOr(b + (l0 >> 5), 1u << (l0 & 31));
+        atomicOr(b + (l1 >> 5), 1u << (l1 & 31));
+        atomicOr(b + (l2 >> 5), 1u << (l2 & 31));
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void k_pattern_count(PatternArgs a) {
+  extern __shared__ unsigned bm[];
+  const int j = blockIdx.x;
+  build_bitmaps(a, j, bm);
+  __shared__ int red[32];
+  for (int sl = 0; sl < a.s_count; ++sl) {
+    int c = 0;
+    for (int w = threadIdx.x; w < a.words; w += blockDim.x) c += __popc(bm[sl * a.words + w]);
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+      a.row_count[(long long)(a.s_begin + sl) * a.M + j] = t;
+    }
+    __syncthreads();
+  }
+}
+
+template <int NM>
+__device__ void gather_entry(const PatternArgs& a, int s, int j, int l, double* out) {
+  double sum[NM], comp[NM];
+#pragma unroll
+  for (int m = 0; m < NM; ++m) sum[m] = comp[m] = 0.0;
+  const long long E2 = (long long)a.E * a.E;
+  (void)E2;
+  const int jb = a.star_off[j], je = a.star_off[j + 1];
+  const int lb = a.star_off[l], le = a.star_off[l + 1];
+  for (int cr = 0; cr < 4; ++cr) {
+    for (int kx = lb; kx < le; ++kx) {
+      const int ex = a.star_ids[kx];
+      for (int ky = jb; ky < je; ++ky) {
+        const int ey = a.star_ids[ky];
+        if (case_of(a.tri, ex, ey) != cr) continue;
+        const long long Pp = (long long)ey * a.E + ex;
+        const FRange fr = a.frange[Pp];
+        const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
+        if (s < s_lo || s >= s_lo + cnt) continue;
+        const long long slot = a.pair_base[Pp] + fr.foff + (s - s_lo);
+        int lx[3], ly[3];
+        pair_topology(a.tri, ex, ey, lx, ly);
+        int pj = 0, pl = 0;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          pj = (a.tri[3 * ey + t] == j) ? t : pj;
+          pl = (a.tri[3 * ex + t] == l) ? t : pl;
+        }
+        int ca = 0, cb = 0;  // chart positions: tri[ly[ca]] == j
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          ca = (ly[t] == pj) ? t : ca;
+          cb = (lx[t] == pl) ? t : cb;
+        }
+        const double* nx = a.normals + 3 * (long long)ex;
+        const double* ny = a.normals + 3 * (long long)ey;
+        const double nd = nx[0] * ny[0] + nx[1] * ny[1] + nx[2] * ny[2];
+        const double* cyv = a.curls + 9 * (long long)ey + 3 * pj;
+        const double* cxv = a.curls + 9 * (long long)ex + 3 * pl;
+        const double cd = cyv[0] * cxv[0] + cyv[1] * cxv[1] + cyv[2] * cxv[2];
+        const double* pv = a.part + slot * a.nacc;
+#pragma unroll
+        for (int m = 0; m < NM; ++m) {
+          const double v = nd * pv[10 * m + 3 * ca + cb] + cd * pv[10 * m + 9];
+          const double y = v - comp[m];
+          const double t = sum[m] + y;
+          comp[m] = (t - sum[m]) - y;
+          sum[m] = t;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < NM; ++m) out[m] = sum[m];
+}
+
+template <int NM>
+__global__ void k_pattern_fill(PatternArgs a) {
+  extern __shared__ unsigned smem_u[];
+  unsigned* bm = smem_u;
+  int* pref = reinterpret_cast<int*>(smem_u + a.s_count * a.words);  // words + 1
+  const int j = blockIdx.x;
+  build_bitmaps(a, j, bm);
+  typedef cub::BlockScan<int, 256> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  for (int sl = 0; sl < a.s_count; ++sl) {
+    const unsigned* b = bm + sl * a.words;
+    const long long row = (long long)(a.s_begin + sl) * a.M + j;
+    const int64_t base = a.indptr[row];
+    // exclusive prefix of popcounts over words (chunks of 256 words)
+    int carry = 0;
+    for (int w0 = 0; w0 < a.words; w0 += 256) {
+      const int w = w0 + threadIdx.x;
+      int c = w < a.words ? __popc(b[w]) : 0, ex;
+      int agg;
+      Scan(tmp).ExclusiveSum(c, ex, agg);
+      if (w < a.words) pref[w] = carry + ex;
+      carry += agg;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) pref[a.words] = carry;
+    __syncthreads();
+    const int nrow = carry;
+    for (int e = threadIdx.x; e < nrow; e += blockDim.x) {
+      int lo = 0, hi = a.words - 1;  // last word with pref[w] <= e
+      while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (pref[mid] <= e) lo = mid; else hi = mid - 1;
+      }
+      unsigned word = b[lo];
+      int rank = e - pref[lo];
+      for (int r = 0; r < rank; ++r) word &= word - 1;
+      const int l = lo * 32 + (__ffs(word) - 1);
+      double vals[NM];
+      gather_entry<NM>(a, a.s_begin + sl, j, l, vals);
+      a.indices[base + e] = l;
+#pragma unroll
+      for (int m = 0; m < NM; ++m) a.data[(base + e) * NM + m] = vals[m];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace tdb
+
+// ===========================================================================
+// host orchestration
+// ===========================================================================
+using namespace tdb;
+
+namespace {
+
+struct Dev {
+  void* p = nullptr;
+  ~Dev() {
+    if (p) cudaFree(p);
+  }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+template <typename T>
+int dalloc(T** out, size_t n) {
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(out), n * sizeof(T));
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaMalloc(") + std::to_string(n * sizeof(T)) + " B): " +
+              cudaGetErrorString(e));
+    return TDB_E_NOMEM;
+  }
+  return TDB_OK;
+}
+
+template <typename T>
+int dupload(T** out, const T* host, size_t n, cudaStream_t st) {
+  int rc = dalloc(out, n);
+  if (rc) return rc;
+  if (n) TDB_CUDA_CHECK(cudaMemcpyAsync(*out, host, n * sizeof(T), cudaMemcpyHostToDevice, st));
+  return TDB_OK;
+}
+
+template <typename T>
+int dalloc_dev(Dev& d, size_t n) {
+  T* p = nullptr;
+  int rc = dalloc(&p, n);
+  d.p = p;
+  return rc;
+}
+
+int exclusive_scan_ll(long long* data, long long n, long long* total, cudaStream_t st) {
+  size_t tmp_bytes = 0;
+  TDB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, data, data, (int64_t)n, st));
+  Dev tmp;
+  int rc = dalloc_dev<char>(tmp, tmp_bytes);
+  if (rc) return rc;
+  long long last = 0;
+  TDB_CUDA_CHECK(cudaMemcpyAsync(&last, data + n - 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  TDB_CUDA_CHECK(cudaStreamSynchronize(st));
+  TDB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, data, data, (int64_t)n, st));
+  long long lastex = 0;
+  TDB_CUDA_CHECK(cudaMemcpyAsync(&lastex, data + n - 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  TDB_CUDA_CHECK(cudaStreamSynchronize(st));
+  *total = lastex + last;
+  return TDB_OK;
+}
+
+struct Timer {
+  cudaEvent_t a, b;
+  Timer() {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+  }
+  ~Timer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+template <int P>
+int launch_quad(const QuadArgs& qa, size_t smem, bool in_smem, int grid, cudaStream_t st) {
+  if (in_smem) {
+    TDB_CUDA_CHECK(cudaFuncSetAttribute(k_quad<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    k_quad<P, true><<<grid, kQuadWarps * 32, smem, st>>>(qa);
+  } else {
+    TDB_CUDA_CHECK(cudaFuncSetAttribute(k_quad<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    k_quad<P, false><<<grid, kQuadWarps * 32, smem, st>>>(qa);
+  }
+  TDB_CUDA_CHECK(cudaGetLastError());
+  return TDB_OK;
+}
+
+template <int NM>
+int launch_fill(const PatternArgs& pa, size_t smem, cudaStream_t st) {
+  TDB_CUDA_CHECK(cudaFuncSetAttribute(k_pattern_fill<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  k_pattern_fill<NM><<<pa.M, 256, smem, st>>>(pa);
+  TDB_CUDA_CHECK(cudaGetLastError());
+  return TDB_OK;
+}
+
+}  // namespace
+
+int tdb_assemble_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDesc* desc,
+                      TdbSystem* sys) {
+  cudaStream_t st = ctx->stream;
+  const int p = desc->p;
+  TDB_REQUIRE(p >= 0 && p <= 3, "assemble: p must be in 0..3");
+  TDB_REQUIRE(desc->num_families >= 1 && desc->num_families <= kMaxFamilies, "assemble: bad family count");
+  const long long E = mesh->num_triangles, V = mesh->num_vertices;
+  TDB_REQUIRE(E >= 1 && E <= 46340, "assemble: triangle count out of range for the E^2 plan");
+  sys->p = p;
+  sys->np1 = p + 1;
+  sys->nm = (p + 1) * (p + 1);
+  sys->nacc = 10 * sys->nm;
+  sys->F = desc->num_families;
+  sys->E = E;
+  sys->V = V;
+  const int F = sys->F, NM = sys->nm, NACC = sys->nacc;
+  const int nt = 2 * NM;
+  Timer t0, t1, t2, t3, t4;
+  TDB_CUDA_CHECK(cudaEventRecord(t0.a, st));
+
+  // ---- mesh upload (int32 topology) ----
+  std::vector<int> tri32(3 * E), soff(V + 1), sids(3 * E);
+  for (long long i = 0; i < 3 * E; ++i) tri32[i] = (int)mesh->triangles[i];
+  for (long long i = 0; i <= V; ++i) soff[i] = (int)mesh->star_off[i];
+  for (long long i = 0; i < 3 * E; ++i) sids[i] = (int)mesh->star_ids[i];
+  int rc;
+  if ((rc = dupload(&sys->corners, mesh->corners, 9 * E, st))) return rc;
+  if ((rc = dupload(&sys->a2, mesh->a2, E, st))) return rc;
+  if ((rc = dupload(&sys->normals, mesh->normals, 3 * E, st))) return rc;
+  if ((rc = dupload(&sys->curls, mesh->curls, 9 * E, st))) return rc;
+  if ((rc = dupload(&sys->tri, tri32.data(), 3 * E, st))) return rc;
+  if ((rc = dupload(&sys->star_off, soff.data(), V + 1, st))) return rc;
+  if ((rc = dupload(&sys->star_ids, sids.data(), 3 * E, st))) return rc;
+
+  // ---- families ----
+  sys->fam.resize(F);
+  sys->famdev_host.resize(F);
+  std::vector<double> blob_all;
+  std::vector<int> fam_blob_off(F), fam_blob_len(F);
+  for (int f = 0; f < F; ++f) {
+    const TdbFamily& hf = desc->families[f];
+    const TdbPsiPack& pk = hf.pack;
+    TDB_REQUIRE(pk.p == p, "family pack p mismatch");
+    TDB_REQUIRE(pk.deg == kDeg, "assemble: tables must have Chebyshev degree 16");
+    TDB_REQUIRE(hf.npos >= 1 && hf.npos < 32768, "family position count out of range");
+    FamDev fd{};
+    fd.npos = hf.npos;
+    fd.nt = nt;
+    fd.nsub = (int)pk.nsub[0];
+    fd.fold = pk.fold[0];
+    fd.lo = pk.lo[0];
+    fd.w = pk.width[0];
+    fd.inv_w = 1.0 / pk.width[0];
+    for (int t = 0; t < nt; ++t) {
+      TDB_REQUIRE(pk.active[t] == 1, "assemble: inactive table inside a family");
+      TDB_REQUIRE(pk.nsub[t] == fd.nsub && pk.fold[t] == fd.fold && pk.lo[t] == fd.lo &&
+                      pk.width[t] == fd.w,
+                  "assemble: tables of one family must share their domain");
+      fd.sp[t] = pk.sp[t];
+      fd.sn[t] = pk.sn[t];
+    }
+    const double thi = fd.lo + fd.nsub * fd.w;
+    fd.amin = fd.fold ? -thi : fd.lo;
+    fd.amax = thi;
+    for (int s = 1; s < hf.npos; ++s)
+      TDB_REQUIRE(hf.slo[s] >= hf.slo[s - 1] && hf.shi[s] >= hf.shi[s - 1],
+                  "assemble: family positions must be in lag order (slo, shi non-decreasing)");
+    FamilyStore& fs = sys->fam[f];
+    fs.npos = hf.npos;
+    if ((rc = dupload(&fs.delta, hf.delta, hf.npos, st))) return rc;
+    if ((rc = dupload(&fs.slo, hf.slo, hf.npos, st))) return rc;
+    if ((rc = dupload(&fs.shi, hf.shi, hf.npos, st))) return rc;
+    // compact (nt, nsub, deg+1) copy (pack stride is max_nsub)
+    const int len = nt * fd.nsub * (kDeg + 1);
+    fam_blob_off[f] = (int)blob_all.size();
+    fam_blob_len[f] = len;
+    for (int t = 0; t < nt; ++t)
+      for (int k = 0; k < fd.nsub; ++k)
+        for (int c = 0; c <= kDeg; ++c)
+          blob_all.push_back(pk.coeffs[((size_t)t * pk.max_nsub + k) * (kDeg + 1) + c]);
+    fd.delta = fs.delta;
+    fd.slo = fs.slo;
+    fd.shi = fs.shi;
+    sys->famdev_host[f] = fd;
+  }
+  double* d_blob = nullptr;
+  if ((rc = dupload(&d_blob, blob_all.data(), blob_all.size(), st))) return rc;
+  Dev blob_guard;
+  blob_guard.p = d_blob;
+  for (int f = 0; f < F; ++f) sys->famdev_host[f].coeffs = d_blob + fam_blob_off[f];
+
+  // ---- rules ----
+  RuleDev rules[4];
+  std::vector<Dev> rule_mem(20);
+  int nitems_case[4];
+  for (int c = 0; c < 4; ++c) {
+    const TdbRule& r = desc->rules[c];
+    TDB_REQUIRE(r.nq >= 1 || c != TDB_CASE_REGULAR, "assemble: regular rule missing");
+    rules[c].nq = r.nq;
+    rules[c].nitems = (int)((r.nq + kChunk - 1) / kChunk);
+    nitems_case[c] = std::max(1, rules[c].nitems);
+    std::vector<double> x1(r.nq), x2(r.nq), y1(r.nq), y2(r.nq);
+    for (long long q = 0; q < r.nq; ++q) {
+      x1[q] = r.xhat[2 * q];
+      x2[q] = r.xhat[2 * q + 1];
+      y1[q] = r.yhat[2 * q];
+      y2[q] = r.yhat[2 * q + 1];
+    }
+    double* ptrs[5];
+    const double* src[5] = {x1.data(), x2.data(), y1.data(), y2.data(), r.w};
+    for (int k = 0; k < 5; ++k) {
+      if ((rc = dupload(&ptrs[k], src[k], (size_t)std::max<long long>(r.nq, 1) * (r.nq > 0), st)))
+        return rc;
+      rule_mem[5 * c + k].p = ptrs[k];
+    }
+    rules[c].x1 = ptrs[0];
+    rules[c].x2 = ptrs[1];
+    rules[c].y1 = ptrs[2];
+    rules[c].y2 = ptrs[3];
+    rules[c].w = ptrs[4];
+  }
+
+  if ((rc = dupload(&sys->famdev, sys->famdev_host.data(), F, st))) return rc;
+  int* d_nitems_case = nullptr;
+  if ((rc = dupload(&d_nitems_case, nitems_case, 4, st))) return rc;
+  Dev nic_guard;
+  nic_guard.p = d_nitems_case;
+
+  // ---- 1. plan ----
+  const long long E2 = E * E;
+  Dev d_frange, d_units, d_slots, d_nitems, d_pcase;
+  if ((rc = dalloc_dev<FRange>(d_frange, (size_t)F * E2))) return rc;
+  if ((rc = dalloc_dev<int>(d_units, E2))) return rc;
+  if ((rc = dalloc_dev<long long>(d_slots, E2))) return rc;
+  if ((rc = dalloc_dev<long long>(d_nitems, E2))) return rc;
+  if ((rc = dalloc_dev<unsigned char>(d_pcase, E2))) return rc;
+  PlanArgs pa;
+  pa.E = (int)E;
+  pa.F = F;
+  pa.corners = sys->corners;
+  pa.tri = sys->tri;
+  pa.fams = sys->famdev;
+  for (int c = 0; c < 4; ++c) pa.nitems_case[c] = nitems_case[c];
+  pa.frange = d_frange.as<FRange>();
+  pa.units = d_units.as<int>();
+  pa.slots = d_slots.as<long long>();
+  pa.nitems = d_nitems.as<long long>();
+  pa.pcase = d_pcase.as<unsigned char>();
+  {
+    long long blocks = std::min<long long>((E2 + 255) / 256, 148LL * 32);
+    k_plan_pairs<<<(int)blocks, 256, 0, st>>>(pa);
+    TDB_CUDA_CHECK(cudaGetLastError());
+  }
+  long long total_slots = 0, total_items = 0;
+  if ((rc = exclusive_scan_ll(d_slots.as<long long>(), E2, &total_slots, st))) return rc;
+  if ((rc = exclusive_scan_ll(d_nitems.as<long long>(), E2, &total_items, st))) return rc;
+  Dev d_items;
+  if ((rc = dalloc_dev<int2>(d_items, total_items))) return rc;
+  {
+    long long blocks = std::min<long long>((E2 + 255) / 256, 148LL * 32);
+    k_fill_items<<<(int)blocks, 256, 0, st>>>(E2, d_nitems.as<long long>(), nullptr,
+                                              d_units.as<int>(), d_pcase.as<unsigned char>(),
+                                              d_nitems_case, d_items.as<int2>());
+    TDB_CUDA_CHECK(cudaGetLastError());
+  }
+  TDB_CUDA_CHECK(cudaEventRecord(t0.b, st));
+
+  // ---- 3. quadrature ----
+  Dev d_part, d_counters;
+  if ((rc = dalloc_dev<double>(d_part, (size_t)total_slots * NACC))) return rc;
+  if ((rc = dalloc_dev<unsigned long long>(d_counters, 16))) return rc;
+  TDB_CUDA_CHECK(cudaMemsetAsync(d_counters.p, 0, 16 * sizeof(unsigned long long), st));
+  int max_smem = 0;
+  TDB_CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  const size_t warp_bytes = (size_t)kQuadWarps * (2 * kChunk * 8 + kChunk);
+  const size_t budget = (size_t)max_smem - warp_bytes - sizeof(FamDev) * kMaxFamilies - 64;
+  TDB_CUDA_CHECK(cudaEventRecord(t1.a, st));
+  int nlaunch = 0;
+  for (int f0 = 0; f0 < F;) {
+    // greedy grouping of consecutive families whose coefficients fit in smem
+    size_t bytes = 0;
+    int f1 = f0;
+    while (f1 < F && bytes + (size_t)fam_blob_len[f1] * 8 <= budget) bytes += (size_t)fam_blob_len[f1++] * 8;
+    const bool in_smem = f1 > f0;
+    if (!in_smem) f1 = f0 + 1;  // single oversized family: coefficients from global/L1
+    for (int f = f0; f < f1; ++f)
+      sys->famdev_host[f].coeff_off = fam_blob_off[f] - fam_blob_off[f0];
+    TDB_CUDA_CHECK(cudaMemcpyAsync(sys->famdev + f0, sys->famdev_host.data() + f0,
+                                   sizeof(FamDev) * (f1 - f0), cudaMemcpyHostToDevice, st));
+    QuadArgs qa;
+    qa.E = (int)E;
+    qa.fam_begin = f0;
+    qa.fam_count = f1 - f0;
+    qa.fams = sys->famdev;
+    qa.blob = d_blob + fam_blob_off[f0];
+    qa.blob_doubles = (int)(in_smem ? bytes / 8 : 0);
+    qa.coef_in_smem = in_smem;
+    qa.tri = sys->tri;
+    qa.corners = sys->corners;
+    qa.a2 = sys->a2;
+    for (int c = 0; c < 4; ++c) qa.rules[c] = rules[c];
+    qa.items = d_items.as<int2>();
+    qa.nitems = total_items;
+    qa.work = d_counters.as<unsigned long long>() + 1 + nlaunch % 8;
+    qa.frange = d_frange.as<FRange>();
+    qa.pair_base = d_slots.as<long long>();
+    qa.units = d_units.as<int>();
+    qa.part = d_part.as<double>();
+    qa.n_in = d_counters.as<unsigned long long>();
+    const size_t smem = ((sizeof(FamDev) * (f1 - f0) + 7) / 8) * 8 + (in_smem ? bytes : 0) + warp_bytes;
+    const int grid = ctx->num_sms;
+    switch (p) {
+      case 0: rc = launch_quad<0>(qa, smem, in_smem, grid, st); break;
+      case 1: rc = launch_quad<1>(qa, smem, in_smem, grid, st); break;
+      case 2: rc = launch_quad<2>(qa, smem, in_smem, grid, st); break;
+      default: rc = launch_quad<3>(qa, smem, in_smem, grid, st); break;
+    }
+    if (rc) return rc;
+    ++nlaunch;
+    f0 = f1;
+    if (nlaunch % 8 == 0)
+      TDB_CUDA_CHECK(cudaMemsetAsync(d_counters.as<unsigned long long>() + 1, 0, 8 * 8, st));
+  }
+  TDB_CUDA_CHECK(cudaEventRecord(t1.b, st));
+
+  // ---- 4. singular finalize ----
+  TDB_CUDA_CHECK(cudaEventRecord(t2.a, st));
+  {
+    bool multi = false;
+    for (int c = 0; c < 4; ++c) multi |= nitems_case[c] > 1;
+    if (multi) {
+      k_finalize_items<<<148 * 16, 256, 0, st>>>(E2, d_units.as<int>(), d_pcase.as<unsigned char>(),
+                                                 d_slots.as<long long>(), d_nitems_case, NACC,
+                                                 d_part.as<double>());
+      TDB_CUDA_CHECK(cudaGetLastError());
+    }
+  }
+  TDB_CUDA_CHECK(cudaEventRecord(t2.b, st));
+
+  // ---- 5. pattern + gather per family ----
+  TDB_CUDA_CHECK(cudaEventRecord(t3.a, st));
+  const int words = (int)((V + 31) / 32);
+  long long nnz_total = 0;
+  for (int f = 0; f < F; ++f) {
+    FamilyStore& fs = sys->fam[f];
+    const int npos = fs.npos;
+    const long long nrows = (long long)npos * V;
+    Dev d_cnt;
+    if ((rc = dalloc_dev<long long>(d_cnt, nrows + 1))) return rc;
+    PatternArgs ga{};
+    ga.E = (int)E;
+    ga.M = (int)V;
+    ga.f = f;
+    ga.npos = npos;
+    ga.words = words;
+    ga.tri = sys->tri;
+    ga.star_off = sys->star_off;
+    ga.star_ids = sys->star_ids;
+    ga.frange = d_frange.as<FRange>() + (long long)f * E2;
+    ga.row_count = d_cnt.as<long long>();
+    ga.pair_base = d_slots.as<long long>();
+    ga.part = d_part.as<double>();
+    ga.normals = sys->normals;
+    ga.curls = sys->curls;
+    ga.nacc = NACC;
+    ga.nm = NM;
+    const size_t bm_budget = 96 * 1024;
+    const int s_chunk = std::max(1, (int)std::min<long long>(npos, (long long)(bm_budget / (words * 4))));
+    for (int s0 = 0; s0 < npos; s0 += s_chunk) {
+      ga.s_begin = s0;
+      ga.s_count = std::min(s_chunk, npos - s0);
+      const size_t smem = (size_t)ga.s_count * words * 4;
+      TDB_CUDA_CHECK(cudaFuncSetAttribute(k_pattern_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+      k_pattern_count<<<(int)V, 256, smem, st>>>(ga);
+      TDB_CUDA_CHECK(cudaGetLastError());
+    }
+    TDB_CUDA_CHECK(cudaMemsetAsync(d_cnt.as<long long>() + nrows, 0, sizeof(long long), st));
+    long long nnz = 0;
+    if ((rc = exclusive_scan_ll(d_cnt.as<long long>(), nrows + 1, &nnz, st))) return rc;
+    fs.nnz = nnz;
+    nnz_total += nnz;
+    fs.indptr = reinterpret_cast<int64_t*>(d_cnt.p);
+    d_cnt.p = nullptr;  // ownership moves to the family store
+    if ((rc = dalloc(&fs.indices, nnz))) return rc;
+    if ((rc = dalloc(&fs.data, (size_t)nnz * NM))) return rc;
+    ga.indptr = fs.indptr;
+    ga.indices = fs.indices;
+    ga.data = fs.data;
+    for (int s0 = 0; s0 < npos; s0 += s_chunk) {
+      ga.s_begin = s0;
+      ga.s_count = std::min(s_chunk, npos - s0);
+      const size_t smem = (size_t)ga.s_count * words * 4 + (words + 1) * 4;
+      switch (NM) {
+        case 1: rc = launch_fill<1>(ga, smem, st); break;
+        case 4: rc = launch_fill<4>(ga, smem, st); break;
+        case 9: rc = launch_fill<9>(ga, smem, st); break;
+        default: rc = launch_fill<16>(ga, smem, st); break;
+      }
+      if (rc) return rc;
+    }
+  }
+  TDB_CUDA_CHECK(cudaEventRecord(t3.b, st));
+  TDB_CUDA_CHECK(cudaStreamSynchronize(st));
+
+  unsigned long long n_in = 0;
+  TDB_CUDA_CHECK(cudaMemcpy(&n_in, d_counters.p, sizeof(n_in), cudaMemcpyDeviceToHost));
+  // units = sum over pairs (count on the host side from scans: slots minus singular items)
+  long long units = 0;
+  {
+    Dev d_tmp;
+    size_t tb = 0;
+    TDB_CUDA_CHECK(cub::DeviceReduce::Sum(nullptr, tb, d_units.as<int>(), (long long*)nullptr, (int64_t)E2, st));
+    if ((rc = dalloc_dev<char>(d_tmp, tb + 16))) return rc;
+    long long* d_sum = reinterpret_cast<long long*>(static_cast<char*>(d_tmp.p) + ((tb + 7) / 8) * 8);
+    TDB_CUDA_CHECK(cub::DeviceReduce::Sum(d_tmp.p, tb, d_units.as<int>(), d_sum, (int64_t)E2, st));
+    TDB_CUDA_CHECK(cudaMemcpyAsync(&units, d_sum, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    TDB_CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+  sys->stats.units = units;
+  sys->stats.items = total_items;
+  sys->stats.n_in = (int64_t)n_in;
+  sys->stats.nnz_total = nnz_total;
+  sys->stats.ms_plan = elapsed(t0.a, t0.b);
+  sys->stats.ms_quad = elapsed(t1.a, t1.b);
+  sys->stats.ms_finalize = elapsed(t2.a, t2.b);
+  sys->stats.ms_pattern = elapsed(t3.a, t3.b);
+  sys->stats.ms_total = elapsed(t0.a, t3.b);
+  sys->famdev_host.clear();
+  return TDB_OK;
+}

@@ -1,0 +1,87 @@
+// Internal (non-ABI) structures shared by the CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/tdb.h"
+
+namespace tdb {
+
+constexpr int kMaxTables = 32;   // nt = 2 (p+1)^2, p <= 3
+constexpr int kMaxFamilies = 16;
+constexpr int kDeg = 16;         // Chebyshev degree of the fast path (PrototypeTables default)
+constexpr int kChunk = 256;      // rule points per warp work item
+
+// One table family on the device (all tables share domain/nsub/fold).
+struct FamDev {
+  int npos, nsub, nt, fold;
+  int coeff_off;   // offset (doubles) of this family's coefficients in the launch blob
+  int pad_;
+  double lo, w, inv_w, amin, amax;
+  double sp[kMaxTables], sn[kMaxTables];
+  const double* delta;
+  const double* slo;
+  const double* shi;
+  const double* coeffs;  // (nt, nsub, kDeg+1) global copy
+};
+
+struct RuleDev {
+  long long nq;
+  int nitems;  // ceil(nq / kChunk)
+  int pad_;
+  const double* x1;
+  const double* x2;
+  const double* y1;
+  const double* y2;
+  const double* w;
+};
+
+// Admissible position range of one (family, pair): s in [s_lo, s_lo + cnt),
+// partial-slot offset foff within the pair.
+struct FRange {
+  int foff;
+  int lo_cnt;  // s_lo | (cnt << 16)
+};
+
+struct FamilyStore {
+  int npos = 0;
+  long long nnz = 0;
+  int64_t* indptr = nullptr;   // npos * M + 1
+  int32_t* indices = nullptr;  // nnz
+  double* data = nullptr;      // nnz * (p+1)^2
+  // device copies of the position tables
+  double* delta = nullptr;
+  double* slo = nullptr;
+  double* shi = nullptr;
+  double* coeffs = nullptr;
+};
+
+}  // namespace tdb
+
+struct TdbContext {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+};
+
+struct TdbSystem {
+  TdbContext* ctx = nullptr;
+  int p = 0, np1 = 1, nm = 1, nacc = 10, F = 0;
+  long long E = 0, V = 0;
+  // mesh
+  double* corners = nullptr;
+  double* a2 = nullptr;
+  double* normals = nullptr;
+  double* curls = nullptr;
+  int* tri = nullptr;
+  int* star_off = nullptr;
+  int* star_ids = nullptr;
+  // families
+  std::vector<tdb::FamilyStore> fam;
+  std::vector<tdb::FamDev> famdev_host;
+  tdb::FamDev* famdev = nullptr;
+  TdbStats stats{};
+};

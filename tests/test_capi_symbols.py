@@ -1,0 +1,35 @@
+"""The C-ABI library loads on a CPU host and exports every symbol include/tdb.h declares."""
+
+import ctypes
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared():
+    src = open(os.path.join(ROOT, "include", "tdb.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(tdb_\w+)\s*\(", src, re.M)))
+
+
+def test_header_symbols_exported():
+    from paper_1503_07221_b200 import _lib
+
+    names = declared()
+    assert len(names) >= 15
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(names) == set(_lib.EXPORTED)
+    assert _lib.LIB.tdb_abi_version() == 1
+
+
+def test_no_device_errors_are_loud():
+    from paper_1503_07221_b200 import _lib
+
+    if _lib.device_count() > 0:
+        return
+    import pytest
+
+    with pytest.raises(RuntimeError):
+        _lib.Context(0)
