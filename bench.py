@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark: lag-block assembly throughput (triangle-pair x lag quadratures/s) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], the metric's single-GPU configuration):
+icosphere refined 3x (1280 triangles, 642 P1 dofs), dt = 0.05, N = 80, p = 0,
+reference quadrature rules (q_reg 4, q_sing 5, n_rad auto).  A "step" is one
+complete assembly of every canonical block position (pair plan with exact
+distance bounds, all-lags quadrature, singular reduction, CSR pattern and
+compensated gather) from device-resident mesh/tables.  `value` = units / s,
+units = admissible (triangle pair, block position) quadratures.  `e2e` is the
+same metric through the public API (assemble_system from host arrays, all
+blocks copied back to host as CSR).
+
+N > 1 (torchrun, one process per GPU): every rank assembles the full system
+(replicas, weak scaling); times are the max over ranks.  --impl reference
+times the reference's own compiled kernel (oracle/_ref) on the host cores on a
+stratified sample of the same workload (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "assembly triangle-pair x lag quadratures/s"
+UNIT = "units/s"
+
+
+def flops_per_launch(st, p):
+    """ALGORITHMIC FP64 flops of the quadrature kernel:
+    36 per geometry point + (1 + 160 (p+1)^2) per in-support (unit, point) evaluation."""
+    return 36.0 * st["n_geom"] + (1.0 + 160.0 * (p + 1) ** 2) * st["n_in"]
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join("/tmp", f"tdb_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if os.environ.get("TDB_BENCH_BACKEND", "nccl") == "nccl" else "gloo"
+        dist.init_process_group(backend)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(world, v: float, device) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_quad_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get("dram_bytes_per_launch"), d
+    except (OSError, ValueError):
+        return None, None
+
+
+def cpu_baseline(cfg, mesh, grid, tables, plan, units_case, kind, workers, sample_scale=1.0, seed=0):
+    from oracle import cpu_baseline as CB
+
+    n = {"regular": int(2000 * sample_scale), "coincident": max(2, int(12 * sample_scale)),
+         "edge": max(2, int(12 * sample_scale)), "vertex": max(2, int(24 * sample_scale))}
+    tasks = CB.build_tasks(mesh, grid, tables, plan, n, seed=seed)
+    meas = CB.measure(tasks, kind=kind, workers=workers)
+    seconds, rate = CB.estimate(meas, units_case)
+    sample_units = sum(u for u, _ in meas.values())
+    sample_secs = sum(t for _, t in meas.values())
+    return rate, seconds, {
+        "sample": (f"stratified: {n} pairs per case, all admissible positions "
+                   f"({sample_units} units, {sample_secs:.1f} s wall on {workers} process(es)); "
+                   f"full {cfg.name} extrapolated by exact per-case unit counts; kernel "
+                   f"{'reference _core (oracle/_ref)' if kind == 'reference' else 'C port (oracle)'}"),
+        "strata": {c: {"units": u, "seconds": round(t, 4)} for c, (u, t) in meas.items()},
+        "extrapolated_seconds_full_assembly": seconds,
+    }
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    from paper_1503_07221_b200.assembly import build_plan
+    from paper_1503_07221_b200.block_system import canonical_positions
+    from paper_1503_07221_b200.configs import get_config
+    from paper_1503_07221_b200.kernel_weights import tables_for
+    from oracle import assembly as OA
+
+    cfg = get_config(args.config)
+    mesh, grid = cfg.mesh(), cfg.grid()
+    tables = tables_for(grid)
+    plan = build_plan(mesh, grid, tables, canonical_positions(grid, mesh.diameter))
+    units_case = unit_counts_host(mesh, plan)
+    kind = "reference" if OA.ref_core() is not None else "port"
+    workers = os.cpu_count() or 1
+    rates = []
+    info = None
+    for step in range(args.warmup + args.steps):
+        rate, seconds, info = cpu_baseline(cfg, mesh, grid, tables, plan, units_case,
+                                           "reference" if kind == "reference" else "c", workers,
+                                           sample_scale=args.ref_sample, seed=step)
+        if step >= args.warmup:
+            rates.append(rate)
+    value = float(np.median(rates))
+    total_units = sum(units_case.values())
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total_units / value, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8d meshes)",
+        "config": {"workload": cfg.name, "units_per_step": total_units, "p": grid.p,
+                   "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": kind,
+                         "sample": info["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "detail": info,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def unit_counts_host(mesh, plan):
+    """Exact units per case with the oracle's (reference-order) distance bounds."""
+    from oracle import assembly as OA
+    from oracle import cpu_baseline as CB
+    from paper_1503_07221_b200.mesh import touching_pairs
+
+    slo = np.concatenate([f.slo for f in plan.families])
+    shi = np.concatenate([f.shi for f in plan.families])
+    tmin, tmax = OA.tri_distance_bounds(mesh)
+    total = 0
+    for a, b in zip(slo, shi):
+        total += int(((tmin <= b) & (tmax >= a)).sum())
+    out = {}
+    tp = touching_pairs(mesh)
+    for case in ("coincident", "edge", "vertex"):
+        ex, ey, _, _ = tp[case]
+        if len(ex) == 0:
+            out[case] = 0
+            continue
+        t0, t1 = CB.pair_bounds(mesh, ex, ey)
+        out[case] = int(((t0[:, None] <= shi[None, :]) & (t1[:, None] >= slo[None, :])).sum())
+    out["regular"] = total - sum(out.values())
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--ref-sample", type=float, default=1.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+    world, rank, local = dist_init()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+
+    from paper_1503_07221_b200 import _lib
+    from paper_1503_07221_b200.assembly import DeviceAssembly, build_plan
+    from paper_1503_07221_b200.block_system import assemble_system, canonical_positions
+    from paper_1503_07221_b200.configs import get_config
+    from paper_1503_07221_b200.kernel_weights import tables_for
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = get_config(args.config)
+    mesh, grid = cfg.mesh(), cfg.grid()
+    tables = tables_for(grid)
+    positions = canonical_positions(grid, mesh.diameter)
+    plan = build_plan(mesh, grid, tables, positions)
+    ctx = _lib.default_context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+
+    # device-resident system: inputs uploaded + buffers sized once (untimed)
+    sys_ = DeviceAssembly(mesh, plan, ctx)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)  # 256 MB > L2
+    for _ in range(args.warmup):
+        sys_.rerun()
+    clocks = ClockSampler(local)
+    step_ms, quad_ms = [], []
+    stats = None
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flush between timed steps (outside the events)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sys_.rerun()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        stats = sys_.stats()
+        quad_ms.append(stats["ms_quad"])
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    clk = clocks.stop()
+    ms = max_over_ranks(world, float(np.mean(step_ms)), dev)
+    units = int(stats["units"])
+    value = world * units / (ms * 1e-3)
+
+    # roofline of the dominant kernel (the quadrature kernel), FP64-bound
+    fl = flops_per_launch(stats, grid.p)
+    q_ms = float(np.mean(quad_ms))
+    achieved = fl / (q_ms * 1e-3) / 1e12
+    peak_meas = _lib.fp64_peak_tflops(ctx, repeats=5)
+    traffic, _ = load_traffic()
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak_meas, "unit": "TFLOP/s",
+                "frac": achieved / peak_meas,
+                "peak_source": "measured in-run DFMA microbenchmark (tdb_fp64_peak); "
+                               "MEASURED_PEAKS.json has no FP64 entry",
+                "peak_nominal": 37.2, "frac_of_nominal": achieved / 37.2,
+                "traffic": traffic, "kernel": "k_quad", "kernel_ms": q_ms,
+                "kernel_share_of_step": q_ms / float(np.mean(step_ms)),
+                "flops_per_launch": fl, "n_in": stats["n_in"], "n_geom": stats["n_geom"]}
+
+    # end to end through the public API (host mesh in, every block back on the host)
+    e2e = None
+    if not args.no_e2e:
+        e2e_ms = []
+        h2d = d2h = 0
+        for i in range(max(1, min(args.steps, 3)) + 1):
+            barrier(world)
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            A = assemble_system(mesh, grid, tables=tables, device=local)
+            host = [A._dev.family_arrays(f) for f in range(A._dev.num_families)]
+            torch.cuda.synchronize(dev)
+            t1 = time.perf_counter()
+            if i > 0:  # first call warms the allocator / plan caches
+                e2e_ms.append((t1 - t0) * 1e3)
+            d2h = sum(a.nbytes + b.nbytes + c.nbytes for a, b, c in host)
+            h2d = (mesh.corners.nbytes + mesh.normals.nbytes + mesh.curls.nbytes + mesh.areas.nbytes
+                   + mesh.triangles.nbytes + 2 * mesh.triangles.nbytes
+                   + sum(f.pack.coeffs.nbytes for f in plan.families)
+                   + sum(sum(a.nbytes for a in plan.rules[c]) for c in plan.rules))
+            del A, host
+        ems = max_over_ranks(world, float(np.mean(e2e_ms)), dev)
+        e2e = {"value": world * units / (ems * 1e-3), "unit": UNIT, "ms_per_step": ems,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "path": "block_system.assemble_system (C ABI tdb_system_assemble) + "
+                       "tdb_system_copy_family for every family"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import assembly as OA
+
+        kind = "reference" if OA.ref_core() is not None else "port"
+        uc = {"regular": int(stats["units_case"][0]), "coincident": int(stats["units_case"][1]),
+              "edge": int(stats["units_case"][2]), "vertex": int(stats["units_case"][3])}
+        rate, secs, info = cpu_baseline(cfg, mesh, grid, tables, plan, uc,
+                                        "reference" if kind == "reference" else "c", 1)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": kind, "sample": info["sample"],
+               "extrapolated_seconds_full_assembly": secs}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8d meshes)",
+            "config": {"workload": cfg.name, "units_per_step": units, "p": grid.p,
+                       "positions": len(plan.where), "nnz": stats["nnz_total"],
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "l2": "flushed between timed steps (256 MB write)"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(stats["launches"]) * args.steps,
+            "clocks": clk,
+            "phases_ms": {k: stats[k] for k in ("ms_plan", "ms_quad", "ms_finalize", "ms_pattern", "ms_total")},
+            "units_case": stats["units_case"],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -123,12 +123,18 @@ typedef struct TdbStats {
   double ms_finalize;      /* singular item reduction */
   double ms_pattern;       /* CSR pattern + compensated gather */
   double ms_total;
+  int64_t units_case[4];   /* units per pair case (regular, coincident, edge, vertex) */
+  int64_t pairs_case[4];   /* pairs with >= 1 unit, per case */
+  int64_t launches;        /* kernel launches issued by the last tdb_system_run */
 } TdbStats;
 
 typedef struct TdbContext TdbContext;
 typedef struct TdbSystem TdbSystem;
 
 int tdb_abi_version(void);
+/* Measured FP64 FMA throughput of the device (TFLOP/s, 2 flops per DFMA):
+ * a dependent-chain microbenchmark over all SMs, best of `repeats`. */
+int tdb_fp64_peak(TdbContext* ctx, int repeats, double* tflops);
 const char* tdb_last_error(void);
 int tdb_device_count(int* count);
 
@@ -137,7 +143,24 @@ int tdb_ctx_destroy(TdbContext* ctx);
 /* stream used by all stream-ordered calls on this context (0 = legacy default) */
 int tdb_ctx_set_stream(TdbContext* ctx, void* cuda_stream);
 
-/* Assemble every family's blocks into device memory (host inputs). */
+/* SurfaceMesh.tri_distance_bounds rows (mesh.py:146-153, :357-391) on the
+ * device: tmin (exact triangle distance, 0 for touching pairs) and tmax (max
+ * corner distance) of triangles rows[r] x every triangle, (nrows, E) each,
+ * bit-identical to the reference's numpy evaluation order.  Only the mesh's
+ * corners and triangles are read. */
+int tdb_tri_distance_bounds(TdbContext* ctx, const TdbMesh* mesh, int64_t nrows,
+                            const int64_t* rows, double* tmin, double* tmax);
+
+/* Upload the mesh, tables and rules (host inputs), size every device buffer
+ * (pair plan, work items, partials, CSR patterns); no values yet. */
+int tdb_system_create(TdbContext* ctx, const TdbMesh* mesh,
+                      const TdbAssemblyDesc* desc, TdbSystem** out);
+/* (Re)compute all blocks on the device from the resident inputs: pair plan,
+ * quadrature, singular item reduction, CSR pattern + compensated gather.
+ * Stream-ordered without host round trips; synchronises once at the end to
+ * publish TdbStats. */
+int tdb_system_run(TdbSystem* sys);
+/* tdb_system_create + tdb_system_run */
 int tdb_system_assemble(TdbContext* ctx, const TdbMesh* mesh,
                         const TdbAssemblyDesc* desc, TdbSystem** out);
 int tdb_system_destroy(TdbSystem* sys);

@@ -69,10 +69,15 @@ class TdbStats(C.Structure):
         ("units", i64), ("items", i64), ("n_in", i64), ("n_geom", i64), ("nnz_total", i64),
         ("ms_plan", C.c_double), ("ms_quad", C.c_double), ("ms_finalize", C.c_double),
         ("ms_pattern", C.c_double), ("ms_total", C.c_double),
+        ("units_case", i64 * 4), ("pairs_case", i64 * 4), ("launches", i64),
     ]
 
     def as_dict(self) -> dict:
-        return {name: getattr(self, name) for name, _ in self._fields_}
+        out = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            out[name] = list(v) if not isinstance(v, (int, float)) else v
+        return out
 
 
 class TdbMatvecDesc(C.Structure):
@@ -94,6 +99,7 @@ def _load():
     P = C.c_void_p
     sig = {
         "tdb_abi_version": (i32, []),
+        "tdb_fp64_peak": (i32, [P, C.c_int, C.POINTER(C.c_double)]),
         "tdb_last_error": (C.c_char_p, []),
         "tdb_device_count": (i32, [C.POINTER(C.c_int)]),
         "tdb_pair_block_contributions": (
@@ -101,7 +107,10 @@ def _load():
         "tdb_ctx_create": (i32, [C.c_int, C.POINTER(P)]),
         "tdb_ctx_destroy": (i32, [P]),
         "tdb_ctx_set_stream": (i32, [P, P]),
+        "tdb_tri_distance_bounds": (i32, [P, C.POINTER(TdbMesh), i64, i64p, f64p, f64p]),
         "tdb_system_assemble": (i32, [P, C.POINTER(TdbMesh), C.POINTER(TdbAssemblyDesc), C.POINTER(P)]),
+        "tdb_system_create": (i32, [P, C.POINTER(TdbMesh), C.POINTER(TdbAssemblyDesc), C.POINTER(P)]),
+        "tdb_system_run": (i32, [P]),
         "tdb_system_destroy": (i32, [P]),
         "tdb_system_stats": (i32, [P, C.POINTER(TdbStats)]),
         "tdb_system_family_nnz": (i32, [P, i32, C.POINTER(i64)]),
@@ -127,7 +136,8 @@ EXPORTED = (
     "tdb_ctx_create", "tdb_ctx_destroy", "tdb_ctx_set_stream", "tdb_system_assemble",
     "tdb_system_destroy", "tdb_system_stats", "tdb_system_family_nnz", "tdb_system_copy_family",
     "tdb_system_family_device", "tdb_matvec_plan_create", "tdb_matvec_plan_destroy", "tdb_matvec",
-    "tdb_matvec_plan_work",
+    "tdb_matvec_plan_work", "tdb_tri_distance_bounds", "tdb_system_create", "tdb_system_run",
+    "tdb_fp64_peak",
 )
 
 
@@ -180,3 +190,11 @@ def default_context(device: int | None = None) -> Context:
     if ctx is None:
         ctx = _CTX[device] = Context(device)
     return ctx
+
+
+def fp64_peak_tflops(ctx: "Context | None" = None, repeats: int = 5) -> float:
+    """Measured DFMA throughput of the device (TFLOP/s)."""
+    ctx = ctx or default_context()
+    out = C.c_double()
+    check(LIB.tdb_fp64_peak(ctx.handle, repeats, C.byref(out)), "fp64_peak")
+    return out.value

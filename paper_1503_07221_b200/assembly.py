@@ -279,6 +279,11 @@ class DeviceAssembly:
                                                 _lib.C.byref(desc), _lib.C.byref(h)), "system_assemble")
         self.handle = h
 
+    def rerun(self) -> None:
+        """Recompute every block from the device-resident inputs (no host round trips)."""
+        if self.handle is not None:
+            _lib.check(_lib.LIB.tdb_system_run(self.handle), "system_run")
+
     def stats(self) -> dict:
         if self.handle is None:
             return {}
@@ -349,3 +354,18 @@ def assemble_subblocks(mesh: SurfaceMesh, grid: TimeGrid, tables: PrototypeTable
 
 def assemble_block(mesh, grid, tables, kt, it, m2, m1, config=QuadratureConfig()):
     return assemble_subblocks(mesh, grid, tables, kt, it, config)[m2][m1]
+
+
+def tri_distance_bounds(mesh: SurfaceMesh, rows=None, ctx: _lib.Context | None = None):
+    """Device drop-in for SurfaceMesh.tri_distance_bounds (mesh.py:146-153):
+    (tmin, tmax) of triangle rows x all triangles, bit-identical to the reference."""
+    ctx = ctx or _lib.default_context()
+    E = mesh.num_triangles
+    rows = np.arange(E, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
+    tmin = np.empty((len(rows), E))
+    tmax = np.empty((len(rows), E))
+    keep: list = []
+    _lib.check(_lib.LIB.tdb_tri_distance_bounds(
+        ctx.handle, _lib.C.byref(_mesh_c(mesh, keep)), len(rows), _lib.ptr(rows, _lib.C.c_int64),
+        _lib.ptr(tmin), _lib.ptr(tmax)), "tri_distance_bounds")
+    return tmin, tmax

@@ -39,50 +39,70 @@ namespace tdb {
 
 // ---------------------------------------------------------------------------
 // geometry primitives (restating mesh.py:286-354)
+//
+// Admissibility is a comparison of these distances with multiples of dt, and
+// on symmetric meshes the two meet exactly (SURVEY finding 11: the last lag
+// of config 1 is decided by the last bit of tmax).  Every operation below is
+// therefore an explicitly rounded IEEE op (no FMA contraction) in the
+// evaluation order numpy uses in the reference: einsum('ij,ij->i') on 3-vectors
+// sums (x + z) + y, linalg.norm sums (x + y) + z.  tests pin tmin/tmax
+// bitwise against the reference (tests/test_gpu_parity.py).
 // ---------------------------------------------------------------------------
 struct V3 {
   double x, y, z;
 };
-__device__ __forceinline__ V3 sub(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
-__device__ __forceinline__ double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ double mul_(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ V3 vsub(V3 a, V3 b) { return {sub_(a.x, b.x), sub_(a.y, b.y), sub_(a.z, b.z)}; }
+__device__ __forceinline__ V3 vadd(V3 a, V3 b) { return {add_(a.x, b.x), add_(a.y, b.y), add_(a.z, b.z)}; }
+__device__ __forceinline__ V3 vscale(double s, V3 a) { return {mul_(s, a.x), mul_(s, a.y), mul_(s, a.z)}; }
+// numpy einsum('ij,ij->i') order
+__device__ __forceinline__ double edot(V3 a, V3 b) {
+  return add_(add_(mul_(a.x, b.x), mul_(a.z, b.z)), mul_(a.y, b.y));
+}
+// numpy linalg.norm(axis=-1) order
+__device__ __forceinline__ double enorm(V3 d) {
+  return sqrt(add_(add_(mul_(d.x, d.x), mul_(d.y, d.y)), mul_(d.z, d.z)));
+}
 __device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+__device__ __forceinline__ V3 sub(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
 
 __device__ double seg_seg(V3 p0, V3 p1, V3 q0, V3 q1) {
-  V3 d1 = sub(p1, p0), d2 = sub(q1, q0), r = sub(p0, q0);
-  double a = dot(d1, d1), e = dot(d2, d2), b = dot(d1, d2), c = dot(d1, r), f = dot(d2, r);
-  double den = a * e - b * b;
+  V3 d1 = vsub(p1, p0), d2 = vsub(q1, q0), r = vsub(p0, q0);
+  double a = edot(d1, d1), e = edot(d2, d2), b = edot(d1, d2), c = edot(d1, r), f = edot(d2, r);
+  double den = sub_(mul_(a, e), mul_(b, b));
   double as = a > 0 ? a : 1.0, es = e > 0 ? e : 1.0;
-  double s = den > 0.0 ? clip01((b * f - c * e) / den) : 0.0;
-  double t = (b * s + f) / es;
+  double s = den > 0.0 ? clip01(sub_(mul_(b, f), mul_(c, e)) / den) : 0.0;
+  double t = add_(mul_(b, s), f) / es;
   if (t < 0.0) s = clip01(-c / as);
-  else if (t > 1.0) s = clip01((b - c) / as);
+  if (t > 1.0) s = clip01(sub_(b, c) / as);
   t = e > 0.0 ? clip01(t) : 0.0;
   s = a > 0.0 ? s : 0.0;
-  V3 d = {p0.x + s * d1.x - (q0.x + t * d2.x), p0.y + s * d1.y - (q0.y + t * d2.y),
-          p0.z + s * d1.z - (q0.z + t * d2.z)};
-  return sqrt(dot(d, d));
+  return enorm(vsub(vadd(p0, vscale(s, d1)), vadd(q0, vscale(t, d2))));
 }
 
 __device__ double pt_seg(V3 p, V3 a, V3 b) {
-  V3 ab = sub(b, a);
-  double den = dot(ab, ab);
-  double t = dot(sub(p, a), ab) / (den > 0 ? den : 1.0);
+  V3 ab = vsub(b, a);
+  double den = edot(ab, ab);
+  double t = edot(vsub(p, a), ab) / (den > 0 ? den : 1.0);
   t = den > 0.0 ? clip01(t) : 0.0;
-  V3 d = {p.x - a.x - t * ab.x, p.y - a.y - t * ab.y, p.z - a.z - t * ab.z};
-  return sqrt(dot(d, d));
+  return enorm(vsub(vsub(p, a), vscale(t, ab)));
 }
 
 __device__ double pt_tri(V3 p, V3 v0, V3 v1, V3 v2) {
-  V3 e0 = sub(v1, v0), e1 = sub(v2, v0);
-  V3 n = {e0.y * e1.z - e0.z * e1.y, e0.z * e1.x - e0.x * e1.z, e0.x * e1.y - e0.y * e1.x};
-  double nn = dot(n, n);
-  V3 w = sub(p, v0);
-  double dplane = fabs(dot(w, n)) / sqrt(nn > 0 ? nn : 1.0);
-  double d00 = dot(e0, e0), d01 = dot(e0, e1), d11 = dot(e1, e1), d20 = dot(w, e0), d21 = dot(w, e1);
-  double den = d00 * d11 - d01 * d01;
+  V3 e0 = vsub(v1, v0), e1 = vsub(v2, v0);
+  V3 n = {sub_(mul_(e0.y, e1.z), mul_(e0.z, e1.y)), sub_(mul_(e0.z, e1.x), mul_(e0.x, e1.z)),
+          sub_(mul_(e0.x, e1.y), mul_(e0.y, e1.x))};
+  double nn = edot(n, n);
+  V3 w = vsub(p, v0);
+  double dplane = fabs(edot(w, n)) / sqrt(nn > 0 ? nn : 1.0);
+  double d00 = edot(e0, e0), d01 = edot(e0, e1), d11 = edot(e1, e1), d20 = edot(w, e0), d21 = edot(w, e1);
+  double den = sub_(mul_(d00, d11), mul_(d01, d01));
   double dens = den > 0 ? den : 1.0;
-  double u = (d11 * d20 - d01 * d21) / dens, v = (d00 * d21 - d01 * d20) / dens;
-  bool inside = u >= 0.0 && v >= 0.0 && u + v <= 1.0 && den > 0.0 && nn > 0.0;
+  double u = sub_(mul_(d11, d20), mul_(d01, d21)) / dens;
+  double v = sub_(mul_(d00, d21), mul_(d01, d20)) / dens;
+  bool inside = u >= 0.0 && v >= 0.0 && add_(u, v) <= 1.0 && den > 0.0 && nn > 0.0;
   if (inside) return dplane;
   return fmin(fmin(pt_seg(p, v0, v1), pt_seg(p, v1, v2)), pt_seg(p, v2, v0));
 }
@@ -146,6 +166,56 @@ __device__ __forceinline__ int case_of(const int* __restrict__ tri, int ex, int 
   return n == 0 ? TDB_CASE_REGULAR : (n == 2 ? TDB_CASE_EDGE : TDB_CASE_VERTEX);
 }
 
+// Exact triangle-triangle distance and max corner distance of (ex, ey)
+// (mesh.py:357-391 _tri_pair_bounds, row ex / column ey); returns the case.
+__device__ int pair_bounds(const double* __restrict__ corners, const int* __restrict__ tri, int ex,
+                           int ey, double& tmin, double& tmax) {
+  V3 A[3], B[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    A[k] = corner(corners, ex, k);
+    B[k] = corner(corners, ey, k);
+  }
+  double dmax = 0.0, dmin = 1e300;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      double v = enorm(vsub(A[i], B[k]));
+      dmax = fmax(dmax, v);
+      dmin = fmin(dmin, v);
+    }
+  const int cs = case_of(tri, ex, ey);
+  if (cs != TDB_CASE_REGULAR) {
+    dmin = 0.0;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        dmin = fmin(dmin, seg_seg(A[i], A[(i + 1) % 3], B[k], B[(k + 1) % 3]));
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      dmin = fmin(dmin, pt_tri(A[i], B[0], B[1], B[2]));
+      dmin = fmin(dmin, pt_tri(B[i], A[0], A[1], A[2]));
+    }
+  }
+  tmin = dmin;
+  tmax = dmax;
+  return cs;
+}
+
+__global__ void k_bounds_rows(const double* __restrict__ corners, const int* __restrict__ tri, int E,
+                              const long long* __restrict__ rows, long long nrows,
+                              double* __restrict__ tmin, double* __restrict__ tmax) {
+  const long long n = nrows * E;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int ex = (int)rows[i / E], ey = (int)(i % E);
+    pair_bounds(corners, tri, ex, ey, tmin[i], tmax[i]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // 1. plan: bounds, admissible ranges, unit counts
 // ---------------------------------------------------------------------------
@@ -177,6 +247,7 @@ struct PlanArgs {
   long long* slots;         // [E*E] -> exclusive scan -> pair_base
   long long* nitems;        // [E*E] -> exclusive scan -> item_base
   unsigned char* pcase;     // [E*E]
+  unsigned long long* case_pairs;  // [4] pairs with >= 1 unit, [4..7] units, per case
 };
 
 __global__ void k_plan_pairs(PlanArgs a) {
@@ -184,37 +255,8 @@ __global__ void k_plan_pairs(PlanArgs a) {
   for (long long P = blockIdx.x * (long long)blockDim.x + threadIdx.x; P < E2;
        P += (long long)gridDim.x * blockDim.x) {
     const int ey = (int)(P / a.E), ex = (int)(P % a.E);
-    V3 A[3], B[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      A[k] = corner(a.corners, ex, k);
-      B[k] = corner(a.corners, ey, k);
-    }
-    double dmax = 0.0, dmin = 1e300;
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        V3 d = sub(A[i], B[k]);
-        double v = sqrt(dot(d, d));
-        dmax = fmax(dmax, v);
-        dmin = fmin(dmin, v);
-      }
-    const int cs = case_of(a.tri, ex, ey);
-    if (cs != TDB_CASE_REGULAR) {
-      dmin = 0.0;
-    } else {
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-          dmin = fmin(dmin, seg_seg(A[i], A[(i + 1) % 3], B[k], B[(k + 1) % 3]));
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        dmin = fmin(dmin, pt_tri(A[i], B[0], B[1], B[2]));
-        dmin = fmin(dmin, pt_tri(B[i], A[0], A[1], A[2]));
-      }
-    }
+    double dmin, dmax;
+    const int cs = pair_bounds(a.corners, a.tri, ex, ey, dmin, dmax);
     int units = 0;
     for (int f = 0; f < a.F; ++f) {
       const FamDev& fd = a.fams[f];
@@ -232,6 +274,10 @@ __global__ void k_plan_pairs(PlanArgs a) {
     const int ni = units > 0 ? a.nitems_case[cs] : 0;
     a.slots[P] = (long long)units * ni;
     a.nitems[P] = ni;
+    if (units > 0) {
+      atomicAdd(a.case_pairs + cs, 1ULL);
+      atomicAdd(a.case_pairs + 4 + cs, (unsigned long long)units);
+    }
   }
 }
 
@@ -725,8 +771,259 @@ int launch_fill(const PatternArgs& pa, size_t smem, cudaStream_t st) {
 
 }  // namespace
 
-int tdb_assemble_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDesc* desc,
-                      TdbSystem* sys) {
+// Persistent assembly workspace: everything sized once in tdb_system_create,
+// every kernel re-run (no host synchronisation in between) by tdb_system_run.
+struct AsmWorkspace {
+  long long E2 = 0;
+  double* blob = nullptr;
+  std::vector<int> fam_blob_off, fam_blob_len;
+  RuleDev rules[4];
+  std::vector<void*> rule_mem;
+  int nitems_case[4] = {1, 1, 1, 1};
+  int* d_nitems_case = nullptr;
+  FRange* frange = nullptr;
+  int* units = nullptr;
+  long long* slots = nullptr;
+  long long* nitems = nullptr;
+  unsigned char* pcase = nullptr;
+  int2* items = nullptr;
+  long long total_items = 0, total_slots = 0;
+  double* part = nullptr;
+  unsigned long long* counters = nullptr;  // [0] n_in, [1..32] work, [40..43] case pairs
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  struct Launch {
+    int f0, f1;
+    bool in_smem;
+    size_t bytes, smem;
+  };
+  std::vector<Launch> launches;
+  std::vector<int> s_chunk;
+  int words = 0;
+  cudaEvent_t ev[6];
+  bool events = false;
+  long long launch_count = 0;
+  ~AsmWorkspace() {
+    cudaFree(blob);
+    for (void* p : rule_mem) cudaFree(p);
+    cudaFree(d_nitems_case);
+    cudaFree(frange);
+    cudaFree(units);
+    cudaFree(slots);
+    cudaFree(nitems);
+    cudaFree(pcase);
+    cudaFree(items);
+    cudaFree(part);
+    cudaFree(counters);
+    cudaFree(cub_tmp);
+    if (events)
+      for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
+void tdb_workspace_free(TdbSystem* sys) {
+  delete sys->ws;
+  sys->ws = nullptr;
+}
+
+static int scan_inplace(AsmWorkspace* ws, long long* data, long long n, cudaStream_t st) {
+  size_t need = 0;
+  TDB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, need, data, data, (int64_t)n, st));
+  if (need > ws->cub_bytes) {
+    set_error("internal: cub workspace too small");
+    return TDB_E_CUDA;
+  }
+  TDB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ws->cub_tmp, need, data, data, (int64_t)n, st));
+  return TDB_OK;
+}
+
+static int read_ll(const long long* dev, long long* host, cudaStream_t st) {
+  TDB_CUDA_CHECK(cudaMemcpyAsync(host, dev, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  TDB_CUDA_CHECK(cudaStreamSynchronize(st));
+  return TDB_OK;
+}
+
+static PlanArgs plan_args(TdbSystem* sys) {
+  AsmWorkspace* ws = sys->ws;
+  PlanArgs pa;
+  pa.E = (int)sys->E;
+  pa.F = sys->F;
+  pa.corners = sys->corners;
+  pa.tri = sys->tri;
+  pa.fams = sys->famdev;
+  for (int c = 0; c < 4; ++c) pa.nitems_case[c] = ws->nitems_case[c];
+  pa.frange = ws->frange;
+  pa.units = ws->units;
+  pa.slots = ws->slots;
+  pa.nitems = ws->nitems;
+  pa.pcase = ws->pcase;
+  pa.case_pairs = ws->counters + 40;
+  return pa;
+}
+
+static PatternArgs pattern_args(TdbSystem* sys, int f) {
+  AsmWorkspace* ws = sys->ws;
+  PatternArgs ga{};
+  ga.E = (int)sys->E;
+  ga.M = (int)sys->V;
+  ga.f = f;
+  ga.npos = sys->fam[f].npos;
+  ga.words = ws->words;
+  ga.tri = sys->tri;
+  ga.star_off = sys->star_off;
+  ga.star_ids = sys->star_ids;
+  ga.frange = ws->frange + (long long)f * ws->E2;
+  ga.row_count = reinterpret_cast<long long*>(sys->fam[f].indptr);
+  ga.indptr = sys->fam[f].indptr;
+  ga.indices = sys->fam[f].indices;
+  ga.data = sys->fam[f].data;
+  ga.pair_base = ws->slots;
+  ga.part = ws->part;
+  ga.normals = sys->normals;
+  ga.curls = sys->curls;
+  ga.nacc = sys->nacc;
+  ga.nm = sys->nm;
+  return ga;
+}
+
+// plan kernels (bounds, ranges, scans, items) - no host sync
+static int run_plan(TdbSystem* sys, cudaStream_t st) {
+  AsmWorkspace* ws = sys->ws;
+  TDB_CUDA_CHECK(cudaMemsetAsync(ws->counters, 0, 64 * sizeof(unsigned long long), st));
+  PlanArgs pa = plan_args(sys);
+  const long long blocks = std::min<long long>((ws->E2 + 255) / 256, 148LL * 32);
+  k_plan_pairs<<<(int)blocks, 256, 0, st>>>(pa);
+  TDB_CUDA_CHECK(cudaGetLastError());
+  int rc;
+  if ((rc = scan_inplace(ws, ws->slots, ws->E2, st))) return rc;
+  if ((rc = scan_inplace(ws, ws->nitems, ws->E2, st))) return rc;
+  if (ws->items) {
+    k_fill_items<<<(int)blocks, 256, 0, st>>>(ws->E2, ws->nitems, nullptr, ws->units, ws->pcase,
+                                              ws->d_nitems_case, ws->items);
+    TDB_CUDA_CHECK(cudaGetLastError());
+  }
+  return TDB_OK;
+}
+
+static int run_pattern_count(TdbSystem* sys, int f, cudaStream_t st) {
+  AsmWorkspace* ws = sys->ws;
+  PatternArgs ga = pattern_args(sys, f);
+  const int npos = ga.npos;
+  for (int s0 = 0; s0 < npos; s0 += ws->s_chunk[f]) {
+    ga.s_begin = s0;
+    ga.s_count = std::min(ws->s_chunk[f], npos - s0);
+    const size_t smem = (size_t)ga.s_count * ws->words * 4;
+    TDB_CUDA_CHECK(cudaFuncSetAttribute(k_pattern_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    k_pattern_count<<<(int)sys->V, 256, smem, st>>>(ga);
+    TDB_CUDA_CHECK(cudaGetLastError());
+  }
+  const long long nrows = (long long)npos * sys->V;
+  TDB_CUDA_CHECK(cudaMemsetAsync(ga.row_count + nrows, 0, sizeof(long long), st));
+  return scan_inplace(ws, ga.row_count, nrows + 1, st);
+}
+
+int tdb_system_run_impl(TdbSystem* sys) {
+  AsmWorkspace* ws = sys->ws;
+  TdbContext* ctx = sys->ctx;
+  cudaStream_t st = ctx->stream;
+  const int p = sys->p, NACC = sys->nacc, NM = sys->nm;
+  int rc;
+  TDB_CUDA_CHECK(cudaEventRecord(ws->ev[0], st));
+  // kernel launches of this run: plan (k_plan_pairs, 2 cub scans x 2, k_fill_items), quad
+  // groups, finalize, per family (count chunks + cub scan x 2 + fill chunks)
+  long long nl = 6 + (long long)ws->launches.size();
+  {
+    bool multi_ = false;
+    for (int c = 0; c < 4; ++c) multi_ |= ws->nitems_case[c] > 1;
+    nl += multi_ ? 1 : 0;
+    for (int f = 0; f < sys->F; ++f) {
+      const int chunks = (sys->fam[f].npos + ws->s_chunk[f] - 1) / ws->s_chunk[f];
+      nl += 2 * chunks + 2;
+    }
+  }
+  ws->launch_count = nl;
+  if ((rc = run_plan(sys, st))) return rc;
+  TDB_CUDA_CHECK(cudaEventRecord(ws->ev[1], st));
+  int li = 0;
+  for (const auto& L : ws->launches) {
+    QuadArgs qa;
+    qa.E = (int)sys->E;
+    qa.fam_begin = L.f0;
+    qa.fam_count = L.f1 - L.f0;
+    qa.fams = sys->famdev;
+    qa.blob = ws->blob + ws->fam_blob_off[L.f0];
+    qa.blob_doubles = (int)(L.in_smem ? L.bytes / 8 : 0);
+    qa.coef_in_smem = L.in_smem;
+    qa.tri = sys->tri;
+    qa.corners = sys->corners;
+    qa.a2 = sys->a2;
+    for (int c = 0; c < 4; ++c) qa.rules[c] = ws->rules[c];
+    qa.items = ws->items;
+    qa.nitems = ws->total_items;
+    qa.work = ws->counters + 1 + (li % 32);
+    qa.frange = ws->frange;
+    qa.pair_base = ws->slots;
+    qa.units = ws->units;
+    qa.part = ws->part;
+    qa.n_in = ws->counters;
+    switch (p) {
+      case 0: rc = launch_quad<0>(qa, L.smem, L.in_smem, ctx->num_sms, st); break;
+      case 1: rc = launch_quad<1>(qa, L.smem, L.in_smem, ctx->num_sms, st); break;
+      case 2: rc = launch_quad<2>(qa, L.smem, L.in_smem, ctx->num_sms, st); break;
+      default: rc = launch_quad<3>(qa, L.smem, L.in_smem, ctx->num_sms, st); break;
+    }
+    if (rc) return rc;
+    ++li;
+  }
+  TDB_CUDA_CHECK(cudaEventRecord(ws->ev[2], st));
+  bool multi = false;
+  for (int c = 0; c < 4; ++c) multi |= ws->nitems_case[c] > 1;
+  if (multi) {
+    k_finalize_items<<<148 * 16, 256, 0, st>>>(ws->E2, ws->units, ws->pcase, ws->slots,
+                                               ws->d_nitems_case, NACC, ws->part);
+    TDB_CUDA_CHECK(cudaGetLastError());
+  }
+  TDB_CUDA_CHECK(cudaEventRecord(ws->ev[3], st));
+  for (int f = 0; f < sys->F; ++f) {
+    if ((rc = run_pattern_count(sys, f, st))) return rc;
+    PatternArgs ga = pattern_args(sys, f);
+    for (int s0 = 0; s0 < ga.npos; s0 += ws->s_chunk[f]) {
+      ga.s_begin = s0;
+      ga.s_count = std::min(ws->s_chunk[f], ga.npos - s0);
+      const size_t smem = (size_t)ga.s_count * ws->words * 4 + (ws->words + 1) * 4;
+      switch (NM) {
+        case 1: rc = launch_fill<1>(ga, smem, st); break;
+        case 4: rc = launch_fill<4>(ga, smem, st); break;
+        case 9: rc = launch_fill<9>(ga, smem, st); break;
+        default: rc = launch_fill<16>(ga, smem, st); break;
+      }
+      if (rc) return rc;
+    }
+  }
+  TDB_CUDA_CHECK(cudaEventRecord(ws->ev[4], st));
+  TDB_CUDA_CHECK(cudaEventSynchronize(ws->ev[4]));
+  unsigned long long cnt[64];
+  TDB_CUDA_CHECK(cudaMemcpy(cnt, ws->counters, sizeof(cnt), cudaMemcpyDeviceToHost));
+  long long n_geom = 0;
+  for (int c = 0; c < 4; ++c) {
+    n_geom += (long long)cnt[40 + c] * ws->rules[c].nq;
+    sys->stats.pairs_case[c] = (int64_t)cnt[40 + c];
+    sys->stats.units_case[c] = (int64_t)cnt[44 + c];
+  }
+  sys->stats.launches = ws->launch_count;
+  sys->stats.n_in = (int64_t)cnt[0];
+  sys->stats.n_geom = n_geom;
+  sys->stats.ms_plan = elapsed(ws->ev[0], ws->ev[1]);
+  sys->stats.ms_quad = elapsed(ws->ev[1], ws->ev[2]);
+  sys->stats.ms_finalize = elapsed(ws->ev[2], ws->ev[3]);
+  sys->stats.ms_pattern = elapsed(ws->ev[3], ws->ev[4]);
+  sys->stats.ms_total = elapsed(ws->ev[0], ws->ev[4]);
+  return TDB_OK;
+}
+
+int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDesc* desc,
+                           TdbSystem* sys) {
   cudaStream_t st = ctx->stream;
   const int p = desc->p;
   TDB_REQUIRE(p >= 0 && p <= 3, "assemble: p must be in 0..3");
@@ -740,17 +1037,19 @@ int tdb_assemble_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDes
   sys->F = desc->num_families;
   sys->E = E;
   sys->V = V;
-  const int F = sys->F, NM = sys->nm, NACC = sys->nacc;
-  const int nt = 2 * NM;
-  Timer t0, t1, t2, t3, t4;
-  TDB_CUDA_CHECK(cudaEventRecord(t0.a, st));
+  sys->ws = new AsmWorkspace();
+  AsmWorkspace* ws = sys->ws;
+  for (auto& e : ws->ev) TDB_CUDA_CHECK(cudaEventCreate(&e));
+  ws->events = true;
+  const int F = sys->F, NACC = sys->nacc;
+  const int nt = 2 * sys->nm;
+  int rc;
 
-  // ---- mesh upload (int32 topology) ----
+  // ---- mesh (int32 topology) ----
   std::vector<int> tri32(3 * E), soff(V + 1), sids(3 * E);
   for (long long i = 0; i < 3 * E; ++i) tri32[i] = (int)mesh->triangles[i];
   for (long long i = 0; i <= V; ++i) soff[i] = (int)mesh->star_off[i];
   for (long long i = 0; i < 3 * E; ++i) sids[i] = (int)mesh->star_ids[i];
-  int rc;
   if ((rc = dupload(&sys->corners, mesh->corners, 9 * E, st))) return rc;
   if ((rc = dupload(&sys->a2, mesh->a2, E, st))) return rc;
   if ((rc = dupload(&sys->normals, mesh->normals, 3 * E, st))) return rc;
@@ -763,7 +1062,8 @@ int tdb_assemble_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDes
   sys->fam.resize(F);
   sys->famdev_host.resize(F);
   std::vector<double> blob_all;
-  std::vector<int> fam_blob_off(F), fam_blob_len(F);
+  ws->fam_blob_off.resize(F);
+  ws->fam_blob_len.resize(F);
   for (int f = 0; f < F; ++f) {
     const TdbFamily& hf = desc->families[f];
     const TdbPsiPack& pk = hf.pack;
@@ -797,10 +1097,9 @@ int tdb_assemble_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDes
     if ((rc = dupload(&fs.delta, hf.delta, hf.npos, st))) return rc;
     if ((rc = dupload(&fs.slo, hf.slo, hf.npos, st))) return rc;
     if ((rc = dupload(&fs.shi, hf.shi, hf.npos, st))) return rc;
-    // compact (nt, nsub, deg+1) copy (pack stride is max_nsub)
     const int len = nt * fd.nsub * (kDeg + 1);
-    fam_blob_off[f] = (int)blob_all.size();
-    fam_blob_len[f] = len;
+    ws->fam_blob_off[f] = (int)blob_all.size();
+    ws->fam_blob_len[f] = len;
     for (int t = 0; t < nt; ++t)
       for (int k = 0; k < fd.nsub; ++k)
         for (int c = 0; c <= kDeg; ++c)
@@ -810,22 +1109,17 @@ int tdb_assemble_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDes
     fd.shi = fs.shi;
     sys->famdev_host[f] = fd;
   }
-  double* d_blob = nullptr;
-  if ((rc = dupload(&d_blob, blob_all.data(), blob_all.size(), st))) return rc;
-  Dev blob_guard;
-  blob_guard.p = d_blob;
-  for (int f = 0; f < F; ++f) sys->famdev_host[f].coeffs = d_blob + fam_blob_off[f];
+  if ((rc = dupload(&ws->blob, blob_all.data(), blob_all.size(), st))) return rc;
+  for (int f = 0; f < F; ++f) sys->famdev_host[f].coeffs = ws->blob + ws->fam_blob_off[f];
 
   // ---- rules ----
-  RuleDev rules[4];
-  std::vector<Dev> rule_mem(20);
-  int nitems_case[4];
   for (int c = 0; c < 4; ++c) {
     const TdbRule& r = desc->rules[c];
     TDB_REQUIRE(r.nq >= 1 || c != TDB_CASE_REGULAR, "assemble: regular rule missing");
-    rules[c].nq = r.nq;
-    rules[c].nitems = (int)((r.nq + kChunk - 1) / kChunk);
-    nitems_case[c] = std::max(1, rules[c].nitems);
+    RuleDev& rd = ws->rules[c];
+    rd.nq = r.nq;
+    rd.nitems = (int)((r.nq + kChunk - 1) / kChunk);
+    ws->nitems_case[c] = std::max(1, rd.nitems);
     std::vector<double> x1(r.nq), x2(r.nq), y1(r.nq), y2(r.nq);
     for (long long q = 0; q < r.nq; ++q) {
       x1[q] = r.xhat[2 * q];
@@ -836,223 +1130,187 @@ int tdb_assemble_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDes
     double* ptrs[5];
     const double* src[5] = {x1.data(), x2.data(), y1.data(), y2.data(), r.w};
     for (int k = 0; k < 5; ++k) {
-      if ((rc = dupload(&ptrs[k], src[k], (size_t)std::max<long long>(r.nq, 1) * (r.nq > 0), st)))
-        return rc;
-      rule_mem[5 * c + k].p = ptrs[k];
+      if ((rc = dupload(&ptrs[k], src[k], (size_t)(r.nq > 0 ? r.nq : 0), st))) return rc;
+      ws->rule_mem.push_back(ptrs[k]);
     }
-    rules[c].x1 = ptrs[0];
-    rules[c].x2 = ptrs[1];
-    rules[c].y1 = ptrs[2];
-    rules[c].y2 = ptrs[3];
-    rules[c].w = ptrs[4];
+    rd.x1 = ptrs[0];
+    rd.x2 = ptrs[1];
+    rd.y1 = ptrs[2];
+    rd.y2 = ptrs[3];
+    rd.w = ptrs[4];
   }
+  if ((rc = dupload(&ws->d_nitems_case, ws->nitems_case, 4, st))) return rc;
 
-  if ((rc = dupload(&sys->famdev, sys->famdev_host.data(), F, st))) return rc;
-  int* d_nitems_case = nullptr;
-  if ((rc = dupload(&d_nitems_case, nitems_case, 4, st))) return rc;
-  Dev nic_guard;
-  nic_guard.p = d_nitems_case;
-
-  // ---- 1. plan ----
-  const long long E2 = E * E;
-  Dev d_frange, d_units, d_slots, d_nitems, d_pcase;
-  if ((rc = dalloc_dev<FRange>(d_frange, (size_t)F * E2))) return rc;
-  if ((rc = dalloc_dev<int>(d_units, E2))) return rc;
-  if ((rc = dalloc_dev<long long>(d_slots, E2))) return rc;
-  if ((rc = dalloc_dev<long long>(d_nitems, E2))) return rc;
-  if ((rc = dalloc_dev<unsigned char>(d_pcase, E2))) return rc;
-  PlanArgs pa;
-  pa.E = (int)E;
-  pa.F = F;
-  pa.corners = sys->corners;
-  pa.tri = sys->tri;
-  pa.fams = sys->famdev;
-  for (int c = 0; c < 4; ++c) pa.nitems_case[c] = nitems_case[c];
-  pa.frange = d_frange.as<FRange>();
-  pa.units = d_units.as<int>();
-  pa.slots = d_slots.as<long long>();
-  pa.nitems = d_nitems.as<long long>();
-  pa.pcase = d_pcase.as<unsigned char>();
-  {
-    long long blocks = std::min<long long>((E2 + 255) / 256, 148LL * 32);
-    k_plan_pairs<<<(int)blocks, 256, 0, st>>>(pa);
-    TDB_CUDA_CHECK(cudaGetLastError());
-  }
-  long long total_slots = 0, total_items = 0;
-  if ((rc = exclusive_scan_ll(d_slots.as<long long>(), E2, &total_slots, st))) return rc;
-  if ((rc = exclusive_scan_ll(d_nitems.as<long long>(), E2, &total_items, st))) return rc;
-  Dev d_items;
-  if ((rc = dalloc_dev<int2>(d_items, total_items))) return rc;
-  {
-    long long blocks = std::min<long long>((E2 + 255) / 256, 148LL * 32);
-    k_fill_items<<<(int)blocks, 256, 0, st>>>(E2, d_nitems.as<long long>(), nullptr,
-                                              d_units.as<int>(), d_pcase.as<unsigned char>(),
-                                              d_nitems_case, d_items.as<int2>());
-    TDB_CUDA_CHECK(cudaGetLastError());
-  }
-  TDB_CUDA_CHECK(cudaEventRecord(t0.b, st));
-
-  // ---- 3. quadrature ----
-  Dev d_part, d_counters;
-  if ((rc = dalloc_dev<double>(d_part, (size_t)total_slots * NACC))) return rc;
-  if ((rc = dalloc_dev<unsigned long long>(d_counters, 16))) return rc;
-  TDB_CUDA_CHECK(cudaMemsetAsync(d_counters.p, 0, 16 * sizeof(unsigned long long), st));
+  // ---- quadrature launch groups (families whose coefficients fit in smem) ----
   int max_smem = 0;
   TDB_CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   const size_t warp_bytes = (size_t)kQuadWarps * (2 * kChunk * 8 + kChunk);
   const size_t budget = (size_t)max_smem - warp_bytes - sizeof(FamDev) * kMaxFamilies - 64;
-  TDB_CUDA_CHECK(cudaEventRecord(t1.a, st));
-  int nlaunch = 0;
   for (int f0 = 0; f0 < F;) {
-    // greedy grouping of consecutive families whose coefficients fit in smem
     size_t bytes = 0;
     int f1 = f0;
-    while (f1 < F && bytes + (size_t)fam_blob_len[f1] * 8 <= budget) bytes += (size_t)fam_blob_len[f1++] * 8;
+    while (f1 < F && bytes + (size_t)ws->fam_blob_len[f1] * 8 <= budget)
+      bytes += (size_t)ws->fam_blob_len[f1++] * 8;
     const bool in_smem = f1 > f0;
-    if (!in_smem) f1 = f0 + 1;  // single oversized family: coefficients from global/L1
+    if (!in_smem) f1 = f0 + 1;
     for (int f = f0; f < f1; ++f)
-      sys->famdev_host[f].coeff_off = fam_blob_off[f] - fam_blob_off[f0];
-    TDB_CUDA_CHECK(cudaMemcpyAsync(sys->famdev + f0, sys->famdev_host.data() + f0,
-                                   sizeof(FamDev) * (f1 - f0), cudaMemcpyHostToDevice, st));
-    QuadArgs qa;
-    qa.E = (int)E;
-    qa.fam_begin = f0;
-    qa.fam_count = f1 - f0;
-    qa.fams = sys->famdev;
-    qa.blob = d_blob + fam_blob_off[f0];
-    qa.blob_doubles = (int)(in_smem ? bytes / 8 : 0);
-    qa.coef_in_smem = in_smem;
-    qa.tri = sys->tri;
-    qa.corners = sys->corners;
-    qa.a2 = sys->a2;
-    for (int c = 0; c < 4; ++c) qa.rules[c] = rules[c];
-    qa.items = d_items.as<int2>();
-    qa.nitems = total_items;
-    qa.work = d_counters.as<unsigned long long>() + 1 + nlaunch % 8;
-    qa.frange = d_frange.as<FRange>();
-    qa.pair_base = d_slots.as<long long>();
-    qa.units = d_units.as<int>();
-    qa.part = d_part.as<double>();
-    qa.n_in = d_counters.as<unsigned long long>();
-    const size_t smem = ((sizeof(FamDev) * (f1 - f0) + 7) / 8) * 8 + (in_smem ? bytes : 0) + warp_bytes;
-    const int grid = ctx->num_sms;
-    switch (p) {
-      case 0: rc = launch_quad<0>(qa, smem, in_smem, grid, st); break;
-      case 1: rc = launch_quad<1>(qa, smem, in_smem, grid, st); break;
-      case 2: rc = launch_quad<2>(qa, smem, in_smem, grid, st); break;
-      default: rc = launch_quad<3>(qa, smem, in_smem, grid, st); break;
-    }
-    if (rc) return rc;
-    ++nlaunch;
+      sys->famdev_host[f].coeff_off = ws->fam_blob_off[f] - ws->fam_blob_off[f0];
+    AsmWorkspace::Launch L;
+    L.f0 = f0;
+    L.f1 = f1;
+    L.in_smem = in_smem;
+    L.bytes = in_smem ? bytes : 0;
+    L.smem = ((sizeof(FamDev) * (f1 - f0) + 7) / 8) * 8 + L.bytes + warp_bytes;
+    ws->launches.push_back(L);
     f0 = f1;
-    if (nlaunch % 8 == 0)
-      TDB_CUDA_CHECK(cudaMemsetAsync(d_counters.as<unsigned long long>() + 1, 0, 8 * 8, st));
   }
-  TDB_CUDA_CHECK(cudaEventRecord(t1.b, st));
+  if ((rc = dupload(&sys->famdev, sys->famdev_host.data(), F, st))) return rc;
 
-  // ---- 4. singular finalize ----
-  TDB_CUDA_CHECK(cudaEventRecord(t2.a, st));
+  // ---- plan buffers and sizes ----
+  ws->E2 = E * E;
+  const long long E2 = ws->E2;
+  if ((rc = dalloc(&ws->frange, (size_t)F * E2))) return rc;
+  if ((rc = dalloc(&ws->units, E2))) return rc;
+  if ((rc = dalloc(&ws->slots, E2))) return rc;
+  if ((rc = dalloc(&ws->nitems, E2))) return rc;
+  if ((rc = dalloc(&ws->pcase, E2))) return rc;
+  if ((rc = dalloc(&ws->counters, 64))) return rc;
+  ws->words = (int)((V + 31) / 32);
+  ws->s_chunk.resize(F);
+  long long max_rows = 0;
+  for (int f = 0; f < F; ++f) {
+    const int npos = sys->fam[f].npos;
+    ws->s_chunk[f] = std::max(1, (int)std::min<long long>(npos, (96LL * 1024) / (ws->words * 4)));
+    max_rows = std::max(max_rows, (long long)npos * V + 1);
+  }
   {
-    bool multi = false;
-    for (int c = 0; c < 4; ++c) multi |= nitems_case[c] > 1;
-    if (multi) {
-      k_finalize_items<<<148 * 16, 256, 0, st>>>(E2, d_units.as<int>(), d_pcase.as<unsigned char>(),
-                                                 d_slots.as<long long>(), d_nitems_case, NACC,
-                                                 d_part.as<double>());
-      TDB_CUDA_CHECK(cudaGetLastError());
-    }
+    size_t b1 = 0, b2 = 0;
+    TDB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, b1, ws->slots, ws->slots, (int64_t)E2, st));
+    TDB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, b2, ws->slots, ws->slots, (int64_t)max_rows, st));
+    ws->cub_bytes = std::max(b1, b2) + 256;
+    if ((rc = dalloc(reinterpret_cast<char**>(&ws->cub_tmp), ws->cub_bytes))) return rc;
   }
-  TDB_CUDA_CHECK(cudaEventRecord(t2.b, st));
-
-  // ---- 5. pattern + gather per family ----
-  TDB_CUDA_CHECK(cudaEventRecord(t3.a, st));
-  const int words = (int)((V + 31) / 32);
+  // sizing pass: run the plan once and read the totals
+  if ((rc = run_plan(sys, st))) return rc;
+  {
+    long long last_s = 0, last_i = 0;
+    // slots/nitems are exclusive scans now; totals = last exclusive + last raw (recomputed)
+    long long ex_s = 0, ex_i = 0;
+    if ((rc = read_ll(ws->slots + E2 - 1, &ex_s, st))) return rc;
+    if ((rc = read_ll(ws->nitems + E2 - 1, &ex_i, st))) return rc;
+    int u_last = 0;
+    unsigned char c_last = 0;
+    TDB_CUDA_CHECK(cudaMemcpy(&u_last, ws->units + E2 - 1, sizeof(int), cudaMemcpyDeviceToHost));
+    TDB_CUDA_CHECK(cudaMemcpy(&c_last, ws->pcase + E2 - 1, 1, cudaMemcpyDeviceToHost));
+    const int ni = u_last > 0 ? ws->nitems_case[c_last] : 0;
+    last_s = (long long)u_last * ni;
+    last_i = ni;
+    ws->total_slots = ex_s + last_s;
+    ws->total_items = ex_i + last_i;
+  }
+  if ((rc = dalloc(&ws->items, ws->total_items))) return rc;
+  if ((rc = dalloc(&ws->part, (size_t)ws->total_slots * NACC))) return rc;
+  // pattern sizing: counts -> scan -> nnz
   long long nnz_total = 0;
   for (int f = 0; f < F; ++f) {
     FamilyStore& fs = sys->fam[f];
-    const int npos = fs.npos;
-    const long long nrows = (long long)npos * V;
-    Dev d_cnt;
-    if ((rc = dalloc_dev<long long>(d_cnt, nrows + 1))) return rc;
-    PatternArgs ga{};
-    ga.E = (int)E;
-    ga.M = (int)V;
-    ga.f = f;
-    ga.npos = npos;
-    ga.words = words;
-    ga.tri = sys->tri;
-    ga.star_off = sys->star_off;
-    ga.star_ids = sys->star_ids;
-    ga.frange = d_frange.as<FRange>() + (long long)f * E2;
-    ga.row_count = d_cnt.as<long long>();
-    ga.pair_base = d_slots.as<long long>();
-    ga.part = d_part.as<double>();
-    ga.normals = sys->normals;
-    ga.curls = sys->curls;
-    ga.nacc = NACC;
-    ga.nm = NM;
-    const size_t bm_budget = 96 * 1024;
-    const int s_chunk = std::max(1, (int)std::min<long long>(npos, (long long)(bm_budget / (words * 4))));
-    for (int s0 = 0; s0 < npos; s0 += s_chunk) {
-      ga.s_begin = s0;
-      ga.s_count = std::min(s_chunk, npos - s0);
-      const size_t smem = (size_t)ga.s_count * words * 4;
-      TDB_CUDA_CHECK(cudaFuncSetAttribute(k_pattern_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
-      k_pattern_count<<<(int)V, 256, smem, st>>>(ga);
-      TDB_CUDA_CHECK(cudaGetLastError());
-    }
-    TDB_CUDA_CHECK(cudaMemsetAsync(d_cnt.as<long long>() + nrows, 0, sizeof(long long), st));
+    const long long nrows = (long long)fs.npos * V;
+    if ((rc = dalloc(&fs.indptr, nrows + 1))) return rc;
+    if ((rc = run_pattern_count(sys, f, st))) return rc;
     long long nnz = 0;
-    if ((rc = exclusive_scan_ll(d_cnt.as<long long>(), nrows + 1, &nnz, st))) return rc;
+    if ((rc = read_ll(reinterpret_cast<long long*>(fs.indptr) + nrows, &nnz, st))) return rc;
     fs.nnz = nnz;
     nnz_total += nnz;
-    fs.indptr = reinterpret_cast<int64_t*>(d_cnt.p);
-    d_cnt.p = nullptr;  // ownership moves to the family store
     if ((rc = dalloc(&fs.indices, nnz))) return rc;
-    if ((rc = dalloc(&fs.data, (size_t)nnz * NM))) return rc;
-    ga.indptr = fs.indptr;
-    ga.indices = fs.indices;
-    ga.data = fs.data;
-    for (int s0 = 0; s0 < npos; s0 += s_chunk) {
-      ga.s_begin = s0;
-      ga.s_count = std::min(s_chunk, npos - s0);
-      const size_t smem = (size_t)ga.s_count * words * 4 + (words + 1) * 4;
-      switch (NM) {
-        case 1: rc = launch_fill<1>(ga, smem, st); break;
-        case 4: rc = launch_fill<4>(ga, smem, st); break;
-        case 9: rc = launch_fill<9>(ga, smem, st); break;
-        default: rc = launch_fill<16>(ga, smem, st); break;
-      }
-      if (rc) return rc;
-    }
+    if ((rc = dalloc(&fs.data, (size_t)nnz * sys->nm))) return rc;
   }
-  TDB_CUDA_CHECK(cudaEventRecord(t3.b, st));
-  TDB_CUDA_CHECK(cudaStreamSynchronize(st));
-
-  unsigned long long n_in = 0;
-  TDB_CUDA_CHECK(cudaMemcpy(&n_in, d_counters.p, sizeof(n_in), cudaMemcpyDeviceToHost));
-  // units = sum over pairs (count on the host side from scans: slots minus singular items)
+  // units: one reduction
   long long units = 0;
   {
-    Dev d_tmp;
     size_t tb = 0;
-    TDB_CUDA_CHECK(cub::DeviceReduce::Sum(nullptr, tb, d_units.as<int>(), (long long*)nullptr, (int64_t)E2, st));
-    if ((rc = dalloc_dev<char>(d_tmp, tb + 16))) return rc;
-    long long* d_sum = reinterpret_cast<long long*>(static_cast<char*>(d_tmp.p) + ((tb + 7) / 8) * 8);
-    TDB_CUDA_CHECK(cub::DeviceReduce::Sum(d_tmp.p, tb, d_units.as<int>(), d_sum, (int64_t)E2, st));
-    TDB_CUDA_CHECK(cudaMemcpyAsync(&units, d_sum, sizeof(long long), cudaMemcpyDeviceToHost, st));
-    TDB_CUDA_CHECK(cudaStreamSynchronize(st));
+    TDB_CUDA_CHECK(cub::DeviceReduce::Sum(nullptr, tb, ws->units, (long long*)nullptr, (int64_t)E2, st));
+    Dev tmp;
+    if ((rc = dalloc_dev<char>(tmp, tb + 16))) return rc;
+    long long* d_sum = reinterpret_cast<long long*>(static_cast<char*>(tmp.p) + ((tb + 7) / 8) * 8);
+    TDB_CUDA_CHECK(cub::DeviceReduce::Sum(tmp.p, tb, ws->units, d_sum, (int64_t)E2, st));
+    if ((rc = read_ll(d_sum, &units, st))) return rc;
   }
   sys->stats.units = units;
-  sys->stats.items = total_items;
-  sys->stats.n_in = (int64_t)n_in;
+  sys->stats.items = ws->total_items;
   sys->stats.nnz_total = nnz_total;
-  sys->stats.ms_plan = elapsed(t0.a, t0.b);
-  sys->stats.ms_quad = elapsed(t1.a, t1.b);
-  sys->stats.ms_finalize = elapsed(t2.a, t2.b);
-  sys->stats.ms_pattern = elapsed(t3.a, t3.b);
-  sys->stats.ms_total = elapsed(t0.a, t3.b);
-  sys->famdev_host.clear();
+  return TDB_OK;
+}
+
+// Device computation of SurfaceMesh.tri_distance_bounds rows (mesh.py:146-153):
+// tmin/tmax (nrows, E) for triangle rows `rows` against every triangle.
+int tdb_tri_bounds_impl(TdbContext* ctx, const TdbMesh* mesh, int64_t nrows, const int64_t* rows,
+                        double* tmin, double* tmax) {
+  cudaStream_t st = ctx->stream;
+  const long long E = mesh->num_triangles;
+  TDB_REQUIRE(E >= 1 && nrows >= 0, "bounds: bad sizes");
+  for (long long i = 0; i < nrows; ++i) TDB_REQUIRE(rows[i] >= 0 && rows[i] < E, "bounds: row out of range");
+  if (nrows == 0) return TDB_OK;
+  std::vector<int> tri32(3 * E);
+  for (long long i = 0; i < 3 * E; ++i) tri32[i] = (int)mesh->triangles[i];
+  std::vector<long long> rows64(rows, rows + nrows);
+  Dev dc, dt, dr, dmn, dmx;
+  double* pc = nullptr;
+  int* pt = nullptr;
+  long long* pr = nullptr;
+  int rc;
+  if ((rc = dupload(&pc, mesh->corners, 9 * E, st))) return rc;
+  dc.p = pc;
+  if ((rc = dupload(&pt, tri32.data(), 3 * E, st))) return rc;
+  dt.p = pt;
+  if ((rc = dupload(&pr, rows64.data(), (size_t)nrows, st))) return rc;
+  dr.p = pr;
+  if ((rc = dalloc_dev<double>(dmn, (size_t)nrows * E))) return rc;
+  if ((rc = dalloc_dev<double>(dmx, (size_t)nrows * E))) return rc;
+  const long long n = nrows * E;
+  k_bounds_rows<<<(int)std::min<long long>((n + 255) / 256, 148LL * 32), 256, 0, st>>>(
+      pc, pt, (int)E, pr, nrows, dmn.as<double>(), dmx.as<double>());
+  TDB_CUDA_CHECK(cudaGetLastError());
+  TDB_CUDA_CHECK(cudaMemcpyAsync(tmin, dmn.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  TDB_CUDA_CHECK(cudaMemcpyAsync(tmax, dmx.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  TDB_CUDA_CHECK(cudaStreamSynchronize(st));
+  return TDB_OK;
+}
+
+namespace tdb {
+__global__ void k_dfma_peak(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-9, x2 = x0 + 2e-9, x3 = x0 + 3e-9;
+  double x4 = x0 + 4e-9, x5 = x0 + 5e-9, x6 = x0 + 6e-9, x7 = x0 + 7e-9;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  const double s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+  if (s == 1234.5678) out[0] = s;  // keep the chains alive
+}
+}  // namespace tdb
+
+int tdb_fp64_peak_impl(TdbContext* ctx, int repeats, double* tflops) {
+  cudaStream_t st = ctx->stream;
+  Dev d;
+  int rc;
+  if ((rc = dalloc_dev<double>(d, 1))) return rc;
+  const int threads = 256, blocks = ctx->num_sms * 8, iters = 2048;
+  Timer t;
+  double best = 0.0;
+  k_dfma_peak<<<blocks, threads, 0, st>>>(d.as<double>(), 64, 0.999999, 1e-7);
+  for (int r = 0; r < std::max(1, repeats); ++r) {
+    TDB_CUDA_CHECK(cudaEventRecord(t.a, st));
+    k_dfma_peak<<<blocks, threads, 0, st>>>(d.as<double>(), iters, 0.999999, 1e-7);
+    TDB_CUDA_CHECK(cudaEventRecord(t.b, st));
+    TDB_CUDA_CHECK(cudaEventSynchronize(t.b));
+    const double ms = elapsed(t.a, t.b);
+    const double flops = 2.0 * 64.0 * iters * (double)threads * blocks;
+    best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  }
+  TDB_CUDA_CHECK(cudaGetLastError());
+  *tflops = best;
   return TDB_OK;
 }

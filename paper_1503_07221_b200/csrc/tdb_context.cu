@@ -11,8 +11,12 @@ static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 }  // namespace tdb
 
-int tdb_assemble_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDesc* desc,
-                      TdbSystem* sys);
+int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDesc* desc,
+                           TdbSystem* sys);
+int tdb_system_run_impl(TdbSystem* sys);
+int tdb_fp64_peak_impl(TdbContext* ctx, int repeats, double* tflops);
+int tdb_tri_bounds_impl(TdbContext* ctx, const TdbMesh* mesh, int64_t nrows, const int64_t* rows,
+                        double* tmin, double* tmax);
 
 using namespace tdb;
 
@@ -21,6 +25,12 @@ extern "C" {
 int tdb_abi_version(void) { return TDB_ABI_VERSION; }
 
 const char* tdb_last_error(void) { return g_last_error.c_str(); }
+
+int tdb_fp64_peak(TdbContext* ctx, int repeats, double* tflops) {
+  TDB_REQUIRE(ctx && tflops, "NULL argument");
+  TDB_CUDA_CHECK(cudaSetDevice(ctx->device));
+  return tdb_fp64_peak_impl(ctx, repeats, tflops);
+}
 
 int tdb_device_count(int* count) {
   TDB_REQUIRE(count != nullptr, "count is NULL");
@@ -61,6 +71,8 @@ int tdb_ctx_set_stream(TdbContext* ctx, void* stream) {
 
 int tdb_system_destroy(TdbSystem* sys) {
   if (!sys) return TDB_OK;
+  if (sys->ctx) cudaSetDevice(sys->ctx->device);
+  tdb_workspace_free(sys);
   cudaFree(sys->corners);
   cudaFree(sys->a2);
   cudaFree(sys->normals);
@@ -81,19 +93,44 @@ int tdb_system_destroy(TdbSystem* sys) {
   return TDB_OK;
 }
 
-int tdb_system_assemble(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDesc* desc,
-                        TdbSystem** out) {
+int tdb_system_create(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDesc* desc,
+                      TdbSystem** out) {
   TDB_REQUIRE(ctx && mesh && desc && out, "NULL argument");
   TDB_CUDA_CHECK(cudaSetDevice(ctx->device));
   TdbSystem* sys = new TdbSystem();
   sys->ctx = ctx;
-  int rc = tdb_assemble_impl(ctx, mesh, desc, sys);
+  int rc = tdb_system_create_impl(ctx, mesh, desc, sys);
   if (rc != TDB_OK) {
     tdb_system_destroy(sys);
     return rc;
   }
   *out = sys;
   return TDB_OK;
+}
+
+int tdb_system_run(TdbSystem* sys) {
+  TDB_REQUIRE(sys != nullptr, "NULL system");
+  TDB_CUDA_CHECK(cudaSetDevice(sys->ctx->device));
+  return tdb_system_run_impl(sys);
+}
+
+int tdb_system_assemble(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDesc* desc,
+                        TdbSystem** out) {
+  int rc = tdb_system_create(ctx, mesh, desc, out);
+  if (rc != TDB_OK) return rc;
+  rc = tdb_system_run(*out);
+  if (rc != TDB_OK) {
+    tdb_system_destroy(*out);
+    *out = nullptr;
+  }
+  return rc;
+}
+
+int tdb_tri_distance_bounds(TdbContext* ctx, const TdbMesh* mesh, int64_t nrows,
+                            const int64_t* rows, double* tmin, double* tmax) {
+  TDB_REQUIRE(ctx && mesh && (nrows == 0 || (rows && tmin && tmax)), "NULL argument");
+  TDB_CUDA_CHECK(cudaSetDevice(ctx->device));
+  return tdb_tri_bounds_impl(ctx, mesh, nrows, rows, tmin, tmax);
 }
 
 int tdb_system_stats(const TdbSystem* sys, TdbStats* out) {

@@ -67,8 +67,12 @@ struct TdbContext {
   int num_sms = 148;
 };
 
+struct AsmWorkspace;
+void tdb_workspace_free(struct TdbSystem* sys);
+
 struct TdbSystem {
   TdbContext* ctx = nullptr;
+  AsmWorkspace* ws = nullptr;
   int p = 0, np1 = 1, nm = 1, nacc = 10, F = 0;
   long long E = 0, V = 0;
   // mesh

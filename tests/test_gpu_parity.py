@@ -198,3 +198,17 @@ def test_cfg1_positions_vs_reference(G, cfg1_mesh):
         d = abs(got - ref)
         dmax = d.max() if d.nnz else 0.0
         assert dmax <= 1e-10 * max(scale, 1e-300) or (scale == 0 and dmax < 1e-18), (kt, it, dmax, scale)
+
+
+def test_distance_bounds_bitwise(G, cfg1_mesh):
+    from oracle import assembly as OA
+
+    g = golden("blocks_cfg1.npz")
+    tmin, tmax = G[1].tri_distance_bounds(cfg1_mesh, g["bound_rows"])
+    assert np.array_equal(tmin, g["tmin_rows"]) and np.array_equal(tmax, g["tmax_rows"])
+    from paper_1503_07221_b200.mesh import jittered_cube
+
+    cube = jittered_cube(6, 0.05, 0)
+    t1, x1 = OA.tri_distance_bounds(cube)
+    t2, x2 = G[1].tri_distance_bounds(cube)
+    assert np.array_equal(t1, t2) and np.array_equal(x1, x2)
