@@ -299,8 +299,9 @@ __global__ void k_fill_items(long long E2, const long long* __restrict__ item_ba
 // ---------------------------------------------------------------------------
 struct QuadArgs {
   int E;
-  int fam_begin, fam_count;
-  const FamDev* fams;
+  int fam_count;
+  int fam_ids[kMaxFamilies];  // global family index of each launch family (frange slices)
+  const FamDev* fams;         // this launch's descriptors (coeff_off into `blob`)
   const double* blob;      // coefficients of the launch's families, concatenated
   int blob_doubles;
   int coef_in_smem;
@@ -318,26 +319,163 @@ struct QuadArgs {
   unsigned long long* n_in;
 };
 
-constexpr int kQuadWarps = 16;
+constexpr int kQuadWarps = 12;
 constexpr int kNK = kChunk / 32;
+constexpr int kBuckets = 256;
+// per-warp scratch: r, c, x1, x2, y1, y2 (FP64, r-sorted order) + bucket cursors
+constexpr int kWarpScratchBytes = 6 * kChunk * 8 + (kBuckets + 1) * 4 + 12;  // 16-byte multiple
+
+// ---- warp reduce-scatter (deterministic) -----------------------------------
+// Each level halves the value list: the lane with the level bit clear keeps
+// [0, h), the other [h, 2h); the kept half is summed with the partner's copy.
+// Every partial sum is formed by exactly one lane in a fixed order.
+template <int N, int O>
+__device__ __forceinline__ void rs_level(const double (&v)[N], double (&w)[(N + 1) / 2], bool hi) {
+  constexpr int H = (N + 1) / 2;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const double lo_v = v[i];
+    const double hi_v = (i + H < N) ? v[i + H] : 0.0;
+    const double send = hi ? lo_v : hi_v;
+    const double keep = hi ? hi_v : lo_v;
+    w[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+  }
+}
+
+template <int N>
+struct RS {
+  static constexpr int H1 = (N + 1) / 2, H2 = (H1 + 1) / 2, H3 = (H2 + 1) / 2, H4 = (H3 + 1) / 2,
+                       H5 = (H4 + 1) / 2;
+};
+
+// After the call the lane holds `valid` (<= RS<N>::H5) sums out[i] of value indices
+// base + i.  Odd list lengths are padded with zeros at every level; `valid` tracks
+// how many of the lane's kept values are real (pads never alias real indices).
+template <int N>
+__device__ __forceinline__ void warp_reduce_scatter(const double (&v)[N], int lane,
+                                                    double (&out)[RS<N>::H5], int& base, int& valid) {
+  double w1[RS<N>::H1], w2[RS<N>::H2], w3[RS<N>::H3], w4[RS<N>::H4];
+  rs_level<N, 16>(v, w1, lane & 16);
+  rs_level<RS<N>::H1, 8>(w1, w2, lane & 8);
+  rs_level<RS<N>::H2, 4>(w2, w3, lane & 4);
+  rs_level<RS<N>::H3, 2>(w3, w4, lane & 2);
+  rs_level<RS<N>::H4, 1>(w4, out, lane & 1);
+  const int H[5] = {RS<N>::H1, RS<N>::H2, RS<N>::H3, RS<N>::H4, RS<N>::H5};
+  int n = N, b = 0;
+#pragma unroll
+  for (int l = 0; l < 5; ++l) {
+    const bool hi = (lane >> (4 - l)) & 1;
+    if (hi) {
+      b += H[l];
+      n = n > H[l] ? n - H[l] : 0;
+    } else {
+      n = n < H[l] ? n : H[l];
+    }
+  }
+  base = b;
+  valid = n;
+}
+
+// ---- table evaluation (transposed layout [k][idx][t], t fastest) ------------
+// (psi_m, psi~_m) are the adjacent tables 2m, 2m+1: one 16-byte load per
+// Chebyshev coefficient for both.  Lanes of a warp evaluate r-sorted points, so
+// their subintervals idx are clustered and the loads coalesce to few wavefronts.
+template <int NT, int NSUB>
+__device__ __forceinline__ void clenshaw_pair(const double* __restrict__ cf, int nsub_rt, int idx,
+                                              int m, double x, double& v0, double& v1) {
+  const int nsub = NSUB > 0 ? NSUB : nsub_rt;
+  const double2* p = reinterpret_cast<const double2*>(cf + idx * NT + 2 * m);
+  const int stride = nsub * NT / 2;  // in double2
+  double2 c[kDeg + 1];
+#pragma unroll
+  for (int k = 0; k <= kDeg; ++k) c[k] = p[k * stride];
+  const double y = 2.0 * x;
+  double b1a = c[kDeg].x, b2a = 0.0, b1b = c[kDeg].y, b2b = 0.0;
+#pragma unroll
+  for (int k = kDeg - 1; k >= 1; --k) {
+    const double ta = fma(y, b1a, c[k].x - b2a);
+    const double tb = fma(y, b1b, c[k].y - b2b);
+    b2a = b1a;
+    b1a = ta;
+    b2b = b1b;
+    b1b = tb;
+  }
+  v0 = fma(x, b1a, c[0].x - b2a);
+  v1 = fma(x, b1b, c[0].y - b2b);
+}
+
+template <int P, int NSUB>
+__device__ __forceinline__ void eval_position(const FamDev& fd, const double* __restrict__ cf,
+                                              const double* __restrict__ sr, const double* __restrict__ sc,
+                                              const double* __restrict__ sx1, const double* __restrict__ sx2,
+                                              const double* __restrict__ sy1, const double* __restrict__ sy2,
+                                              int i0, int i1, double delta, int lane,
+                                              double (&acc)[10 * (P + 1) * (P + 1)], unsigned& n_act) {
+  constexpr int NM = (P + 1) * (P + 1);
+  constexpr int NT = 2 * NM;
+  const int nround = (i1 - i0 + 31) >> 5;
+  for (int rr = 0; rr < nround; ++rr) {
+    const int i = i0 + lane + 32 * rr;
+    const bool in = i < i1;
+    const double r = in ? sr[i] : 1e300;
+    const double av = r + delta;
+    const bool act = in && av >= fd.amin && av <= fd.amax;
+    n_act += __popc(__ballot_sync(0xffffffffu, act));
+    if (!act) continue;
+    const double c = sc[i];
+    const double x1 = sx1[i], x2 = sx2[i], y1 = sy1[i], y2 = sy2[i];
+    const double aa = fd.fold ? fabs(av) : av;
+    double x;
+    const int idx = cheb_locate(aa, fd.lo, fd.w, fd.inv_w, fd.nsub, x);
+    const bool neg = av < 0.0;
+    const double shx0 = 1.0 - x1, shx1 = x1 - x2;
+    const double shy0 = 1.0 - y1, shy1 = y1 - y2;
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+      double v0, v1;
+      clenshaw_pair<NT, NSUB>(cf, fd.nsub, idx, m, x, v0, v1);
+      if (fd.fold) {
+        v0 *= neg ? fd.sn[2 * m] : fd.sp[2 * m];
+        v1 *= neg ? fd.sn[2 * m + 1] : fd.sp[2 * m + 1];
+      }
+      const double cp = c * v0;
+      const double u0 = cp * shy0, u1 = cp * shy1, u2 = cp * y2;
+      double* S = acc + 10 * m;
+      S[0] = fma(u0, shx0, S[0]);
+      S[1] = fma(u0, shx1, S[1]);
+      S[2] = fma(u0, x2, S[2]);
+      S[3] = fma(u1, shx0, S[3]);
+      S[4] = fma(u1, shx1, S[4]);
+      S[5] = fma(u1, x2, S[5]);
+      S[6] = fma(u2, shx0, S[6]);
+      S[7] = fma(u2, shx1, S[7]);
+      S[8] = fma(u2, x2, S[8]);
+      S[9] = fma(c, v1, S[9]);
+    }
+  }
+}
 
 template <int P, bool SMEM_COEF>
 __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
   constexpr int NM = (P + 1) * (P + 1);
   constexpr int NACC = 10 * NM;
   extern __shared__ __align__(16) double smem[];
-  // layout: [fam descriptors][coef blob][per warp: r[256], c[256], list[256] bytes]
+  // layout: [fam descriptors][coef blob][per warp scratch]
   FamDev* sfam = reinterpret_cast<FamDev*>(smem);
-  double* sblob = smem + (sizeof(FamDev) * a.fam_count + 7) / 8;
-  double* swarp = sblob + (SMEM_COEF ? a.blob_doubles : 0);
+  double* sblob = smem + (sizeof(FamDev) * a.fam_count + 15) / 16 * 2;
+  char* swarp = reinterpret_cast<char*>(sblob + (SMEM_COEF ? (a.blob_doubles + 1) / 2 * 2 : 0));
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* sr = swarp + wid * (2 * kChunk + kChunk / 8);
+  double* sr = reinterpret_cast<double*>(swarp + (size_t)wid * kWarpScratchBytes);
   double* sc = sr + kChunk;
-  unsigned char* slist = reinterpret_cast<unsigned char*>(sc + kChunk);
+  double* sx1 = sc + kChunk;
+  double* sx2 = sx1 + kChunk;
+  double* sy1 = sx2 + kChunk;
+  double* sy2 = sy1 + kChunk;
+  unsigned* cur = reinterpret_cast<unsigned*>(sy2 + kChunk);  // kBuckets + 1
 
   {  // stage family descriptors and coefficients
     const int nwords = (int)((sizeof(FamDev) * a.fam_count + 7) / 8);
-    const double* src = reinterpret_cast<const double*>(a.fams + a.fam_begin);
+    const double* src = reinterpret_cast<const double*>(a.fams);
     for (int i = threadIdx.x; i < nwords; i += blockDim.x) smem[i] = src[i];
     if (SMEM_COEF)
       for (int i = threadIdx.x; i < a.blob_doubles; i += blockDim.x) sblob[i] = a.blob[i];
@@ -346,6 +484,7 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
   const double* coef_base = SMEM_COEF ? sblob : a.blob;
   const long long E2 = (long long)a.E * a.E;
   unsigned long long my_in = 0;
+  const unsigned lanemask_lt = (1u << lane) - 1u;
 
   while (true) {
     long long it;
@@ -354,6 +493,11 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
     if (it >= a.nitems) break;
     const int2 item = a.items[it];
     const int Pp = item.x, isub = item.y;
+    // any unit of this item in the launch's families?
+    bool any = false;
+    for (int fi = 0; fi < a.fam_count; ++fi)
+      any |= (a.frange[(long long)a.fam_ids[fi] * E2 + Pp].lo_cnt >> 16) != 0;
+    if (!any) continue;
     const int ey = Pp / a.E, ex = Pp % a.E;
     int lx[3], ly[3];
     const int cs = pair_topology(a.tri, ex, ey, lx, ly);
@@ -366,103 +510,128 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
              Y2 = corner(a.corners, ey, ly[2]);
     const V3 e1 = sub(X1, X0), e2 = sub(X2, X1), f1 = sub(Y1, Y0), f2 = sub(Y2, Y1);
     const double scale = kInv4Pi * a.a2[ex] * a.a2[ey];
-    double rk[kNK];
+    // geometry of this lane's points (q = lane + 32 k)
+    double rk[kNK], ck[kNK], px1[kNK], px2[kNK], py1[kNK], py2[kNK];
+    double rmin = 1e300, rmax = -1e300;
 #pragma unroll
     for (int k = 0; k < kNK; ++k) {
       const int q = lane + 32 * k;
-      double r = 1e300, c = 0.0;
+      rk[k] = 1e300;
+      ck[k] = px1[k] = px2[k] = py1[k] = py2[k] = 0.0;
       if (q < nq) {
         const long long g = q0 + q;
-        const double x1 = R.x1[g], x2 = R.x2[g], y1 = R.y1[g], y2 = R.y2[g];
-        const double dx = (X0.x + x1 * e1.x + x2 * e2.x) - (Y0.x + y1 * f1.x + y2 * f2.x);
-        const double dy = (X0.y + x1 * e1.y + x2 * e2.y) - (Y0.y + y1 * f1.y + y2 * f2.y);
-        const double dz = (X0.z + x1 * e1.z + x2 * e2.z) - (Y0.z + y1 * f1.z + y2 * f2.z);
-        r = sqrt(dx * dx + dy * dy + dz * dz);
-        c = scale * R.w[g] / r;
+        px1[k] = R.x1[g];
+        px2[k] = R.x2[g];
+        py1[k] = R.y1[g];
+        py2[k] = R.y2[g];
+        const double dx = (X0.x + px1[k] * e1.x + px2[k] * e2.x) - (Y0.x + py1[k] * f1.x + py2[k] * f2.x);
+        const double dy = (X0.y + px1[k] * e1.y + px2[k] * e2.y) - (Y0.y + py1[k] * f1.y + py2[k] * f2.y);
+        const double dz = (X0.z + px1[k] * e1.z + px2[k] * e2.z) - (Y0.z + py1[k] * f1.z + py2[k] * f2.z);
+        rk[k] = sqrt(dx * dx + dy * dy + dz * dz);
+        ck[k] = scale * R.w[g] / rk[k];
+        rmin = fmin(rmin, rk[k]);
+        rmax = fmax(rmax, rk[k]);
       }
-      rk[k] = r;
-      sr[q] = r;
-      sc[q] = c;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      rmin = fmin(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
+      rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    }
+    const double span = rmax - rmin;
+    const double inv_wb = span > 0.0 ? (double)kBuckets / span : 0.0;
+    // stable counting sort of the points by r bucket (deterministic)
+    for (int b = lane; b <= kBuckets; b += 32) cur[b] = 0u;
+    __syncwarp();
+    int bk[kNK];
+#pragma unroll
+    for (int k = 0; k < kNK; ++k) {
+      int b = kBuckets;  // invalid points last
+      if (lane + 32 * k < nq) b = min(kBuckets - 1, (int)((rk[k] - rmin) * inv_wb));
+      bk[k] = b;
+      atomicAdd(cur + b, 1u);
     }
     __syncwarp();
+    {  // exclusive scan of the counts (9 entries per lane, 288 >= 257)
+      unsigned loc[9], run = 0;
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        const int b = lane * 9 + t;
+        loc[t] = b <= kBuckets ? cur[b] : 0u;
+        run += loc[t];
+      }
+      unsigned incl = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      unsigned ex_ = incl - run;
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        const int b = lane * 9 + t;
+        if (b <= kBuckets) cur[b] = ex_;
+        ex_ += loc[t];
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kNK; ++k) {
+      const int b = bk[k];
+      const unsigned grp = __match_any_sync(0xffffffffu, b);
+      const unsigned pos = cur[b] + __popc(grp & lanemask_lt);
+      __syncwarp();
+      if ((grp & lanemask_lt) == 0) cur[b] += __popc(grp);
+      sr[pos] = rk[k];
+      sc[pos] = ck[k];
+      sx1[pos] = px1[k];
+      sx2[pos] = px2[k];
+      sy1[pos] = py1[k];
+      sy2[pos] = py2[k];
+      __syncwarp();
+    }
+    // now cur[b] = end of bucket b in the sorted arrays
     const int nunits = a.units[Pp];
     const long long slot0 = a.pair_base[Pp] + (long long)isub * nunits;
 
     for (int fi = 0; fi < a.fam_count; ++fi) {
-      const int fglob = a.fam_begin + fi;
-      const FRange fr = a.frange[(long long)fglob * E2 + Pp];
+      const FRange fr = a.frange[(long long)a.fam_ids[fi] * E2 + Pp];
       const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
       if (cnt == 0) continue;
       const FamDev& fd = sfam[fi];
       const double* cf = coef_base + fd.coeff_off;
-      const int tstride = fd.nsub * (kDeg + 1);
       for (int si = 0; si < cnt; ++si) {
         const int s = s_lo + si;
         const double delta = fd.delta[s];
-        // ballot compaction of the in-support points
-        int total = 0;
-#pragma unroll
-        for (int k = 0; k < kNK; ++k) {
-          const double av = rk[k] + delta;
-          const bool act = (av >= fd.amin) && (av <= fd.amax);
-          const unsigned m = __ballot_sync(0xffffffffu, act);
-          if (act) slist[total + __popc(m & ((1u << lane) - 1u))] = (unsigned char)(lane + 32 * k);
-          total += __popc(m);
+        // bucket range of r in [amin - delta, amax - delta] (monotone in r)
+        const double rlo = fd.amin - delta, rhi = fd.amax - delta;
+        int i0 = 0, i1 = 0;
+        if (rhi >= rmin && rlo <= rmax) {
+          const int blo = rlo <= rmin ? 0 : min(kBuckets - 1, (int)((rlo - rmin) * inv_wb));
+          const int bhi = rhi >= rmax ? kBuckets - 1 : min(kBuckets - 1, (int)((rhi - rmin) * inv_wb));
+          i0 = blo == 0 ? 0 : (int)cur[blo - 1];
+          i1 = (int)cur[bhi];
         }
-        __syncwarp();
-        my_in += total;
         double acc[NACC];
 #pragma unroll
         for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
-        for (int i = lane; i < total; i += 32) {
-          const int q = slist[i];
-          const double r = sr[q], c = sc[q];
-          const long long g = q0 + q;
-          const double x1 = R.x1[g], x2 = R.x2[g], y1 = R.y1[g], y2 = R.y2[g];
-          const double av = r + delta;
-          const double aa = fd.fold ? fabs(av) : av;
-          double x;
-          const int idx = cheb_locate(aa, fd.lo, fd.w, fd.inv_w, fd.nsub, x);
-          const bool neg = av < 0.0;
-          const double shx0 = 1.0 - x1, shx1 = x1 - x2;
-          const double shy0 = 1.0 - y1, shy1 = y1 - y2;
-#pragma unroll
-          for (int m = 0; m < NM; ++m) {
-            const double* c0 = cf + (2 * m) * tstride + idx * (kDeg + 1);
-            const double* c1 = c0 + tstride;
-            double v0, v1;
-            clenshaw2<kDeg>(c0, c1, x, x, v0, v1);
-            if (fd.fold) {
-              v0 *= neg ? fd.sn[2 * m] : fd.sp[2 * m];
-              v1 *= neg ? fd.sn[2 * m + 1] : fd.sp[2 * m + 1];
-            }
-            const double cp = c * v0;
-            const double u0 = cp * shy0, u1 = cp * shy1, u2 = cp * y2;
-            double* S = acc + 10 * m;
-            S[0] = fma(u0, shx0, S[0]);
-            S[1] = fma(u0, shx1, S[1]);
-            S[2] = fma(u0, x2, S[2]);
-            S[3] = fma(u1, shx0, S[3]);
-            S[4] = fma(u1, shx1, S[4]);
-            S[5] = fma(u1, x2, S[5]);
-            S[6] = fma(u2, shx0, S[6]);
-            S[7] = fma(u2, shx1, S[7]);
-            S[8] = fma(u2, x2, S[8]);
-            S[9] = fma(c, v1, S[9]);
-          }
+        unsigned n_act = 0;
+        switch (fd.nsub) {
+          case 16: eval_position<P, 16>(fd, cf, sr, sc, sx1, sx2, sy1, sy2, i0, i1, delta, lane, acc, n_act); break;
+          case 32: eval_position<P, 32>(fd, cf, sr, sc, sx1, sx2, sy1, sy2, i0, i1, delta, lane, acc, n_act); break;
+          case 64: eval_position<P, 64>(fd, cf, sr, sc, sx1, sx2, sy1, sy2, i0, i1, delta, lane, acc, n_act); break;
+          case 96: eval_position<P, 96>(fd, cf, sr, sc, sx1, sx2, sy1, sy2, i0, i1, delta, lane, acc, n_act); break;
+          default: eval_position<P, 0>(fd, cf, sr, sc, sx1, sx2, sy1, sy2, i0, i1, delta, lane, acc, n_act); break;
         }
-        double outv = 0.0;
+        my_in += n_act;
+        double outv[RS<NACC>::H5];
+        int base, valid;
+        warp_reduce_scatter<NACC>(acc, lane, outv, base, valid);
+        double* dst = a.part + (slot0 + fr.foff + si) * NACC;
 #pragma unroll
-        for (int k = 0; k < NACC; ++k) {
-          const double v = warp_allsum(acc[k]);
-          outv = (lane == (k & 31)) ? v : outv;
-          if ((k & 31) == 31 || k == NACC - 1) {
-            const int kb = k & ~31;
-            if (lane < NACC - kb && lane <= (k & 31))
-              a.part[(slot0 + fr.foff + si) * NACC + kb + lane] = outv;
-          }
-        }
-        __syncwarp();
+        for (int k = 0; k < RS<NACC>::H5; ++k)
+          if (k < valid) dst[base + k] = outv[k];
       }
     }
   }
@@ -793,9 +962,12 @@ struct AsmWorkspace {
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
   struct Launch {
-    int f0, f1;
-    bool in_smem;
-    size_t bytes, smem;
+    std::vector<int> fams;
+    bool in_smem = false;
+    size_t bytes = 0, smem = 0;
+    FamDev* d_fam = nullptr;
+    double* d_blob = nullptr;
+    int blob_doubles = 0;
   };
   std::vector<Launch> launches;
   std::vector<int> s_chunk;
@@ -816,6 +988,10 @@ struct AsmWorkspace {
     cudaFree(part);
     cudaFree(counters);
     cudaFree(cub_tmp);
+    for (auto& L : launches) {
+      cudaFree(L.d_fam);
+      cudaFree(L.d_blob);
+    }
     if (events)
       for (auto& e : ev) cudaEventDestroy(e);
   }
@@ -949,11 +1125,11 @@ int tdb_system_run_impl(TdbSystem* sys) {
   for (const auto& L : ws->launches) {
     QuadArgs qa;
     qa.E = (int)sys->E;
-    qa.fam_begin = L.f0;
-    qa.fam_count = L.f1 - L.f0;
-    qa.fams = sys->famdev;
-    qa.blob = ws->blob + ws->fam_blob_off[L.f0];
-    qa.blob_doubles = (int)(L.in_smem ? L.bytes / 8 : 0);
+    qa.fam_count = (int)L.fams.size();
+    for (int i = 0; i < qa.fam_count; ++i) qa.fam_ids[i] = L.fams[i];
+    qa.fams = L.d_fam;
+    qa.blob = L.d_blob;
+    qa.blob_doubles = L.in_smem ? L.blob_doubles : 0;
     qa.coef_in_smem = L.in_smem;
     qa.tri = sys->tri;
     qa.corners = sys->corners;
@@ -1100,10 +1276,14 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
     const int len = nt * fd.nsub * (kDeg + 1);
     ws->fam_blob_off[f] = (int)blob_all.size();
     ws->fam_blob_len[f] = len;
+    // transposed layout [c][sub][t]: the (psi_m, psi~_m) pair of one coefficient is one
+    // 16-byte load and r-sorted lanes read clustered subintervals
+    blob_all.resize(blob_all.size() + len);
+    double* dstb = blob_all.data() + ws->fam_blob_off[f];
     for (int t = 0; t < nt; ++t)
       for (int k = 0; k < fd.nsub; ++k)
         for (int c = 0; c <= kDeg; ++c)
-          blob_all.push_back(pk.coeffs[((size_t)t * pk.max_nsub + k) * (kDeg + 1) + c]);
+          dstb[((size_t)c * fd.nsub + k) * nt + t] = pk.coeffs[((size_t)t * pk.max_nsub + k) * (kDeg + 1) + c];
     fd.delta = fs.delta;
     fd.slo = fs.slo;
     fd.shi = fs.shi;
@@ -1144,25 +1324,50 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
   // ---- quadrature launch groups (families whose coefficients fit in smem) ----
   int max_smem = 0;
   TDB_CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-  const size_t warp_bytes = (size_t)kQuadWarps * (2 * kChunk * 8 + kChunk);
+  const size_t warp_bytes = (size_t)kQuadWarps * kWarpScratchBytes;
   const size_t budget = (size_t)max_smem - warp_bytes - sizeof(FamDev) * kMaxFamilies - 64;
-  for (int f0 = 0; f0 < F;) {
-    size_t bytes = 0;
-    int f1 = f0;
-    while (f1 < F && bytes + (size_t)ws->fam_blob_len[f1] * 8 <= budget)
-      bytes += (size_t)ws->fam_blob_len[f1++] * 8;
-    const bool in_smem = f1 > f0;
-    if (!in_smem) f1 = f0 + 1;
-    for (int f = f0; f < f1; ++f)
-      sys->famdev_host[f].coeff_off = ws->fam_blob_off[f] - ws->fam_blob_off[f0];
-    AsmWorkspace::Launch L;
-    L.f0 = f0;
-    L.f1 = f1;
-    L.in_smem = in_smem;
-    L.bytes = in_smem ? bytes : 0;
-    L.smem = ((sizeof(FamDev) * (f1 - f0) + 7) / 8) * 8 + L.bytes + warp_bytes;
-    ws->launches.push_back(L);
-    f0 = f1;
+  {
+    std::vector<int> order(F);
+    for (int f = 0; f < F; ++f) order[f] = f;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a_, int b_) { return sys->fam[a_].npos > sys->fam[b_].npos; });
+    std::vector<bool> used(F, false);
+    for (int oi = 0; oi < F; ++oi) {
+      const int f0 = order[oi];
+      if (used[f0]) continue;
+      // a launch starts with the largest unassigned family; smaller ones fill the rest
+      AsmWorkspace::Launch L;
+      size_t bytes = (size_t)ws->fam_blob_len[f0] * 8;
+      L.fams.push_back(f0);
+      used[f0] = true;
+      L.in_smem = bytes <= budget;
+      if (L.in_smem) {
+        for (int oj = oi + 1; oj < F; ++oj) {
+          const int f = order[oj];
+          const size_t fb = (size_t)ws->fam_blob_len[f] * 8;
+          if (!used[f] && bytes + fb <= budget && (int)L.fams.size() < kMaxFamilies) {
+            L.fams.push_back(f);
+            used[f] = true;
+            bytes += fb;
+          }
+        }
+      }
+      std::vector<FamDev> fdv;
+      std::vector<double> lb;
+      for (int f : L.fams) {
+        FamDev fd = sys->famdev_host[f];
+        fd.coeff_off = (int)lb.size();
+        lb.insert(lb.end(), blob_all.begin() + ws->fam_blob_off[f],
+                  blob_all.begin() + ws->fam_blob_off[f] + ws->fam_blob_len[f]);
+        fdv.push_back(fd);
+      }
+      L.blob_doubles = (int)lb.size();
+      L.bytes = L.in_smem ? bytes : 0;
+      if ((rc = dupload(&L.d_blob, lb.data(), lb.size(), st))) return rc;
+      if ((rc = dupload(&L.d_fam, fdv.data(), fdv.size(), st))) return rc;
+      L.smem = ((sizeof(FamDev) * L.fams.size() + 15) / 16) * 16 + (L.bytes + 15) / 16 * 16 + warp_bytes;
+      ws->launches.push_back(std::move(L));
+    }
   }
   if ((rc = dupload(&sys->famdev, sys->famdev_host.data(), F, st))) return rc;
 
