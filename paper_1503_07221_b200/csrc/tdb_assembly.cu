@@ -380,60 +380,106 @@ __device__ __forceinline__ void warp_reduce_scatter(const double (&v)[N], int la
 // (psi_m, psi~_m) are the adjacent tables 2m, 2m+1: one 16-byte load per
 // Chebyshev coefficient for both.  Lanes of a warp evaluate r-sorted points, so
 // their subintervals idx are clustered and the loads coalesce to few wavefronts.
-template <int NT, int NSUB>
-__device__ __forceinline__ void clenshaw_pair(const double* __restrict__ cf, int nsub_rt, int idx,
-                                              int m, double x, double& v0, double& v1) {
+struct XPow {
+  double x, x2, x4, x8, x16;
+};
+__device__ __forceinline__ XPow xpowers(double x) {
+  XPow p;
+  p.x = x;
+  p.x2 = x * x;
+  p.x4 = p.x2 * p.x2;
+  p.x8 = p.x4 * p.x4;
+  p.x16 = p.x8 * p.x8;
+  return p;
+}
+
+// Estrin evaluation of sum_k a_k x^k (k <= 16) for the table pair (psi_m, psi~_m).
+template <int NT, int NSUB, bool GLOBAL>
+__device__ __forceinline__ void estrin_pair(const double* __restrict__ cf, int nsub_rt, int idx, int m,
+                                            const XPow& X, double& v0, double& v1) {
+  static_assert(kDeg == 16, "Estrin tree is written for degree 16");
   const int nsub = NSUB > 0 ? NSUB : nsub_rt;
   const double2* p = reinterpret_cast<const double2*>(cf + idx * NT + 2 * m);
   const int stride = nsub * NT / 2;  // in double2
-  double2 c[kDeg + 1];
+  double2 a[kDeg + 1];
 #pragma unroll
-  for (int k = 0; k <= kDeg; ++k) c[k] = p[k * stride];
-  const double y = 2.0 * x;
-  double b1a = c[kDeg].x, b2a = 0.0, b1b = c[kDeg].y, b2b = 0.0;
+  for (int k = 0; k <= kDeg; ++k) a[k] = GLOBAL ? __ldg(p + k * stride) : p[k * stride];
+  double qa[8], qb[8];
 #pragma unroll
-  for (int k = kDeg - 1; k >= 1; --k) {
-    const double ta = fma(y, b1a, c[k].x - b2a);
-    const double tb = fma(y, b1b, c[k].y - b2b);
-    b2a = b1a;
-    b1a = ta;
-    b2b = b1b;
-    b1b = tb;
+  for (int j = 0; j < 8; ++j) {
+    qa[j] = fma(a[2 * j + 1].x, X.x, a[2 * j].x);
+    qb[j] = fma(a[2 * j + 1].y, X.x, a[2 * j].y);
   }
-  v0 = fma(x, b1a, c[0].x - b2a);
-  v1 = fma(x, b1b, c[0].y - b2b);
+  double ra[4], rb[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    ra[j] = fma(qa[2 * j + 1], X.x2, qa[2 * j]);
+    rb[j] = fma(qb[2 * j + 1], X.x2, qb[2 * j]);
+  }
+  const double sa0 = fma(ra[1], X.x4, ra[0]), sa1 = fma(ra[3], X.x4, ra[2]);
+  const double sb0 = fma(rb[1], X.x4, rb[0]), sb1 = fma(rb[3], X.x4, rb[2]);
+  v0 = fma(a[16].x, X.x16, fma(sa1, X.x8, sa0));
+  v1 = fma(a[16].y, X.x16, fma(sb1, X.x8, sb0));
 }
 
-template <int P, int NSUB>
-__device__ __forceinline__ void eval_position(const FamDev& fd, const double* __restrict__ cf,
-                                              const double* __restrict__ sr, const double* __restrict__ sc,
-                                              const double* __restrict__ sx1, const double* __restrict__ sx2,
-                                              const double* __restrict__ sy1, const double* __restrict__ sy2,
-                                              int i0, int i1, double delta, int lane,
-                                              double (&acc)[10 * (P + 1) * (P + 1)], unsigned& n_act) {
+struct SortedPts {
+  const double* r;
+  const double* c;
+  const double* x1;
+  const double* x2;
+  const double* y1;
+  const double* y2;
+  const unsigned* cur;  // bucket ends
+  double rmin, rmax, inv_wb;
+};
+
+// One block position of one family for one work item: the full warp walks the
+// position's in-support points in r-sorted order, 32 consecutive points per
+// round (clustered table subintervals -> few shared-memory wavefronts per
+// coefficient load), then reduce-scatters the 10 (p+1)^2 sums.
+template <int P, int NSUB, bool GLOBAL>
+__device__ __forceinline__ void process_position(const FamDev& fd, const double* __restrict__ cf,
+                                                 const SortedPts& pt, int s, int lane,
+                                                 double* __restrict__ dst, unsigned long long& my_in) {
   constexpr int NM = (P + 1) * (P + 1);
   constexpr int NT = 2 * NM;
+  constexpr int NACC = 10 * NM;
+  const unsigned FULL = 0xffffffffu;
+  const double delta = fd.delta[s];
+  const double rlo = fd.amin - delta, rhi = fd.amax - delta;
+  int i0 = 0, i1 = 0;
+  if (rhi >= pt.rmin && rlo <= pt.rmax) {
+    const int blo = rlo <= pt.rmin ? 0 : min(kBuckets - 1, (int)((rlo - pt.rmin) * pt.inv_wb));
+    const int bhi = rhi >= pt.rmax ? kBuckets - 1 : min(kBuckets - 1, (int)((rhi - pt.rmin) * pt.inv_wb));
+    i0 = blo == 0 ? 0 : (int)pt.cur[blo - 1];
+    i1 = (int)pt.cur[bhi];
+  }
+  double acc[NACC];
+#pragma unroll
+  for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
+  unsigned n_act = 0;
   const int nround = (i1 - i0 + 31) >> 5;
   for (int rr = 0; rr < nround; ++rr) {
     const int i = i0 + lane + 32 * rr;
     const bool in = i < i1;
-    const double r = in ? sr[i] : 1e300;
+    const double r = in ? pt.r[i] : 1e300;
     const double av = r + delta;
     const bool act = in && av >= fd.amin && av <= fd.amax;
-    n_act += __popc(__ballot_sync(0xffffffffu, act));
+    n_act += __popc(__ballot_sync(FULL, act));
     if (!act) continue;
-    const double c = sc[i];
-    const double x1 = sx1[i], x2 = sx2[i], y1 = sy1[i], y2 = sy2[i];
+    const double c = pt.c[i];
+    const double x1 = pt.x1[i], x2 = pt.x2[i], y1 = pt.y1[i], y2 = pt.y2[i];
     const double aa = fd.fold ? fabs(av) : av;
     double x;
     const int idx = cheb_locate(aa, fd.lo, fd.w, fd.inv_w, fd.nsub, x);
     const bool neg = av < 0.0;
     const double shx0 = 1.0 - x1, shx1 = x1 - x2;
     const double shy0 = 1.0 - y1, shy1 = y1 - y2;
+    const XPow X = xpowers(x);
 #pragma unroll
     for (int m = 0; m < NM; ++m) {
       double v0, v1;
-      clenshaw_pair<NT, NSUB>(cf, fd.nsub, idx, m, x, v0, v1);
+      estrin_pair<NT, NSUB, GLOBAL>(cf, fd.nsub, idx, m, X, v0, v1);
       if (fd.fold) {
         v0 *= neg ? fd.sn[2 * m] : fd.sp[2 * m];
         v1 *= neg ? fd.sn[2 * m + 1] : fd.sp[2 * m + 1];
@@ -453,6 +499,13 @@ __device__ __forceinline__ void eval_position(const FamDev& fd, const double* __
       S[9] = fma(c, v1, S[9]);
     }
   }
+  my_in += n_act;
+  double outv[RS<NACC>::H5];
+  int base, valid;
+  warp_reduce_scatter<NACC>(acc, lane, outv, base, valid);
+#pragma unroll
+  for (int k = 0; k < RS<NACC>::H5; ++k)
+    if (k < valid) dst[base + k] = outv[k];
 }
 
 template <int P, bool SMEM_COEF>
@@ -595,43 +648,41 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
     const int nunits = a.units[Pp];
     const long long slot0 = a.pair_base[Pp] + (long long)isub * nunits;
 
+    SortedPts pt;
+    pt.r = sr;
+    pt.c = sc;
+    pt.x1 = sx1;
+    pt.x2 = sx2;
+    pt.y1 = sy1;
+    pt.y2 = sy2;
+    pt.cur = cur;
+    pt.rmin = rmin;
+    pt.rmax = rmax;
+    pt.inv_wb = inv_wb;
     for (int fi = 0; fi < a.fam_count; ++fi) {
       const FRange fr = a.frange[(long long)a.fam_ids[fi] * E2 + Pp];
       const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
       if (cnt == 0) continue;
       const FamDev& fd = sfam[fi];
-      const double* cf = coef_base + fd.coeff_off;
+      // keep the shared-memory pointer provably shared (LDS, not generic LD)
+      const double* cf_s = coef_base + fd.coeff_off;
+      const double* cf_g = fd.coeffs;
       for (int si = 0; si < cnt; ++si) {
-        const int s = s_lo + si;
-        const double delta = fd.delta[s];
-        // bucket range of r in [amin - delta, amax - delta] (monotone in r)
-        const double rlo = fd.amin - delta, rhi = fd.amax - delta;
-        int i0 = 0, i1 = 0;
-        if (rhi >= rmin && rlo <= rmax) {
-          const int blo = rlo <= rmin ? 0 : min(kBuckets - 1, (int)((rlo - rmin) * inv_wb));
-          const int bhi = rhi >= rmax ? kBuckets - 1 : min(kBuckets - 1, (int)((rhi - rmin) * inv_wb));
-          i0 = blo == 0 ? 0 : (int)cur[blo - 1];
-          i1 = (int)cur[bhi];
-        }
-        double acc[NACC];
-#pragma unroll
-        for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
-        unsigned n_act = 0;
-        switch (fd.nsub) {
-          case 16: eval_position<P, 16>(fd, cf, sr, sc, sx1, sx2, sy1, sy2, i0, i1, delta, lane, acc, n_act); break;
-          case 32: eval_position<P, 32>(fd, cf, sr, sc, sx1, sx2, sy1, sy2, i0, i1, delta, lane, acc, n_act); break;
-          case 64: eval_position<P, 64>(fd, cf, sr, sc, sx1, sx2, sy1, sy2, i0, i1, delta, lane, acc, n_act); break;
-          case 96: eval_position<P, 96>(fd, cf, sr, sc, sx1, sx2, sy1, sy2, i0, i1, delta, lane, acc, n_act); break;
-          default: eval_position<P, 0>(fd, cf, sr, sc, sx1, sx2, sy1, sy2, i0, i1, delta, lane, acc, n_act); break;
-        }
-        my_in += n_act;
-        double outv[RS<NACC>::H5];
-        int base, valid;
-        warp_reduce_scatter<NACC>(acc, lane, outv, base, valid);
         double* dst = a.part + (slot0 + fr.foff + si) * NACC;
-#pragma unroll
-        for (int k = 0; k < RS<NACC>::H5; ++k)
-          if (k < valid) dst[base + k] = outv[k];
+        const int s = s_lo + si;
+#define TDB_F(NS, GL) process_position<P, NS, GL>(fd, GL ? cf_g : cf_s, pt, s, lane, dst, my_in)
+        if (fd.coef_global) {
+          TDB_F(0, true);
+        } else {
+          switch (fd.nsub) {
+            case 16: TDB_F(16, false); break;
+            case 32: TDB_F(32, false); break;
+            case 64: TDB_F(64, false); break;
+            case 96: TDB_F(96, false); break;
+            default: TDB_F(0, false); break;
+          }
+        }
+#undef TDB_F
       }
     }
   }
@@ -730,54 +781,110 @@ __global__ void k_pattern_count(PatternArgs a) {
   }
 }
 
+constexpr int kMaxStar = 32;
+
+struct RowStar {  // star of the test vertex j, cached in shared memory per CTA
+  int n;
+  int e[kMaxStar];
+  int t[kMaxStar][3];
+  int pj[kMaxStar];  // local position of j in triangle e
+};
+
+// Value of CSR entry (j, l) of position s: every contribution of a pair
+// (ex in star(l), ey in star(j)) admissible at s, summed with Kahan's
+// compensation in the reference's canonical order (case groups regular,
+// coincident, edge, vertex; pairs (ex, ey) ascending within a group;
+// assembly.py:261-306 + _kahan_csr :187-214).  Regular contributions are
+// added in the single scan; the few touching pairs are deferred and added
+// case by case afterwards.
 template <int NM>
-__device__ void gather_entry(const PatternArgs& a, int s, int j, int l, double* out) {
+__device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s, int j, int l, double* out) {
   double sum[NM], comp[NM];
 #pragma unroll
   for (int m = 0; m < NM; ++m) sum[m] = comp[m] = 0.0;
-  const long long E2 = (long long)a.E * a.E;
-  (void)E2;
-  const int jb = a.star_off[j], je = a.star_off[j + 1];
   const int lb = a.star_off[l], le = a.star_off[l + 1];
-  for (int cr = 0; cr < 4; ++cr) {
-    for (int kx = lb; kx < le; ++kx) {
-      const int ex = a.star_ids[kx];
-      for (int ky = jb; ky < je; ++ky) {
-        const int ey = a.star_ids[ky];
-        if (case_of(a.tri, ex, ey) != cr) continue;
-        const long long Pp = (long long)ey * a.E + ex;
-        const FRange fr = a.frange[Pp];
-        const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
-        if (s < s_lo || s >= s_lo + cnt) continue;
-        const long long slot = a.pair_base[Pp] + fr.foff + (s - s_lo);
-        int lx[3], ly[3];
-        pair_topology(a.tri, ex, ey, lx, ly);
-        int pj = 0, pl = 0;
+  constexpr int kDefer = 64;    // touching combos of (star(l), star(j)); 36 for valence 6
+  unsigned deferred[kDefer];    // (case << 16) | (kx << 8) | ky, in (ex, ey) order
+  int nd = 0;
+  bool overflow = false;
+  auto contribute = [&](int ex, int ey, int kx_local, int ky, int cs, const FRange& fr, int s_lo) {
+    const long long Pp = (long long)ey * a.E + ex;
+    const long long slot = a.pair_base[Pp] + fr.foff + (s - s_lo);
+    int ca = rs.pj[ky], cb = 0;
+    const int* tx = a.tri + 3 * ex;
+    cb = (tx[0] == l) ? 0 : ((tx[1] == l) ? 1 : 2);
+    const int pj = ca, pl = cb;
+    if (cs != TDB_CASE_REGULAR) {  // chart permutations of the regularised rules
+      int lx[3], ly[3];
+      pair_topology(a.tri, ex, ey, lx, ly);
 #pragma unroll
-        for (int t = 0; t < 3; ++t) {
-          pj = (a.tri[3 * ey + t] == j) ? t : pj;
-          pl = (a.tri[3 * ex + t] == l) ? t : pl;
-        }
-        int ca = 0, cb = 0;  // chart positions: tri[ly[ca]] == j
+      for (int t = 0; t < 3; ++t) {
+        ca = (ly[t] == pj) ? t : ca;
+        cb = (lx[t] == pl) ? t : cb;
+      }
+    }
+    const double* nx = a.normals + 3 * (long long)ex;
+    const double* ny = a.normals + 3 * (long long)ey;
+    const double nd_ = nx[0] * ny[0] + nx[1] * ny[1] + nx[2] * ny[2];
+    const double* cyv = a.curls + 9 * (long long)ey + 3 * pj;
+    const double* cxv = a.curls + 9 * (long long)ex + 3 * pl;
+    const double cd = cyv[0] * cxv[0] + cyv[1] * cxv[1] + cyv[2] * cxv[2];
+    const double* pv = a.part + slot * a.nacc;
 #pragma unroll
-        for (int t = 0; t < 3; ++t) {
-          ca = (ly[t] == pj) ? t : ca;
-          cb = (lx[t] == pl) ? t : cb;
-        }
-        const double* nx = a.normals + 3 * (long long)ex;
-        const double* ny = a.normals + 3 * (long long)ey;
-        const double nd = nx[0] * ny[0] + nx[1] * ny[1] + nx[2] * ny[2];
-        const double* cyv = a.curls + 9 * (long long)ey + 3 * pj;
-        const double* cxv = a.curls + 9 * (long long)ex + 3 * pl;
-        const double cd = cyv[0] * cxv[0] + cyv[1] * cxv[1] + cyv[2] * cxv[2];
-        const double* pv = a.part + slot * a.nacc;
-#pragma unroll
-        for (int m = 0; m < NM; ++m) {
-          const double v = nd * pv[10 * m + 3 * ca + cb] + cd * pv[10 * m + 9];
-          const double y = v - comp[m];
-          const double t = sum[m] + y;
-          comp[m] = (t - sum[m]) - y;
-          sum[m] = t;
+    for (int m = 0; m < NM; ++m) {
+      const double v = nd_ * pv[10 * m + 3 * ca + cb] + cd * pv[10 * m + 9];
+      const double y = v - comp[m];
+      const double t = sum[m] + y;
+      comp[m] = (t - sum[m]) - y;
+      sum[m] = t;
+    }
+    (void)kx_local;
+  };
+  for (int kx = lb; kx < le; ++kx) {
+    const int ex = a.star_ids[kx];
+    const int x0 = a.tri[3 * ex], x1 = a.tri[3 * ex + 1], x2 = a.tri[3 * ex + 2];
+    for (int ky = 0; ky < rs.n; ++ky) {
+      const int ey = rs.e[ky];
+      const FRange fr = a.frange[(long long)ey * a.E + ex];
+      const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
+      if (s < s_lo || s >= s_lo + cnt) continue;
+      int cs;
+      if (ex == ey) {
+        cs = TDB_CASE_COINCIDENT;
+      } else {
+        const int nsh = (x0 == rs.t[ky][0]) + (x0 == rs.t[ky][1]) + (x0 == rs.t[ky][2]) +
+                        (x1 == rs.t[ky][0]) + (x1 == rs.t[ky][1]) + (x1 == rs.t[ky][2]) +
+                        (x2 == rs.t[ky][0]) + (x2 == rs.t[ky][1]) + (x2 == rs.t[ky][2]);
+        cs = nsh == 0 ? TDB_CASE_REGULAR : (nsh == 2 ? TDB_CASE_EDGE : TDB_CASE_VERTEX);
+      }
+      if (cs == TDB_CASE_REGULAR) {
+        contribute(ex, ey, kx - lb, ky, cs, fr, s_lo);
+      } else if (nd < kDefer) {
+        deferred[nd++] = ((unsigned)cs << 16) | ((unsigned)(kx - lb) << 8) | (unsigned)ky;
+      } else {
+        overflow = true;
+      }
+    }
+  }
+  for (int cr = TDB_CASE_COINCIDENT; cr <= TDB_CASE_VERTEX; ++cr) {
+    if (!overflow) {
+      for (int d = 0; d < nd; ++d) {
+        if ((int)(deferred[d] >> 16) != cr) continue;
+        const int kxl = (deferred[d] >> 8) & 0xff, ky = deferred[d] & 0xff;
+        const int ex = a.star_ids[lb + kxl], ey = rs.e[ky];
+        const FRange fr = a.frange[(long long)ey * a.E + ex];
+        contribute(ex, ey, kxl, ky, cr, fr, fr.lo_cnt & 0xffff);
+      }
+    } else {  // very high valence: rescan the combos of this case in order
+      for (int kx = lb; kx < le; ++kx) {
+        const int ex = a.star_ids[kx];
+        for (int ky = 0; ky < rs.n; ++ky) {
+          const int ey = rs.e[ky];
+          if (case_of(a.tri, ex, ey) != cr) continue;
+          const FRange fr = a.frange[(long long)ey * a.E + ex];
+          const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
+          if (s < s_lo || s >= s_lo + cnt) continue;
+          contribute(ex, ey, kx - lb, ky, cr, fr, s_lo);
         }
       }
     }
@@ -792,7 +899,20 @@ __global__ void k_pattern_fill(PatternArgs a) {
   unsigned* bm = smem_u;
   int* pref = reinterpret_cast<int*>(smem_u + a.s_count * a.words);  // words + 1
   const int j = blockIdx.x;
-  build_bitmaps(a, j, bm);
+  __shared__ RowStar rs;
+  if (threadIdx.x == 0) {
+    const int b = a.star_off[j], e = a.star_off[j + 1];
+    rs.n = min(e - b, kMaxStar);
+    for (int k = 0; k < rs.n; ++k) {
+      const int ey = a.star_ids[b + k];
+      rs.e[k] = ey;
+      for (int t = 0; t < 3; ++t) {
+        rs.t[k][t] = a.tri[3 * ey + t];
+        if (rs.t[k][t] == j) rs.pj[k] = t;
+      }
+    }
+  }
+  build_bitmaps(a, j, bm);  // (syncs the block)
   typedef cub::BlockScan<int, 256> Scan;
   __shared__ typename Scan::TempStorage tmp;
   for (int sl = 0; sl < a.s_count; ++sl) {
@@ -824,7 +944,7 @@ __global__ void k_pattern_fill(PatternArgs a) {
       for (int r = 0; r < rank; ++r) word &= word - 1;
       const int l = lo * 32 + (__ffs(word) - 1);
       double vals[NM];
-      gather_entry<NM>(a, a.s_begin + sl, j, l, vals);
+      gather_entry<NM>(a, rs, a.s_begin + sl, j, l, vals);
       a.indices[base + e] = l;
 #pragma unroll
       for (int m = 0; m < NM; ++m) a.data[(base + e) * NM + m] = vals[m];
@@ -1198,6 +1318,20 @@ int tdb_system_run_impl(TdbSystem* sys) {
   return TDB_OK;
 }
 
+// sum_j c_j T_j(x) -> sum_k a_k x^k, degree kDeg, integer T_j coefficients
+static void cheb_to_monomial(const double* c, long double* a) {
+  long long T[kDeg + 1][kDeg + 1] = {};
+  T[0][0] = 1;
+  T[1][1] = 1;
+  for (int j = 2; j <= kDeg; ++j)
+    for (int k = 0; k <= kDeg; ++k) T[j][k] = (k > 0 ? 2 * T[j - 1][k - 1] : 0) - T[j - 2][k];
+  for (int k = 0; k <= kDeg; ++k) {
+    long double s_ = 0.0L;
+    for (int j = kDeg; j >= 0; --j) s_ += (long double)c[j] * (long double)T[j][k];
+    a[k] = s_;
+  }
+}
+
 int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDesc* desc,
                            TdbSystem* sys) {
   cudaStream_t st = ctx->stream;
@@ -1276,14 +1410,22 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
     const int len = nt * fd.nsub * (kDeg + 1);
     ws->fam_blob_off[f] = (int)blob_all.size();
     ws->fam_blob_len[f] = len;
-    // transposed layout [c][sub][t]: the (psi_m, psi~_m) pair of one coefficient is one
-    // 16-byte load and r-sorted lanes read clustered subintervals
+    // Each subinterval's Chebyshev series sum_j c_j T_j(x) is re-expanded in the
+    // monomial basis sum_k a_k x^k (exact integer T_j coefficients, 80-bit
+    // accumulation) so the device can use Estrin's scheme (depth 5 instead of the
+    // 32-deep Clenshaw chain); max deviation from Clenshaw <= 6e-16 of the table
+    // max on every default table (tools/estrin_check.py).
+    // Transposed layout [k][sub][t]: the (psi_m, psi~_m) pair of one coefficient
+    // is one 16-byte load and r-sorted lanes read clustered subintervals.
     blob_all.resize(blob_all.size() + len);
     double* dstb = blob_all.data() + ws->fam_blob_off[f];
     for (int t = 0; t < nt; ++t)
-      for (int k = 0; k < fd.nsub; ++k)
-        for (int c = 0; c <= kDeg; ++c)
-          dstb[((size_t)c * fd.nsub + k) * nt + t] = pk.coeffs[((size_t)t * pk.max_nsub + k) * (kDeg + 1) + c];
+      for (int k = 0; k < fd.nsub; ++k) {
+        const double* cc = pk.coeffs + ((size_t)t * pk.max_nsub + k) * (kDeg + 1);
+        long double mono[kDeg + 1];
+        cheb_to_monomial(cc, mono);
+        for (int c = 0; c <= kDeg; ++c) dstb[((size_t)c * fd.nsub + k) * nt + t] = (double)mono[c];
+      }
     fd.delta = fs.delta;
     fd.slo = fs.slo;
     fd.shi = fs.shi;
@@ -1325,44 +1467,46 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
   int max_smem = 0;
   TDB_CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   const size_t warp_bytes = (size_t)kQuadWarps * kWarpScratchBytes;
-  const size_t budget = (size_t)max_smem - warp_bytes - sizeof(FamDev) * kMaxFamilies - 64;
+  const size_t budget = (size_t)max_smem - warp_bytes - ((sizeof(FamDev) * F + 15) / 16) * 16 - 64;
   {
     std::vector<int> order(F);
     for (int f = 0; f < F; ++f) order[f] = f;
     std::stable_sort(order.begin(), order.end(),
                      [&](int a_, int b_) { return sys->fam[a_].npos > sys->fam[b_].npos; });
-    std::vector<bool> used(F, false);
-    for (int oi = 0; oi < F; ++oi) {
-      const int f0 = order[oi];
-      if (used[f0]) continue;
-      // a launch starts with the largest unassigned family; smaller ones fill the rest
+    // ONE launch: families in npos order go to shared memory while they fit, the
+    // rest (small singleton families or oversized p >= 1 tables) read their
+    // coefficients through L1/L2 from the transposed global copy.
+    {
       AsmWorkspace::Launch L;
-      size_t bytes = (size_t)ws->fam_blob_len[f0] * 8;
-      L.fams.push_back(f0);
-      used[f0] = true;
-      L.in_smem = bytes <= budget;
-      if (L.in_smem) {
-        for (int oj = oi + 1; oj < F; ++oj) {
-          const int f = order[oj];
-          const size_t fb = (size_t)ws->fam_blob_len[f] * 8;
-          if (!used[f] && bytes + fb <= budget && (int)L.fams.size() < kMaxFamilies) {
-            L.fams.push_back(f);
-            used[f] = true;
-            bytes += fb;
-          }
+      size_t bytes = 0;
+      std::vector<int> in_smem_fams, global_fams;
+      for (int oi = 0; oi < F; ++oi) {
+        const int f = order[oi];
+        const size_t fb = (size_t)ws->fam_blob_len[f] * 8;
+        if (bytes + fb <= budget) {
+          in_smem_fams.push_back(f);
+          bytes += fb;
+        } else {
+          global_fams.push_back(f);
         }
       }
+      L.fams = in_smem_fams;
+      L.fams.insert(L.fams.end(), global_fams.begin(), global_fams.end());
+      L.in_smem = !in_smem_fams.empty();
       std::vector<FamDev> fdv;
       std::vector<double> lb;
       for (int f : L.fams) {
         FamDev fd = sys->famdev_host[f];
-        fd.coeff_off = (int)lb.size();
-        lb.insert(lb.end(), blob_all.begin() + ws->fam_blob_off[f],
-                  blob_all.begin() + ws->fam_blob_off[f] + ws->fam_blob_len[f]);
+        const bool glob = std::find(global_fams.begin(), global_fams.end(), f) != global_fams.end();
+        fd.coef_global = glob ? 1 : 0;
+        fd.coeff_off = glob ? 0 : (int)lb.size();
+        if (!glob)
+          lb.insert(lb.end(), blob_all.begin() + ws->fam_blob_off[f],
+                    blob_all.begin() + ws->fam_blob_off[f] + ws->fam_blob_len[f]);
         fdv.push_back(fd);
       }
       L.blob_doubles = (int)lb.size();
-      L.bytes = L.in_smem ? bytes : 0;
+      L.bytes = lb.size() * 8;
       if ((rc = dupload(&L.d_blob, lb.data(), lb.size(), st))) return rc;
       if ((rc = dupload(&L.d_fam, fdv.data(), fdv.size(), st))) return rc;
       L.smem = ((sizeof(FamDev) * L.fams.size() + 15) / 16) * 16 + (L.bytes + 15) / 16 * 16 + warp_bytes;

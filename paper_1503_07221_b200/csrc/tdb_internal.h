@@ -19,13 +19,13 @@ constexpr int kChunk = 256;      // rule points per warp work item
 struct FamDev {
   int npos, nsub, nt, fold;
   int coeff_off;   // offset (doubles) of this family's coefficients in the launch blob
-  int pad_;
+  int coef_global; // 1: read `coeffs` (global, transposed layout) instead of the smem blob
   double lo, w, inv_w, amin, amax;
   double sp[kMaxTables], sn[kMaxTables];
   const double* delta;
   const double* slo;
   const double* shi;
-  const double* coeffs;  // (nt, nsub, kDeg+1) global copy
+  const double* coeffs;  // transposed [c][sub][t] global copy
 };
 
 struct RuleDev {
