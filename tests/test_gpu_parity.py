@@ -212,3 +212,47 @@ def test_distance_bounds_bitwise(G, cfg1_mesh):
     t1, x1 = OA.tri_distance_bounds(cube)
     t2, x2 = G[1].tri_distance_bounds(cube)
     assert np.array_equal(t1, t2) and np.array_equal(x1, x2)
+
+
+def test_device_solvers_two_tri(G, two_tri):
+    import torch
+
+    from paper_1503_07221_b200.solvers import SolverConfig, dgmres, fgmres, gmres, recursive_preconditioner
+    from paper_1503_07221_b200.temporal_basis import TimeGrid
+
+    g = golden("solvers.npz")
+    dense = golden("blocks_two_tri_N6_p1.npz")["dense"]
+    A = G[2].assemble_system(two_tri, TimeGrid(T=3.0, N=6, p=1))
+    b = torch.as_tensor(g["b9"]).cuda()
+    xd = np.linalg.solve(dense, g["b9"])
+    Av = lambda v: A.matvec(v)
+    cfg = SolverConfig(restart=40, tol=1e-12, max_iter=4000, recursion_depth=2, inner_iterations=(2, 6))
+    x, hist = fgmres(Av, b, cfg, precond=recursive_preconditioner(A, cfg))
+    assert hist[-1] <= 1e-12
+    assert np.linalg.norm(x.cpu().numpy() - xd) <= 1e-8 * np.linalg.norm(xd)
+    x, hist = gmres(Av, b, SolverConfig(restart=40, tol=1e-12, max_iter=4000))
+    assert np.linalg.norm(x.cpu().numpy() - xd) <= 1e-8 * np.linalg.norm(xd)
+    x, hist, st = dgmres(Av, b, SolverConfig(restart=20, tol=1e-12, max_iter=4000, deflate_per_restart=2,
+                                             max_deflation=8))
+    assert np.linalg.norm(x.cpu().numpy() - g["dgm_x"]) <= 1e-8 * np.linalg.norm(g["dgm_x"])
+    assert st.rank == int(g["dgm_rank"][0])
+
+
+def test_device_fgmres_recursive_cfg1_vs_direct(G, cfg1_mesh):
+    # config 1 system (E=320, N=40, p=0, L*M = 6480): FGMRES(50, 2(2,10)) at eps=1e-12 vs a
+    # dense direct solve of the same assembled matrix (SURVEY 8d solve-parity protocol)
+    import torch
+
+    from paper_1503_07221_b200.solvers import SolverConfig, solve
+    from paper_1503_07221_b200.temporal_basis import TimeGrid
+
+    grid = TimeGrid(T=3.9, N=40, p=0)
+    A = G[2].assemble_system(cfg1_mesh, grid)
+    dense = G[2].reconstruct_dense(A)
+    b = np.random.default_rng(7).standard_normal(A.shape[0])
+    xd = np.linalg.solve(dense, b)
+    cfg = SolverConfig(method="fgmres-recursive", restart=50, tol=1e-12, max_iter=2000, recursion_depth=2,
+                       inner_iterations=(2, 10))
+    x, hist = solve(A, b, cfg)
+    assert hist[-1] <= 1e-12
+    assert np.linalg.norm(x - xd) <= 1e-8 * np.linalg.norm(xd)
