@@ -342,11 +342,25 @@ class DeviceAssembly:
             self.handle = None
 
 
+def as_product_inputs(mesh, grid):
+    """Accept the reference's SurfaceMesh / TimeGrid (or any look-alike) as well as ours."""
+    if not isinstance(mesh, SurfaceMesh):
+        mesh = SurfaceMesh(np.asarray(mesh.vertices), np.asarray(mesh.triangles))
+    if not isinstance(grid, TimeGrid):
+        grid = TimeGrid(T=float(grid.T), N=int(grid.N), p=int(grid.p))
+    return mesh, grid
+
+
+def _as_tables(tables, grid):
+    """Reference PrototypeTables work as-is (same attributes); None -> our cache."""
+    return tables_for(grid) if tables is None else tables
+
+
 def assemble_subblocks(mesh: SurfaceMesh, grid: TimeGrid, tables: PrototypeTables, kt: int, it: int,
                        config: QuadratureConfig = QuadratureConfig()):
     """All (p+1) x (p+1) CSR sub-blocks of block position (kt, it) (device assembly)."""
-    if tables is None:
-        tables = tables_for(grid)
+    mesh, grid = as_product_inputs(mesh, grid)
+    tables = _as_tables(tables, grid)
     plan = build_plan(mesh, grid, tables, [(kt, it)], config)
     dev = DeviceAssembly(mesh, plan)
     return dev.position_blocks(kt, it)

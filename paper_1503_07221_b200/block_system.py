@@ -299,6 +299,9 @@ def assemble_system(mesh: SurfaceMesh, grid: TimeGrid, tables: PrototypeTables |
                     config: QuadratureConfig = QuadratureConfig(), plan: DistributionPlan | None = None,
                     workers: int | None = None, device: int | None = None) -> BlockHessenbergMatrix:
     """Assemble every canonical block position on the GPU (values independent of `workers`)."""
+    from .assembly import as_product_inputs
+
+    mesh, grid = as_product_inputs(mesh, grid)
     if workers is None:
         workers = int(os.environ.get("TDBEM_WORKERS", "1"))
     if plan is None:

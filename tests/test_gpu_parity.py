@@ -256,3 +256,14 @@ def test_device_fgmres_recursive_cfg1_vs_direct(G, cfg1_mesh):
     x, hist = solve(A, b, cfg)
     assert hist[-1] <= 1e-12
     assert np.linalg.norm(x - xd) <= 1e-8 * np.linalg.norm(xd)
+
+
+def test_reference_lookalike_inputs(G, two_tri):
+    # reference SurfaceMesh / TimeGrid objects (duck-typed) are accepted by the drop-ins
+    import types
+
+    g = golden("blocks_two_tri_N4_p1.npz")
+    mesh = types.SimpleNamespace(vertices=two_tri.vertices.copy(), triangles=two_tri.triangles.copy())
+    grid = types.SimpleNamespace(T=2.0, N=4, p=1)
+    A = G[2].assemble_system(mesh, grid)
+    assert np.linalg.norm(A @ g["x7"] - g["y7"]) <= 1e-12 * np.linalg.norm(g["y7"])
