@@ -393,33 +393,66 @@ __device__ __forceinline__ XPow xpowers(double x) {
   return p;
 }
 
-// Estrin evaluation of sum_k a_k x^k (k <= 16) for the table pair (psi_m, psi~_m).
-template <int NT, int NSUB, bool GLOBAL>
-__device__ __forceinline__ void estrin_pair(const double* __restrict__ cf, int nsub_rt, int idx, int m,
-                                            const XPow& X, double& v0, double& v1) {
-  static_assert(kDeg == 16, "Estrin tree is written for degree 16");
+// Evaluation of the table pair (psi_m, psi~_m) = sum_k a_k x^k, k <= D:
+//   head  k <  K : FP64 coefficients, Estrin tree (depth <= 5),
+//   tail  K..D   : FP32 coefficients, FP32 Horner (FFMA pipe), added as x^K * tail.
+// (D, K) are chosen per family on the host so that the result stays within
+// 3e-15 of the table max of the reference's full Clenshaw evaluation.
+// Coefficient layout: head [k][sub][t] double, tail [k-K][sub][t] float.
+template <int NT, int NSUB, bool GLOBAL, int D, int K>
+__device__ __forceinline__ void eval_pair(const double* __restrict__ cf, int nsub_rt, int tail_off, int idx,
+                                          int m, const XPow& X, double& v0, double& v1) {
   const int nsub = NSUB > 0 ? NSUB : nsub_rt;
   const double2* p = reinterpret_cast<const double2*>(cf + idx * NT + 2 * m);
   const int stride = nsub * NT / 2;  // in double2
-  double2 a[kDeg + 1];
+  double2 a[K];
 #pragma unroll
-  for (int k = 0; k <= kDeg; ++k) a[k] = GLOBAL ? __ldg(p + k * stride) : p[k * stride];
-  double qa[8], qb[8];
+  for (int k = 0; k < K; ++k) a[k] = GLOBAL ? __ldg(p + k * stride) : p[k * stride];
+  if constexpr (K == 17) {
+    double qa[8], qb[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    qa[j] = fma(a[2 * j + 1].x, X.x, a[2 * j].x);
-    qb[j] = fma(a[2 * j + 1].y, X.x, a[2 * j].y);
+    for (int j = 0; j < 8; ++j) {
+      qa[j] = fma(a[2 * j + 1].x, X.x, a[2 * j].x);
+      qb[j] = fma(a[2 * j + 1].y, X.x, a[2 * j].y);
+    }
+    double ra[4], rb[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      ra[j] = fma(qa[2 * j + 1], X.x2, qa[2 * j]);
+      rb[j] = fma(qb[2 * j + 1], X.x2, qb[2 * j]);
+    }
+    const double sa0 = fma(ra[1], X.x4, ra[0]), sa1 = fma(ra[3], X.x4, ra[2]);
+    const double sb0 = fma(rb[1], X.x4, rb[0]), sb1 = fma(rb[3], X.x4, rb[2]);
+    v0 = fma(a[16].x, X.x16, fma(sa1, X.x8, sa0));
+    v1 = fma(a[16].y, X.x16, fma(sb1, X.x8, sb0));
+  } else {
+    static_assert(K == 7, "head split supported at K = 7 or 17");
+    const double qa0 = fma(a[1].x, X.x, a[0].x), qa1 = fma(a[3].x, X.x, a[2].x),
+                 qa2 = fma(a[5].x, X.x, a[4].x);
+    const double qb0 = fma(a[1].y, X.x, a[0].y), qb1 = fma(a[3].y, X.x, a[2].y),
+                 qb2 = fma(a[5].y, X.x, a[4].y);
+    const double ra0 = fma(qa1, X.x2, qa0), ra1 = fma(a[6].x, X.x2, qa2);
+    const double rb0 = fma(qb1, X.x2, qb0), rb1 = fma(a[6].y, X.x2, qb2);
+    v0 = fma(ra1, X.x4, ra0);
+    v1 = fma(rb1, X.x4, rb0);
+    if constexpr (D >= K) {
+      const float2* tp = reinterpret_cast<const float2*>(
+                             reinterpret_cast<const float*>(cf + tail_off) + idx * NT + 2 * m);
+      float2 b[D - K + 1];
+#pragma unroll
+      for (int k = 0; k <= D - K; ++k) b[k] = GLOBAL ? __ldg(tp + k * stride) : tp[k * stride];
+      const float xf = (float)X.x;
+      float ta = b[D - K].x, tb = b[D - K].y;
+#pragma unroll
+      for (int k = D - K - 1; k >= 0; --k) {
+        ta = fmaf(ta, xf, b[k].x);
+        tb = fmaf(tb, xf, b[k].y);
+      }
+      const double x7 = X.x4 * X.x2 * X.x;
+      v0 = fma(x7, (double)ta, v0);
+      v1 = fma(x7, (double)tb, v1);
+    }
   }
-  double ra[4], rb[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    ra[j] = fma(qa[2 * j + 1], X.x2, qa[2 * j]);
-    rb[j] = fma(qb[2 * j + 1], X.x2, qb[2 * j]);
-  }
-  const double sa0 = fma(ra[1], X.x4, ra[0]), sa1 = fma(ra[3], X.x4, ra[2]);
-  const double sb0 = fma(rb[1], X.x4, rb[0]), sb1 = fma(rb[3], X.x4, rb[2]);
-  v0 = fma(a[16].x, X.x16, fma(sa1, X.x8, sa0));
-  v1 = fma(a[16].y, X.x16, fma(sb1, X.x8, sb0));
 }
 
 struct SortedPts {
@@ -433,31 +466,33 @@ struct SortedPts {
   double rmin, rmax, inv_wb;
 };
 
-// One block position of one family for one work item: the full warp walks the
-// position's in-support points in r-sorted order, 32 consecutive points per
-// round (clustered table subintervals -> few shared-memory wavefronts per
-// coefficient load), then reduce-scatters the 10 (p+1)^2 sums.
-template <int P, int NSUB, bool GLOBAL>
-__device__ __forceinline__ void process_position(const FamDev& fd, const double* __restrict__ cf,
-                                                 const SortedPts& pt, int s, int lane,
-                                                 double* __restrict__ dst, unsigned long long& my_in) {
-  constexpr int NM = (P + 1) * (P + 1);
-  constexpr int NT = 2 * NM;
-  constexpr int NACC = 10 * NM;
-  const unsigned FULL = 0xffffffffu;
-  const double delta = fd.delta[s];
+// In-support index range [i0, i1) of the r-sorted points for table offset delta
+// (r in [amin - delta, amax - delta], bucket bounds are monotone in r).
+__device__ __forceinline__ void position_range(const FamDev& fd, const SortedPts& pt, double delta, int& i0,
+                                               int& i1) {
   const double rlo = fd.amin - delta, rhi = fd.amax - delta;
-  int i0 = 0, i1 = 0;
+  i0 = 0;
+  i1 = 0;
   if (rhi >= pt.rmin && rlo <= pt.rmax) {
     const int blo = rlo <= pt.rmin ? 0 : min(kBuckets - 1, (int)((rlo - pt.rmin) * pt.inv_wb));
     const int bhi = rhi >= pt.rmax ? kBuckets - 1 : min(kBuckets - 1, (int)((rhi - pt.rmin) * pt.inv_wb));
     i0 = blo == 0 ? 0 : (int)pt.cur[blo - 1];
     i1 = (int)pt.cur[bhi];
   }
-  double acc[NACC];
-#pragma unroll
-  for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
-  unsigned n_act = 0;
+}
+
+// The full warp walks one position's in-support points in r-sorted order, 32
+// consecutive points per round (clustered table subintervals -> few shared-memory
+// wavefronts per coefficient load) and accumulates S[a][b], s per (m2, m1).
+// Only this loop is specialised per (subintervals, degree split); the range
+// search and the reduction live once in the caller (instruction-cache footprint).
+template <int P, int NSUB, bool GLOBAL, int D, int K>
+__device__ __forceinline__ void eval_rounds(const FamDev& fd, const double* __restrict__ cf,
+                                            const SortedPts& pt, int i0, int i1, double delta, int lane,
+                                            double (&acc)[10 * (P + 1) * (P + 1)], unsigned& n_act) {
+  constexpr int NM = (P + 1) * (P + 1);
+  constexpr int NT = 2 * NM;
+  const unsigned FULL = 0xffffffffu;
   const int nround = (i1 - i0 + 31) >> 5;
   for (int rr = 0; rr < nround; ++rr) {
     const int i = i0 + lane + 32 * rr;
@@ -479,7 +514,7 @@ __device__ __forceinline__ void process_position(const FamDev& fd, const double*
 #pragma unroll
     for (int m = 0; m < NM; ++m) {
       double v0, v1;
-      estrin_pair<NT, NSUB, GLOBAL>(cf, fd.nsub, idx, m, X, v0, v1);
+      eval_pair<NT, NSUB, GLOBAL, D, K>(cf, fd.nsub, fd.tail_off, idx, m, X, v0, v1);
       if (fd.fold) {
         v0 *= neg ? fd.sn[2 * m] : fd.sp[2 * m];
         v1 *= neg ? fd.sn[2 * m + 1] : fd.sp[2 * m + 1];
@@ -499,13 +534,6 @@ __device__ __forceinline__ void process_position(const FamDev& fd, const double*
       S[9] = fma(c, v1, S[9]);
     }
   }
-  my_in += n_act;
-  double outv[RS<NACC>::H5];
-  int base, valid;
-  warp_reduce_scatter<NACC>(acc, lane, outv, base, valid);
-#pragma unroll
-  for (int k = 0; k < RS<NACC>::H5; ++k)
-    if (k < valid) dst[base + k] = outv[k];
 }
 
 template <int P, bool SMEM_COEF>
@@ -669,20 +697,45 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
       const double* cf_g = fd.coeffs;
       for (int si = 0; si < cnt; ++si) {
         double* dst = a.part + (slot0 + fr.foff + si) * NACC;
-        const int s = s_lo + si;
-#define TDB_F(NS, GL) process_position<P, NS, GL>(fd, GL ? cf_g : cf_s, pt, s, lane, dst, my_in)
+        const double delta = fd.delta[s_lo + si];
+        int i0, i1;
+        position_range(fd, pt, delta, i0, i1);
+        double acc[NACC];
+#pragma unroll
+        for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
+        unsigned n_act = 0;
+#define TDB_F(NS, GL, D_, K_) \
+  eval_rounds<P, NS, GL, D_, K_>(fd, GL ? cf_g : cf_s, pt, i0, i1, delta, lane, acc, n_act)
+#define TDB_DK(NS, GL)                                     \
+  if (fd.khead == 17) {                                    \
+    TDB_F(NS, GL, 16, 17);                                 \
+  } else if (fd.deg == 12) {                               \
+    TDB_F(NS, GL, 12, 7);                                  \
+  } else if (fd.deg == 14) {                               \
+    TDB_F(NS, GL, 14, 7);                                  \
+  } else {                                                 \
+    TDB_F(NS, GL, 16, 7);                                  \
+  }
         if (fd.coef_global) {
-          TDB_F(0, true);
+          TDB_DK(0, true)
         } else {
           switch (fd.nsub) {
-            case 16: TDB_F(16, false); break;
-            case 32: TDB_F(32, false); break;
-            case 64: TDB_F(64, false); break;
-            case 96: TDB_F(96, false); break;
-            default: TDB_F(0, false); break;
+            case 16: TDB_DK(16, false) break;
+            case 32: TDB_DK(32, false) break;
+            case 64: TDB_DK(64, false) break;
+            case 96: TDB_DK(96, false) break;
+            default: TDB_DK(0, false) break;
           }
         }
+#undef TDB_DK
 #undef TDB_F
+        my_in += n_act;
+        double outv[RS<NACC>::H5];
+        int base, valid;
+        warp_reduce_scatter<NACC>(acc, lane, outv, base, valid);
+#pragma unroll
+        for (int k = 0; k < RS<NACC>::H5; ++k)
+          if (k < valid) dst[base + k] = outv[k];
       }
     }
   }
@@ -1318,8 +1371,8 @@ int tdb_system_run_impl(TdbSystem* sys) {
   return TDB_OK;
 }
 
-// sum_j c_j T_j(x) -> sum_k a_k x^k, degree kDeg, integer T_j coefficients
-static void cheb_to_monomial(const double* c, long double* a) {
+// sum_{j<=D} c_j T_j(x) -> sum_k a_k x^k (k <= D), integer T_j coefficients
+static void cheb_to_monomial(const double* c, int D, long double* a) {
   long long T[kDeg + 1][kDeg + 1] = {};
   T[0][0] = 1;
   T[1][1] = 1;
@@ -1327,9 +1380,85 @@ static void cheb_to_monomial(const double* c, long double* a) {
     for (int k = 0; k <= kDeg; ++k) T[j][k] = (k > 0 ? 2 * T[j - 1][k - 1] : 0) - T[j - 2][k];
   for (int k = 0; k <= kDeg; ++k) {
     long double s_ = 0.0L;
-    for (int j = kDeg; j >= 0; --j) s_ += (long double)c[j] * (long double)T[j][k];
-    a[k] = s_;
+    for (int j = D; j >= 0; --j) s_ += (long double)c[j] * (long double)T[j][k];
+    a[k] = k <= D ? s_ : 0.0L;
   }
+}
+
+static long double clenshaw_ld(const double* c, long double x) {
+  long double b1 = 0.0L, b2 = 0.0L;
+  for (int k = kDeg; k >= 1; --k) {
+    const long double t = 2.0L * x * b1 - b2 + c[k];
+    b2 = b1;
+    b1 = t;
+  }
+  return x * b1 - b2 + c[0];
+}
+
+// Host emulation of eval_pair's arithmetic for one table (Estrin head, FP32 tail).
+static double emulate_split(const long double* a, int D, int K, double x) {
+  double h[17];
+  for (int k = 0; k < 17; ++k) h[k] = (k < K && k <= D) ? (double)a[k] : 0.0;
+  const double x2 = x * x, x4 = x2 * x2, x8 = x4 * x4, x16 = x8 * x8;
+  double v;
+  if (K == 17) {
+    double q[8], r[4];
+    for (int j = 0; j < 8; ++j) q[j] = std::fma(h[2 * j + 1], x, h[2 * j]);
+    for (int j = 0; j < 4; ++j) r[j] = std::fma(q[2 * j + 1], x2, q[2 * j]);
+    const double s0 = std::fma(r[1], x4, r[0]), s1 = std::fma(r[3], x4, r[2]);
+    v = std::fma(h[16], x16, std::fma(s1, x8, s0));
+  } else {
+    const double q0 = std::fma(h[1], x, h[0]), q1 = std::fma(h[3], x, h[2]), q2 = std::fma(h[5], x, h[4]);
+    const double r0 = std::fma(q1, x2, q0), r1 = std::fma(h[6], x2, q2);
+    v = std::fma(r1, x4, r0);
+    if (K <= D) {
+      const float xf = (float)x;
+      float t = (float)a[D];
+      for (int k = D - 1; k >= K; --k) t = std::fmaf(t, xf, (float)a[k]);
+      const double x7 = x4 * x2 * x;
+      v = std::fma(x7, (double)t, v);
+    }
+  }
+  return v;
+}
+
+// Cheapest (degree D, FP64 head size K) keeping every table of the pack within
+// 3e-15 of its max of the reference's full degree-16 Clenshaw evaluation.
+static void select_split(const TdbPsiPack& pk, int nt, int nsub, int* D_out, int* K_out) {
+  static const int cands[4][2] = {{12, 7}, {14, 7}, {16, 7}, {16, 17}};
+  if (pk.deg != kDeg) {
+    *D_out = 16;
+    *K_out = 17;
+    return;
+  }
+  for (const auto& cd : cands) {
+    const int D = cd[0], K = cd[1];
+    bool ok = true;
+    for (int t = 0; t < nt && ok; ++t) {
+      double tmax = 0.0;
+      for (int k = 0; k < nsub; ++k)
+        for (int c = 0; c <= kDeg; ++c)
+          tmax = std::max(tmax, std::fabs(pk.coeffs[((size_t)t * pk.max_nsub + k) * (kDeg + 1) + c]));
+      for (int k = 0; k < nsub && ok; ++k) {
+        const double* cc = pk.coeffs + ((size_t)t * pk.max_nsub + k) * (kDeg + 1);
+        long double mono[kDeg + 1];
+        cheb_to_monomial(cc, D, mono);
+        for (int sidx = 0; sidx <= 64 && ok; ++sidx) {
+          const double x = -1.0 + 2.0 * sidx / 64.0;
+          const long double ref = clenshaw_ld(cc, x);
+          const double err = std::fabs((double)((long double)emulate_split(mono, D, K, x) - ref));
+          if (err > 3e-15 * tmax) ok = false;
+        }
+      }
+    }
+    if (ok) {
+      *D_out = D;
+      *K_out = K;
+      return;
+    }
+  }
+  *D_out = 16;
+  *K_out = 17;
 }
 
 int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDesc* desc,
@@ -1407,24 +1536,35 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
     if ((rc = dupload(&fs.delta, hf.delta, hf.npos, st))) return rc;
     if ((rc = dupload(&fs.slo, hf.slo, hf.npos, st))) return rc;
     if ((rc = dupload(&fs.shi, hf.shi, hf.npos, st))) return rc;
-    const int len = nt * fd.nsub * (kDeg + 1);
-    ws->fam_blob_off[f] = (int)blob_all.size();
-    ws->fam_blob_len[f] = len;
     // Each subinterval's Chebyshev series sum_j c_j T_j(x) is re-expanded in the
     // monomial basis sum_k a_k x^k (exact integer T_j coefficients, 80-bit
     // accumulation) so the device can use Estrin's scheme (depth 5 instead of the
-    // 32-deep Clenshaw chain); max deviation from Clenshaw <= 6e-16 of the table
-    // max on every default table (tools/estrin_check.py).
-    // Transposed layout [k][sub][t]: the (psi_m, psi~_m) pair of one coefficient
-    // is one 16-byte load and r-sorted lanes read clustered subintervals.
-    blob_all.resize(blob_all.size() + len);
+    // 32-deep Clenshaw chain).  Per family, the trailing Chebyshev coefficients that
+    // are roundoff noise of the reference's own tables are dropped (degree D) and the
+    // small high-order monomials go to an FP32 tail (k >= K) - chosen so every
+    // table stays within 3e-15 of its max of the reference's full Clenshaw value
+    // (select_split, checked on 65 points per subinterval).
+    int D = 16, K = 17;
+    select_split(pk, nt, fd.nsub, &D, &K);
+    fd.deg = D;
+    fd.khead = K;
+    const int head_len = K * fd.nsub * nt;
+    const int tail_floats = (K <= D) ? (D - K + 1) * fd.nsub * nt : 0;
+    const int tail_len = ((tail_floats + 1) / 2 + 1) / 2 * 2;  // doubles, even (16-byte aligned)
+    const int len = head_len + tail_len;
+    fd.tail_off = head_len;
+    ws->fam_blob_off[f] = (int)blob_all.size();
+    ws->fam_blob_len[f] = len;
+    blob_all.resize(blob_all.size() + len, 0.0);
     double* dstb = blob_all.data() + ws->fam_blob_off[f];
+    float* dstt = reinterpret_cast<float*>(dstb + head_len);
     for (int t = 0; t < nt; ++t)
       for (int k = 0; k < fd.nsub; ++k) {
         const double* cc = pk.coeffs + ((size_t)t * pk.max_nsub + k) * (kDeg + 1);
         long double mono[kDeg + 1];
-        cheb_to_monomial(cc, mono);
-        for (int c = 0; c <= kDeg; ++c) dstb[((size_t)c * fd.nsub + k) * nt + t] = (double)mono[c];
+        cheb_to_monomial(cc, D, mono);
+        for (int c = 0; c < K && c <= kDeg; ++c) dstb[((size_t)c * fd.nsub + k) * nt + t] = (double)mono[c];
+        for (int c = K; c <= D; ++c) dstt[((size_t)(c - K) * fd.nsub + k) * nt + t] = (float)mono[c];
       }
     fd.delta = fs.delta;
     fd.slo = fs.slo;

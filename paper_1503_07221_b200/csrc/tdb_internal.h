@@ -20,6 +20,10 @@ struct FamDev {
   int npos, nsub, nt, fold;
   int coeff_off;   // offset (doubles) of this family's coefficients in the launch blob
   int coef_global; // 1: read `coeffs` (global, transposed layout) instead of the smem blob
+  int deg;         // polynomial degree kept (Chebyshev tail below 3e-15 of the table max dropped)
+  int khead;       // monomials 0..khead-1 in FP64, khead..deg in FP32 (float tail)
+  int tail_off;    // doubles from the head start to the FP32 tail block
+  int pad_;
   double lo, w, inv_w, amin, amax;
   double sp[kMaxTables], sn[kMaxTables];
   const double* delta;
