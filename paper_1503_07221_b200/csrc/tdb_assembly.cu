@@ -376,7 +376,7 @@ __device__ __forceinline__ void warp_reduce_scatter(const double (&v)[N], int la
   valid = n;
 }
 
-// ---- table evaluation (transposed layout [k][idx][t], t fastest) ------------
+// ---- table evaluation (coefficient rows [sub][k][t], t fastest) -------------
 // (psi_m, psi~_m) are the adjacent tables 2m, 2m+1: one 16-byte load per
 // Chebyshev coefficient for both.  Lanes of a warp evaluate r-sorted points, so
 // their subintervals idx are clustered and the loads coalesce to few wavefronts.
@@ -398,13 +398,14 @@ __device__ __forceinline__ XPow xpowers(double x) {
 //   tail  K..D   : FP32 coefficients, FP32 Horner (FFMA pipe), added as x^K * tail.
 // (D, K) are chosen per family on the host so that the result stays within
 // 3e-15 of the table max of the reference's full Clenshaw evaluation.
-// Coefficient layout: head [k][sub][t] double, tail [k-K][sub][t] float.
-template <int NT, int NSUB, bool GLOBAL, int D, int K>
-__device__ __forceinline__ void eval_pair(const double* __restrict__ cf, int nsub_rt, int tail_off, int idx,
-                                          int m, const XPow& X, double& v0, double& v1) {
-  const int nsub = NSUB > 0 ? NSUB : nsub_rt;
-  const double2* p = reinterpret_cast<const double2*>(cf + idx * NT + 2 * m);
-  const int stride = nsub * NT / 2;  // in double2
+// Coefficient layout: head [sub][k][t] double, tail [sub][k-K][t] float.
+template <int NT, bool GLOBAL, int D, int K>
+__device__ __forceinline__ void eval_pair(const double* __restrict__ cf, int tail_off, int idx, int m,
+                                          const XPow& X, double& v0, double& v1) {
+  // subinterval-major rows: all K (psi_m, psi~_m) pairs of subinterval idx are
+  // contiguous, so the loads use immediate offsets whatever the subinterval count
+  const double2* p = reinterpret_cast<const double2*>(cf + (idx * K) * NT + 2 * m);
+  constexpr int stride = NT / 2;  // in double2
   double2 a[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) a[k] = GLOBAL ? __ldg(p + k * stride) : p[k * stride];
@@ -437,7 +438,7 @@ __device__ __forceinline__ void eval_pair(const double* __restrict__ cf, int nsu
     v1 = fma(rb1, X.x4, rb0);
     if constexpr (D >= K) {
       const float2* tp = reinterpret_cast<const float2*>(
-                             reinterpret_cast<const float*>(cf + tail_off) + idx * NT + 2 * m);
+                             reinterpret_cast<const float*>(cf + tail_off) + (idx * (D - K + 1)) * NT + 2 * m);
       float2 b[D - K + 1];
 #pragma unroll
       for (int k = 0; k <= D - K; ++k) b[k] = GLOBAL ? __ldg(tp + k * stride) : tp[k * stride];
@@ -486,7 +487,7 @@ __device__ __forceinline__ void position_range(const FamDev& fd, const SortedPts
 // wavefronts per coefficient load) and accumulates S[a][b], s per (m2, m1).
 // Only this loop is specialised per (subintervals, degree split); the range
 // search and the reduction live once in the caller (instruction-cache footprint).
-template <int P, int NSUB, bool GLOBAL, int D, int K>
+template <int P, bool GLOBAL, int D, int K>
 __device__ __forceinline__ void eval_rounds(const FamDev& fd, const double* __restrict__ cf,
                                             const SortedPts& pt, int i0, int i1, double delta, int lane,
                                             double (&acc)[10 * (P + 1) * (P + 1)], unsigned& n_act) {
@@ -514,7 +515,7 @@ __device__ __forceinline__ void eval_rounds(const FamDev& fd, const double* __re
 #pragma unroll
     for (int m = 0; m < NM; ++m) {
       double v0, v1;
-      eval_pair<NT, NSUB, GLOBAL, D, K>(cf, fd.nsub, fd.tail_off, idx, m, X, v0, v1);
+      eval_pair<NT, GLOBAL, D, K>(cf, fd.tail_off, idx, m, X, v0, v1);
       if (fd.fold) {
         v0 *= neg ? fd.sn[2 * m] : fd.sp[2 * m];
         v1 *= neg ? fd.sn[2 * m + 1] : fd.sp[2 * m + 1];
@@ -704,28 +705,21 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
 #pragma unroll
         for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
         unsigned n_act = 0;
-#define TDB_F(NS, GL, D_, K_) \
-  eval_rounds<P, NS, GL, D_, K_>(fd, GL ? cf_g : cf_s, pt, i0, i1, delta, lane, acc, n_act)
-#define TDB_DK(NS, GL)                                     \
+#define TDB_F(GL, D_, K_) eval_rounds<P, GL, D_, K_>(fd, GL ? cf_g : cf_s, pt, i0, i1, delta, lane, acc, n_act)
+#define TDB_DK(GL)                                         \
   if (fd.khead == 17) {                                    \
-    TDB_F(NS, GL, 16, 17);                                 \
+    TDB_F(GL, 16, 17);                                     \
   } else if (fd.deg == 12) {                               \
-    TDB_F(NS, GL, 12, 7);                                  \
+    TDB_F(GL, 12, 7);                                      \
   } else if (fd.deg == 14) {                               \
-    TDB_F(NS, GL, 14, 7);                                  \
+    TDB_F(GL, 14, 7);                                      \
   } else {                                                 \
-    TDB_F(NS, GL, 16, 7);                                  \
+    TDB_F(GL, 16, 7);                                      \
   }
         if (fd.coef_global) {
-          TDB_DK(0, true)
+          TDB_DK(true)
         } else {
-          switch (fd.nsub) {
-            case 16: TDB_DK(16, false) break;
-            case 32: TDB_DK(32, false) break;
-            case 64: TDB_DK(64, false) break;
-            case 96: TDB_DK(96, false) break;
-            default: TDB_DK(0, false) break;
-          }
+          TDB_DK(false)
         }
 #undef TDB_DK
 #undef TDB_F
@@ -1563,8 +1557,8 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
         const double* cc = pk.coeffs + ((size_t)t * pk.max_nsub + k) * (kDeg + 1);
         long double mono[kDeg + 1];
         cheb_to_monomial(cc, D, mono);
-        for (int c = 0; c < K && c <= kDeg; ++c) dstb[((size_t)c * fd.nsub + k) * nt + t] = (double)mono[c];
-        for (int c = K; c <= D; ++c) dstt[((size_t)(c - K) * fd.nsub + k) * nt + t] = (float)mono[c];
+        for (int c = 0; c < K && c <= kDeg; ++c) dstb[((size_t)k * K + c) * nt + t] = (double)mono[c];
+        for (int c = K; c <= D; ++c) dstt[((size_t)k * (D - K + 1) + (c - K)) * nt + t] = (float)mono[c];
       }
     fd.delta = fs.delta;
     fd.slo = fs.slo;

@@ -29,7 +29,7 @@ struct FamDev {
   const double* delta;
   const double* slo;
   const double* shi;
-  const double* coeffs;  // transposed [c][sub][t] global copy
+  const double* coeffs;  // global copy, rows [sub][k][t] (head FP64 + FP32 tail)
 };
 
 struct RuleDev {
