@@ -110,6 +110,11 @@ typedef struct TdbAssemblyDesc {
   int32_t num_families;
   const TdbFamily* families;
   TdbRule rules[4];        /* indexed by TDB_CASE_* */
+  /* Row block (multi-GPU sharding): assemble only the test-vertex
+   * rows listed (strictly increasing); 0 = all vertices.  Pairs are restricted
+   * to test triangles in the owned rows' stars; CSR rows follow `rows`. */
+  int64_t num_rows;
+  const int64_t* rows;
 } TdbAssemblyDesc;
 
 typedef struct TdbStats {
@@ -126,6 +131,8 @@ typedef struct TdbStats {
   int64_t units_case[4];   /* units per pair case (regular, coincident, edge, vertex) */
   int64_t pairs_case[4];   /* pairs with >= 1 unit, per case */
   int64_t launches;        /* kernel launches issued by the last tdb_system_run */
+  int64_t units_primary;   /* units whose test triangle's first vertex is an owned row:
+                              summed over row blocks = the global unit count */
 } TdbStats;
 
 typedef struct TdbContext TdbContext;
@@ -167,7 +174,7 @@ int tdb_system_destroy(TdbSystem* sys);
 int tdb_system_stats(const TdbSystem* sys, TdbStats* out);
 /* nnz of family f (stored pattern incl. explicit zeros) */
 int tdb_system_family_nnz(const TdbSystem* sys, int32_t f, int64_t* nnz);
-/* D2H copy of family f: indptr (npos*M+1,) int64 with rows (s, j);
+/* D2H copy of family f: indptr (npos*nrows+1,) int64 with rows (s, local row r);
  * indices (nnz,) int32 columns; data (nnz,(p+1)^2) */
 int tdb_system_copy_family(const TdbSystem* sys, int32_t f, int64_t* indptr,
                            int32_t* indices, double* data);
@@ -198,13 +205,20 @@ typedef struct TdbMatvecDesc {
   const int32_t* term_pos;
   const int32_t* term_d;
   const uint32_t* term_mask; /* (nterms, words) */
+  /* Layout of x (optional): entry (vertex l, column c) is x[x_map[l] + c*x_stride].
+   * NULL x_map = the reference's time-major layout (x_map[l] = l, stride M).
+   * A multi-GPU caller passes the all-gathered rank-major layout
+   * [rank][column][rows_per_rank] with x_map[l] = owner*ncols*stride + local. */
+  int64_t x_stride;
+  const int64_t* x_map;      /* (M,) */
 } TdbMatvecDesc;
 
 typedef struct TdbMatvecPlan TdbMatvecPlan;
 
 int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* desc, TdbMatvecPlan** out);
 int tdb_matvec_plan_destroy(TdbMatvecPlan* plan);
-/* y_dev[(rhi-rlo+1)(p+1)M] = A[rows, cols] x_dev[(chi-clo+1)(p+1)M] (device pointers) */
+/* y_dev[(rhi-rlo+1)(p+1) * nrows] = A[rows, cols] x_dev (device pointers); y is
+ * time-major over the system's owned test-vertex rows (all M for a full system). */
 int tdb_matvec(TdbMatvecPlan* plan, const double* x_dev, double* y_dev);
 /* canonical stored bytes and logical flops of one application of this plan */
 int tdb_matvec_plan_work(const TdbMatvecPlan* plan, double* algorithmic_bytes, double* flops);

@@ -61,6 +61,7 @@ class TdbAssemblyDesc(C.Structure):
         ("p", i32), ("num_families", i32),
         ("families", C.POINTER(TdbFamily)),
         ("rules", TdbRule * 4),
+        ("num_rows", i64), ("rows", i64p),
     ]
 
 
@@ -69,7 +70,7 @@ class TdbStats(C.Structure):
         ("units", i64), ("items", i64), ("n_in", i64), ("n_geom", i64), ("nnz_total", i64),
         ("ms_plan", C.c_double), ("ms_quad", C.c_double), ("ms_finalize", C.c_double),
         ("ms_pattern", C.c_double), ("ms_total", C.c_double),
-        ("units_case", i64 * 4), ("pairs_case", i64 * 4), ("launches", i64),
+        ("units_case", i64 * 4), ("pairs_case", i64 * 4), ("launches", i64), ("units_primary", i64),
     ]
 
     def as_dict(self) -> dict:
@@ -86,6 +87,7 @@ class TdbMatvecDesc(C.Structure):
         ("nterms", i32), ("words", i32), ("reserved", i32),
         ("term_family", i32p), ("term_pos", i32p), ("term_d", i32p),
         ("term_mask", C.POINTER(C.c_uint32)),
+        ("x_stride", i64), ("x_map", i64p),
     ]
 
 

@@ -245,15 +245,23 @@ def _mesh_c(mesh: SurfaceMesh, keep: list) -> _lib.TdbMesh:
 
 
 class DeviceAssembly:
-    """Owner of a device-resident assembled system (TdbSystem handle)."""
+    """Owner of a device-resident assembled system (TdbSystem handle).
 
-    def __init__(self, mesh: SurfaceMesh, plan: AssemblyPlan, ctx: _lib.Context | None = None):
+    rows: optional strictly increasing test-vertex ids (a multi-GPU row block);
+    only those CSR rows are assembled, from the pairs whose test triangle lies in
+    their stars.  Default: every vertex.
+    """
+
+    def __init__(self, mesh: SurfaceMesh, plan: AssemblyPlan, ctx: _lib.Context | None = None, rows=None,
+                 create_only: bool = False):
         self.mesh = mesh
         self.plan = plan
         self.ctx = ctx or _lib.default_context()
         self.M = mesh.num_vertices
         self.p = plan.grid.p
         self.handle = None
+        self.rows = None if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
+        self.nrows = self.M if self.rows is None else len(self.rows)
         keep: list = []
         fams = (_lib.TdbFamily * max(1, len(plan.families)))()
         for i, f in enumerate(plan.families):
@@ -271,12 +279,16 @@ class DeviceAssembly:
             keep.append((xh, yh, w))
             desc.rules[c].nq = len(w)
             desc.rules[c].xhat, desc.rules[c].yhat, desc.rules[c].w = _lib.ptr(xh), _lib.ptr(yh), _lib.ptr(w)
+        if self.rows is not None:
+            desc.num_rows = len(self.rows)
+            desc.rows = _lib.ptr(self.rows, _lib.C.c_int64)
         self.num_families = len(plan.families)
         if self.num_families == 0:
             return
         h = _lib.C.c_void_p()
-        _lib.check(_lib.LIB.tdb_system_assemble(self.ctx.handle, _lib.C.byref(_mesh_c(mesh, keep)),
-                                                _lib.C.byref(desc), _lib.C.byref(h)), "system_assemble")
+        fn = _lib.LIB.tdb_system_create if create_only else _lib.LIB.tdb_system_assemble
+        _lib.check(fn(self.ctx.handle, _lib.C.byref(_mesh_c(mesh, keep)), _lib.C.byref(desc), _lib.C.byref(h)),
+                   "system_assemble")
         self.handle = h
 
     def rerun(self) -> None:
@@ -296,7 +308,7 @@ class DeviceAssembly:
         nnz = _lib.C.c_int64()
         _lib.check(_lib.LIB.tdb_system_family_nnz(self.handle, f, _lib.C.byref(nnz)), "family_nnz")
         npos = len(self.plan.families[f].positions)
-        indptr = np.empty(npos * self.M + 1, dtype=np.int64)
+        indptr = np.empty(npos * self.nrows + 1, dtype=np.int64)
         indices = np.empty(max(1, nnz.value), dtype=np.int32)
         data = np.empty((max(1, nnz.value), (self.p + 1) ** 2))
         _lib.check(_lib.LIB.tdb_system_copy_family(
@@ -324,8 +336,15 @@ class DeviceAssembly:
             indptr, indices, data = self.family_arrays(f)
             if _cache is not None:
                 _cache[f] = (indptr, indices, data)
-        lo, hi = indptr[s * m], indptr[(s + 1) * m]
-        ip = indptr[s * m : (s + 1) * m + 1] - lo
+        nr = self.nrows
+        lo, hi = indptr[s * nr], indptr[(s + 1) * nr]
+        ipl = indptr[s * nr : (s + 1) * nr + 1] - lo
+        if self.rows is None:
+            ip = ipl
+        else:  # owned rows only: expand the local row pointer to all M rows
+            counts = np.zeros(m, dtype=np.int64)
+            counts[self.rows] = np.diff(ipl)
+            ip = np.concatenate([[0], np.cumsum(counts)])
         out = []
         for m2 in range(np1):
             row = []

@@ -238,6 +238,8 @@ __device__ __forceinline__ int last_leq(const double* __restrict__ a, int n, dou
 
 struct PlanArgs {
   int E, F;
+  int Et;                   // test triangles of this system (pair index P = k*E + ex)
+  const int* tt;            // (Et,) test triangle ids
   const double* corners;
   const int* tri;
   const FamDev* fams;
@@ -247,14 +249,16 @@ struct PlanArgs {
   long long* slots;         // [E*E] -> exclusive scan -> pair_base
   long long* nitems;        // [E*E] -> exclusive scan -> item_base
   unsigned char* pcase;     // [E*E]
-  unsigned long long* case_pairs;  // [4] pairs with >= 1 unit, [4..7] units, per case
+  unsigned long long* case_pairs;  // [4] pairs with >= 1 unit, [4..7] units, per case,
+                                   // [8] units of pairs whose test triangle's first vertex is owned
+  const unsigned char* owned;      // (V,) owned test-vertex rows of this system
 };
 
 __global__ void k_plan_pairs(PlanArgs a) {
-  const long long E2 = (long long)a.E * a.E;
+  const long long E2 = (long long)a.Et * a.E;  // pairs of this system
   for (long long P = blockIdx.x * (long long)blockDim.x + threadIdx.x; P < E2;
        P += (long long)gridDim.x * blockDim.x) {
-    const int ey = (int)(P / a.E), ex = (int)(P % a.E);
+    const int ey = a.tt[P / a.E], ex = (int)(P % a.E);
     double dmin, dmax;
     const int cs = pair_bounds(a.corners, a.tri, ex, ey, dmin, dmax);
     int units = 0;
@@ -277,6 +281,8 @@ __global__ void k_plan_pairs(PlanArgs a) {
     if (units > 0) {
       atomicAdd(a.case_pairs + cs, 1ULL);
       atomicAdd(a.case_pairs + 4 + cs, (unsigned long long)units);
+      // each test triangle is "primary" on exactly one row block (owner of its first vertex)
+      if (a.owned[a.tri[3 * ey]]) atomicAdd(a.case_pairs + 8, (unsigned long long)units);
     }
   }
 }
@@ -299,6 +305,8 @@ __global__ void k_fill_items(long long E2, const long long* __restrict__ item_ba
 // ---------------------------------------------------------------------------
 struct QuadArgs {
   int E;
+  long long npair;            // Et * E
+  const int* tt;              // test triangle of pair-row k
   int fam_count;
   int fam_ids[kMaxFamilies];  // global family index of each launch family (frange slices)
   const FamDev* fams;         // this launch's descriptors (coeff_off into `blob`)
@@ -564,7 +572,7 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
     __syncthreads();
   }
   const double* coef_base = SMEM_COEF ? sblob : a.blob;
-  const long long E2 = (long long)a.E * a.E;
+  const long long E2 = a.npair;
   unsigned long long my_in = 0;
   const unsigned lanemask_lt = (1u << lane) - 1u;
 
@@ -580,7 +588,7 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
     for (int fi = 0; fi < a.fam_count; ++fi)
       any |= (a.frange[(long long)a.fam_ids[fi] * E2 + Pp].lo_cnt >> 16) != 0;
     if (!any) continue;
-    const int ey = Pp / a.E, ex = Pp % a.E;
+    const int ey = a.tt[Pp / a.E], ex = Pp % a.E;
     int lx[3], ly[3];
     const int cs = pair_topology(a.tri, ex, ey, lx, ly);
     const RuleDev& R = a.rules[cs];
@@ -762,6 +770,9 @@ __global__ void k_finalize_items(long long E2, const int* __restrict__ units,
 // ---------------------------------------------------------------------------
 struct PatternArgs {
   int E, M, f, npos;
+  int nrows;              // owned test vertices (CTA r -> vertex rows[r])
+  const int* rows;
+  const int* ey_map;      // triangle -> pair-row k (or -1)
   int s_begin, s_count;   // position chunk handled by this launch
   int words;              // ceil(M / 32)
   const int* tri;
@@ -788,7 +799,7 @@ __device__ void build_bitmaps(const PatternArgs& a, int j, unsigned* bm) {
   (void)E2;
   for (int k = a.star_off[j]; k < a.star_off[j + 1]; ++k) {
     const int ey = a.star_ids[k];
-    const FRange* row = a.frange + (long long)ey * a.E;
+    const FRange* row = a.frange + (long long)a.ey_map[ey] * a.E;
     for (int ex = threadIdx.x; ex < a.E; ex += blockDim.x) {
       const FRange fr = row[ex];
       const int cnt = fr.lo_cnt >> 16;
@@ -810,7 +821,7 @@ __device__ void build_bitmaps(const PatternArgs& a, int j, unsigned* bm) {
 
 __global__ void k_pattern_count(PatternArgs a) {
   extern __shared__ unsigned bm[];
-  const int j = blockIdx.x;
+  const int rloc = blockIdx.x, j = a.rows[rloc];
   build_bitmaps(a, j, bm);
   __shared__ int red[32];
   for (int sl = 0; sl < a.s_count; ++sl) {
@@ -822,7 +833,7 @@ __global__ void k_pattern_count(PatternArgs a) {
     if (threadIdx.x == 0) {
       int t = 0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-      a.row_count[(long long)(a.s_begin + sl) * a.M + j] = t;
+      a.row_count[(long long)(a.s_begin + sl) * a.nrows + rloc] = t;
     }
     __syncthreads();
   }
@@ -833,6 +844,7 @@ constexpr int kMaxStar = 32;
 struct RowStar {  // star of the test vertex j, cached in shared memory per CTA
   int n;
   int e[kMaxStar];
+  int k[kMaxStar];   // pair-row index of e
   int t[kMaxStar][3];
   int pj[kMaxStar];  // local position of j in triangle e
 };
@@ -855,7 +867,7 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s, int
   int nd = 0;
   bool overflow = false;
   auto contribute = [&](int ex, int ey, int kx_local, int ky, int cs, const FRange& fr, int s_lo) {
-    const long long Pp = (long long)ey * a.E + ex;
+    const long long Pp = (long long)rs.k[ky] * a.E + ex;
     const long long slot = a.pair_base[Pp] + fr.foff + (s - s_lo);
     int ca = rs.pj[ky], cb = 0;
     const int* tx = a.tri + 3 * ex;
@@ -892,7 +904,7 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s, int
     const int x0 = a.tri[3 * ex], x1 = a.tri[3 * ex + 1], x2 = a.tri[3 * ex + 2];
     for (int ky = 0; ky < rs.n; ++ky) {
       const int ey = rs.e[ky];
-      const FRange fr = a.frange[(long long)ey * a.E + ex];
+      const FRange fr = a.frange[(long long)rs.k[ky] * a.E + ex];
       const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
       if (s < s_lo || s >= s_lo + cnt) continue;
       int cs;
@@ -919,7 +931,7 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s, int
         if ((int)(deferred[d] >> 16) != cr) continue;
         const int kxl = (deferred[d] >> 8) & 0xff, ky = deferred[d] & 0xff;
         const int ex = a.star_ids[lb + kxl], ey = rs.e[ky];
-        const FRange fr = a.frange[(long long)ey * a.E + ex];
+        const FRange fr = a.frange[(long long)rs.k[ky] * a.E + ex];
         contribute(ex, ey, kxl, ky, cr, fr, fr.lo_cnt & 0xffff);
       }
     } else {  // very high valence: rescan the combos of this case in order
@@ -928,7 +940,7 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s, int
         for (int ky = 0; ky < rs.n; ++ky) {
           const int ey = rs.e[ky];
           if (case_of(a.tri, ex, ey) != cr) continue;
-          const FRange fr = a.frange[(long long)ey * a.E + ex];
+          const FRange fr = a.frange[(long long)rs.k[ky] * a.E + ex];
           const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
           if (s < s_lo || s >= s_lo + cnt) continue;
           contribute(ex, ey, kx - lb, ky, cr, fr, s_lo);
@@ -945,7 +957,7 @@ __global__ void k_pattern_fill(PatternArgs a) {
   extern __shared__ unsigned smem_u[];
   unsigned* bm = smem_u;
   int* pref = reinterpret_cast<int*>(smem_u + a.s_count * a.words);  // words + 1
-  const int j = blockIdx.x;
+  const int rloc = blockIdx.x, j = a.rows[rloc];
   __shared__ RowStar rs;
   if (threadIdx.x == 0) {
     const int b = a.star_off[j], e = a.star_off[j + 1];
@@ -953,6 +965,7 @@ __global__ void k_pattern_fill(PatternArgs a) {
     for (int k = 0; k < rs.n; ++k) {
       const int ey = a.star_ids[b + k];
       rs.e[k] = ey;
+      rs.k[k] = a.ey_map[ey];
       for (int t = 0; t < 3; ++t) {
         rs.t[k][t] = a.tri[3 * ey + t];
         if (rs.t[k][t] == j) rs.pj[k] = t;
@@ -964,7 +977,7 @@ __global__ void k_pattern_fill(PatternArgs a) {
   __shared__ typename Scan::TempStorage tmp;
   for (int sl = 0; sl < a.s_count; ++sl) {
     const unsigned* b = bm + sl * a.words;
-    const long long row = (long long)(a.s_begin + sl) * a.M + j;
+    const long long row = (long long)(a.s_begin + sl) * a.nrows + rloc;
     const int64_t base = a.indptr[row];
     // exclusive prefix of popcounts over words (chunks of 256 words)
     int carry = 0;
@@ -1100,7 +1113,7 @@ template <int NM>
 int launch_fill(const PatternArgs& pa, size_t smem, cudaStream_t st) {
   TDB_CUDA_CHECK(cudaFuncSetAttribute(k_pattern_fill<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
-  k_pattern_fill<NM><<<pa.M, 256, smem, st>>>(pa);
+  k_pattern_fill<NM><<<pa.nrows, 256, smem, st>>>(pa);
   TDB_CUDA_CHECK(cudaGetLastError());
   return TDB_OK;
 }
@@ -1110,7 +1123,12 @@ int launch_fill(const PatternArgs& pa, size_t smem, cudaStream_t st) {
 // Persistent assembly workspace: everything sized once in tdb_system_create,
 // every kernel re-run (no host synchronisation in between) by tdb_system_run.
 struct AsmWorkspace {
-  long long E2 = 0;
+  long long E2 = 0;   // pairs of this system: Et * E
+  int Et = 0, nrows = 0;
+  int* tt = nullptr;      // (Et,) test triangles
+  int* ey_map = nullptr;  // (E,) triangle -> pair row or -1
+  int* rows = nullptr;    // (nrows,) owned test vertices
+  unsigned char* owned = nullptr;  // (V,) 1 if owned
   double* blob = nullptr;
   std::vector<int> fam_blob_off, fam_blob_len;
   RuleDev rules[4];
@@ -1155,6 +1173,10 @@ struct AsmWorkspace {
     cudaFree(part);
     cudaFree(counters);
     cudaFree(cub_tmp);
+    cudaFree(tt);
+    cudaFree(ey_map);
+    cudaFree(rows);
+    cudaFree(owned);
     for (auto& L : launches) {
       cudaFree(L.d_fam);
       cudaFree(L.d_blob);
@@ -1191,6 +1213,9 @@ static PlanArgs plan_args(TdbSystem* sys) {
   PlanArgs pa;
   pa.E = (int)sys->E;
   pa.F = sys->F;
+  pa.Et = ws->Et;
+  pa.tt = ws->tt;
+  pa.owned = ws->owned;
   pa.corners = sys->corners;
   pa.tri = sys->tri;
   pa.fams = sys->famdev;
@@ -1209,13 +1234,16 @@ static PatternArgs pattern_args(TdbSystem* sys, int f) {
   PatternArgs ga{};
   ga.E = (int)sys->E;
   ga.M = (int)sys->V;
+  ga.nrows = ws->nrows;
+  ga.rows = ws->rows;
+  ga.ey_map = ws->ey_map;
   ga.f = f;
   ga.npos = sys->fam[f].npos;
   ga.words = ws->words;
   ga.tri = sys->tri;
   ga.star_off = sys->star_off;
   ga.star_ids = sys->star_ids;
-  ga.frange = ws->frange + (long long)f * ws->E2;
+  ga.frange = ws->frange + (long long)f * ws->E2;  // pair rows k*E + ex
   ga.row_count = reinterpret_cast<long long*>(sys->fam[f].indptr);
   ga.indptr = sys->fam[f].indptr;
   ga.indices = sys->fam[f].indices;
@@ -1258,10 +1286,10 @@ static int run_pattern_count(TdbSystem* sys, int f, cudaStream_t st) {
     const size_t smem = (size_t)ga.s_count * ws->words * 4;
     TDB_CUDA_CHECK(cudaFuncSetAttribute(k_pattern_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
-    k_pattern_count<<<(int)sys->V, 256, smem, st>>>(ga);
+    k_pattern_count<<<ws->nrows, 256, smem, st>>>(ga);
     TDB_CUDA_CHECK(cudaGetLastError());
   }
-  const long long nrows = (long long)npos * sys->V;
+  const long long nrows = (long long)npos * ws->nrows;
   TDB_CUDA_CHECK(cudaMemsetAsync(ga.row_count + nrows, 0, sizeof(long long), st));
   return scan_inplace(ws, ga.row_count, nrows + 1, st);
 }
@@ -1292,6 +1320,8 @@ int tdb_system_run_impl(TdbSystem* sys) {
   for (const auto& L : ws->launches) {
     QuadArgs qa;
     qa.E = (int)sys->E;
+    qa.npair = ws->E2;
+    qa.tt = ws->tt;
     qa.fam_count = (int)L.fams.size();
     for (int i = 0; i < qa.fam_count; ++i) qa.fam_ids[i] = L.fams[i];
     qa.fams = L.d_fam;
@@ -1354,6 +1384,7 @@ int tdb_system_run_impl(TdbSystem* sys) {
     sys->stats.pairs_case[c] = (int64_t)cnt[40 + c];
     sys->stats.units_case[c] = (int64_t)cnt[44 + c];
   }
+  sys->stats.units_primary = (int64_t)cnt[48];
   sys->stats.launches = ws->launch_count;
   sys->stats.n_in = (int64_t)cnt[0];
   sys->stats.n_geom = n_geom;
@@ -1649,8 +1680,42 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
   }
   if ((rc = dupload(&sys->famdev, sys->famdev_host.data(), F, st))) return rc;
 
+  // ---- row subset (multi-GPU row blocks) ----
+  {
+    std::vector<int> rows, tt, eymap(E, -1);
+    if (desc->num_rows > 0) {
+      for (long long i = 0; i < desc->num_rows; ++i) {
+        TDB_REQUIRE(desc->rows[i] >= 0 && desc->rows[i] < V, "assemble: row out of range");
+        TDB_REQUIRE(i == 0 || desc->rows[i] > desc->rows[i - 1], "assemble: rows must be strictly increasing");
+        rows.push_back((int)desc->rows[i]);
+      }
+    } else {
+      for (long long v = 0; v < V; ++v) rows.push_back((int)v);
+    }
+    // test triangles = union of the owned rows' stars (ascending)
+    std::vector<char> need(E, 0);
+    for (int j : rows)
+      for (int k = soff[j]; k < soff[j + 1]; ++k) need[sids[k]] = 1;
+    for (long long e = 0; e < E; ++e)
+      if (need[e]) {
+        eymap[e] = (int)tt.size();
+        tt.push_back((int)e);
+      }
+    if (tt.empty()) tt.push_back(0);  // keep buffers non-empty (no rows -> no work)
+    ws->nrows = (int)rows.size();
+    ws->Et = desc->num_rows > 0 && rows.empty() ? 0 : (int)tt.size();
+    if ((rc = dupload(&ws->rows, rows.data(), rows.size(), st))) return rc;
+    if ((rc = dupload(&ws->tt, tt.data(), tt.size(), st))) return rc;
+    if ((rc = dupload(&ws->ey_map, eymap.data(), eymap.size(), st))) return rc;
+    std::vector<unsigned char> own(V, 0);
+    for (int j : rows) own[j] = 1;
+    if ((rc = dupload(&ws->owned, own.data(), own.size(), st))) return rc;
+    sys->nrows = ws->nrows;
+  }
+  TDB_REQUIRE(ws->nrows > 0, "assemble: no rows to assemble");
+
   // ---- plan buffers and sizes ----
-  ws->E2 = E * E;
+  ws->E2 = (long long)ws->Et * E;
   const long long E2 = ws->E2;
   if ((rc = dalloc(&ws->frange, (size_t)F * E2))) return rc;
   if ((rc = dalloc(&ws->units, E2))) return rc;
@@ -1664,7 +1729,7 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
   for (int f = 0; f < F; ++f) {
     const int npos = sys->fam[f].npos;
     ws->s_chunk[f] = std::max(1, (int)std::min<long long>(npos, (96LL * 1024) / (ws->words * 4)));
-    max_rows = std::max(max_rows, (long long)npos * V + 1);
+    max_rows = std::max(max_rows, (long long)npos * V + 1);  // >= npos * nrows + 1
   }
   {
     size_t b1 = 0, b2 = 0;
@@ -1697,7 +1762,7 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
   long long nnz_total = 0;
   for (int f = 0; f < F; ++f) {
     FamilyStore& fs = sys->fam[f];
-    const long long nrows = (long long)fs.npos * V;
+    const long long nrows = (long long)fs.npos * ws->nrows;
     if ((rc = dalloc(&fs.indptr, nrows + 1))) return rc;
     if ((rc = run_pattern_count(sys, f, st))) return rc;
     long long nnz = 0;

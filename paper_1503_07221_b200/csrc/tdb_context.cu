@@ -152,7 +152,7 @@ int tdb_system_copy_family(const TdbSystem* sys, int32_t f, int64_t* indptr, int
   TDB_REQUIRE(f >= 0 && f < sys->F, "family index out of range");
   const FamilyStore& fs = sys->fam[f];
   TDB_CUDA_CHECK(cudaSetDevice(sys->ctx->device));
-  const size_t nrows = (size_t)fs.npos * sys->V;
+  const size_t nrows = (size_t)fs.npos * sys->nrows;
   if (indptr)
     TDB_CUDA_CHECK(cudaMemcpy(indptr, fs.indptr, (nrows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
   if (indices && fs.nnz)

@@ -79,6 +79,7 @@ struct TdbSystem {
   AsmWorkspace* ws = nullptr;
   int p = 0, np1 = 1, nm = 1, nacc = 10, F = 0;
   long long E = 0, V = 0;
+  int nrows = 0;  // owned test-vertex rows (== V for a full system)
   // mesh
   double* corners = nullptr;
   double* a2 = nullptr;

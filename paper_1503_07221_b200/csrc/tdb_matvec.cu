@@ -35,6 +35,7 @@ struct FamCsr {
 
 struct MvArgs {
   int M, NP1, NM;
+  int nrows;                // owned test-vertex rows (warps per group)
   int rlo, nr, clo, nc;     // block ranges
   int words;
   int G;
@@ -49,13 +50,14 @@ struct MvArgs {
 };
 
 __global__ void k_transpose_in(const double* __restrict__ x, double* __restrict__ xt, int M,
-                               int ncols) {
-  // x[(c)*M + l] -> xt[l*ncols + c], c = (block col)*NP1 + m1
+                               int ncols, const long long* __restrict__ xmap, long long xstride) {
+  // x[xmap[l] + c*xstride] -> xt[l*ncols + c], c = (block col)*NP1 + m1
   __shared__ double tile[32][33];
   const int c0 = blockIdx.y * 32, l0 = blockIdx.x * 32;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int c = c0 + k, l = l0 + threadIdx.x;
-    if (c < ncols && l < M) tile[k][threadIdx.x] = x[(long long)c * M + l];
+    if (c < ncols && l < M)
+      tile[k][threadIdx.x] = x[(xmap ? xmap[l] : (long long)l) + (long long)c * xstride];
   }
   __syncthreads();
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
@@ -69,8 +71,8 @@ __global__ void __launch_bounds__(256) k_matvec(MvArgs a) {
   constexpr int NM = NP1 * NP1;
   const int lane = threadIdx.x & 31;
   const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  if (w >= (long long)a.M * a.G) return;
-  const int j = (int)(w % a.M), g = (int)(w / a.M);
+  if (w >= (long long)a.nrows * a.G) return;
+  const int j = (int)(w % a.nrows), g = (int)(w / a.nrows);  // j = local row
   const int ncol = a.nc * NP1;
   double acc[kMaxRowChunks][NP1];
 #pragma unroll
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(256) k_matvec(MvArgs a) {
       }
     }
     if (__ballot_sync(0xffffffffu, valid != 0) == 0) continue;
-    const long long row = (long long)s * a.M + j;
+    const long long row = (long long)s * a.nrows + j;
     const int64_t e0 = fc.indptr[row], e1 = fc.indptr[row + 1];
     for (int64_t e = e0; e < e1; ++e) {
       const int l = fc.indices[e];
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(256) k_matvec(MvArgs a) {
       }
     }
   }
-  double* yp = a.ypart + ((long long)g * a.M + j) * (a.nr * NP1);
+  double* yp = a.ypart + ((long long)g * a.nrows + j) * (a.nr * NP1);
 #pragma unroll
   for (int c = 0; c < kMaxRowChunks; ++c) {
     const int r = lane + 32 * c;
@@ -152,6 +154,8 @@ using namespace tdb;
 struct TdbMatvecPlan {
   TdbSystem* sys = nullptr;
   MvArgs args{};
+  long long* d_xmap = nullptr;
+  long long xstride = 0;
   FamCsr* d_fam = nullptr;
   int* d_ints = nullptr;       // term_f, term_s, term_d, group_begin
   unsigned* d_mask = nullptr;
@@ -167,6 +171,7 @@ extern "C" int tdb_matvec_plan_destroy(TdbMatvecPlan* p) {
   cudaFree(p->d_mask);
   cudaFree(p->d_xt);
   cudaFree(p->d_ypart);
+  cudaFree(p->d_xmap);
   delete p;
   return TDB_OK;
 }
@@ -179,7 +184,7 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   TDB_REQUIRE(d->words == (d->N + 31) / 32, "matvec: words must be ceil(N/32)");
   TDB_REQUIRE(d->nterms >= 0, "negative term count");
   TDB_CUDA_CHECK(cudaSetDevice(sys->ctx->device));
-  const int M = (int)sys->V, NP1 = sys->np1, NM = sys->nm;
+  const int M = (int)sys->V, NP1 = sys->np1, NM = sys->nm, NR = sys->nrows;
   TdbMatvecPlan* p = new TdbMatvecPlan();
   p->sys = sys;
   const int nt = d->nterms;
@@ -195,8 +200,8 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
       return TDB_E_INVALID;
     }
     int64_t b[2];
-    cudaMemcpy(b, sys->fam[f].indptr + (long long)s * M, sizeof(int64_t), cudaMemcpyDeviceToHost);
-    cudaMemcpy(b + 1, sys->fam[f].indptr + (long long)(s + 1) * M, sizeof(int64_t), cudaMemcpyDeviceToHost);
+    cudaMemcpy(b, sys->fam[f].indptr + (long long)s * NR, sizeof(int64_t), cudaMemcpyDeviceToHost);
+    cudaMemcpy(b + 1, sys->fam[f].indptr + (long long)(s + 1) * NR, sizeof(int64_t), cudaMemcpyDeviceToHost);
     tnnz[t] = b[1] - b[0];
     int nlog = 0;
     for (int w = 0; w < d->words; ++w) nlog += __builtin_popcount(d->term_mask[(long long)t * d->words + w]);
@@ -204,12 +209,12 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
     flops += 2.0 * NM * (double)tnnz[t] * nlog;
   }
   const int nr = d->rhi - d->rlo + 1, nc = d->chi - d->clo + 1;
-  bytes += 8.0 * ((double)nr + nc) * NP1 * M;
+  bytes += 8.0 * ((double)nr * NR + (double)nc * M) * NP1;
   p->bytes = bytes;
   p->flops = flops;
   // groups: enough warps to fill the chip on small meshes
   const int want_warps = sys->ctx->num_sms * 32;
-  int G = std::max(1, std::min(nt, (want_warps + M - 1) / M));
+  int G = std::max(1, std::min(nt, (want_warps + NR - 1) / NR));
   G = std::min(G, 64);
   std::vector<int> gb(G + 1, nt);
   {
@@ -247,11 +252,14 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   ALLOC_COPY(p->d_ints, ints.data(), ints.size(), int);
   ALLOC_COPY(p->d_mask, d->term_mask, (size_t)nt * d->words, unsigned);
   ALLOC_COPY(p->d_xt, (const double*)nullptr, (size_t)M * nc * NP1, double);
-  ALLOC_COPY(p->d_ypart, (const double*)nullptr, (size_t)G * M * nr * NP1, double);
+  ALLOC_COPY(p->d_ypart, (const double*)nullptr, (size_t)G * NR * nr * NP1, double);
+  if (d->x_map) ALLOC_COPY(p->d_xmap, reinterpret_cast<const long long*>(d->x_map), M, long long);
+  p->xstride = d->x_map ? d->x_stride : M;
 #undef ALLOC_COPY
   TDB_CUDA_CHECK(cudaStreamSynchronize(st));
   MvArgs& a = p->args;
   a.M = M;
+  a.nrows = NR;
   a.NP1 = NP1;
   a.NM = NM;
   a.rlo = d->rlo;
@@ -286,10 +294,10 @@ extern "C" int tdb_matvec(TdbMatvecPlan* p, const double* x, double* y) {
   const int ncols = a.nc * a.NP1, nrows = a.nr * a.NP1;
   {
     dim3 blk(32, 8), grd((a.M + 31) / 32, (ncols + 31) / 32);
-    k_transpose_in<<<grd, blk, 0, st>>>(x, p->d_xt, a.M, ncols);
+    k_transpose_in<<<grd, blk, 0, st>>>(x, p->d_xt, a.M, ncols, p->d_xmap, p->xstride);
   }
   {
-    const long long warps = (long long)a.M * a.G;
+    const long long warps = (long long)a.nrows * a.G;
     const int blocks = (int)((warps * 32 + 255) / 256);
     switch (a.NP1) {
       case 1: k_matvec<1><<<blocks, 256, 0, st>>>(a); break;
@@ -299,8 +307,8 @@ extern "C" int tdb_matvec(TdbMatvecPlan* p, const double* x, double* y) {
     }
   }
   {
-    dim3 blk(32, 8), grd((a.M + 31) / 32, (nrows + 31) / 32);
-    k_reduce_out<<<grd, blk, 0, st>>>(p->d_ypart, y, a.M, nrows, a.G);
+    dim3 blk(32, 8), grd((a.nrows + 31) / 32, (nrows + 31) / 32);
+    k_reduce_out<<<grd, blk, 0, st>>>(p->d_ypart, y, a.nrows, nrows, a.G);
   }
   TDB_CUDA_CHECK(cudaGetLastError());
   return TDB_OK;

@@ -1,0 +1,189 @@
+"""Row-block sharding over GPUs: one process per GPU, NCCL over NVLink.
+
+Assembly needs no communication: rank r owns a set of test-vertex rows J_r and
+assembles exactly those CSR rows of every canonical block from the pairs whose
+test triangle lies in a star of J_r (tdb_system_create with `rows`).  Rows are
+owned by the lowest-numbered adjacent triangle, and triangles are split into
+contiguous blocks; refinement numbers children of one parent consecutively, so
+blocks are spatially compact and the halo (test triangles shared between
+ranks, computed twice) stays small.
+
+Vectors are distributed the same way: each rank holds x[time][J_r].  A matvec
+all-gathers the iterate (one ncclAllGather of L*(p+1)*max|J_r| doubles into a
+rank-major buffer), the kernel reads it through an index map (no reshuffle
+copy) and produces the rank's rows of y.  Krylov dots/norms are all-reduced
+(solvers.TorchDistComm).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from .assembly import DeviceAssembly, QuadratureConfig, as_product_inputs, build_plan
+from .block_system import canonical_position, canonical_positions, is_zero_position
+from .kernel_weights import tables_for
+
+__all__ = ["partition_rows", "gathered_x_map", "DistributedBlockHessenbergMatrix", "assemble_system_distributed"]
+
+
+def partition_rows(mesh, nparts: int):
+    """Owned vertex rows per rank (sorted) and their test triangles (sorted)."""
+    E, V = mesh.num_triangles, mesh.num_vertices
+    tri = np.asarray(mesh.triangles)
+    owner_tri = np.full(V, E, dtype=np.int64)
+    for a in range(3):
+        np.minimum.at(owner_tri, tri[:, a], np.arange(E))
+    bounds = [(E * r) // nparts for r in range(nparts + 1)]
+    tri_rank = np.minimum(np.searchsorted(bounds, owner_tri, side="right") - 1, nparts - 1)
+    rows = [np.flatnonzero(tri_rank == r).astype(np.int64) for r in range(nparts)]
+    off, ids = mesh.star_csr
+    tests = []
+    for r in range(nparts):
+        need = np.zeros(E, dtype=bool)
+        for j in rows[r]:
+            need[ids[off[j] : off[j + 1]]] = True
+        tests.append(np.flatnonzero(need))
+    return rows, tests
+
+
+def gathered_x_map(rows_per_rank, M: int, ncols: int, nmax: int) -> np.ndarray:
+    """x_map for the all-gathered rank-major layout [rank][column][nmax] (TdbMatvecDesc)."""
+    xmap = np.empty(M, dtype=np.int64)
+    for r, rows in enumerate(rows_per_rank):
+        xmap[rows] = r * ncols * nmax + np.arange(len(rows))
+    return xmap
+
+
+class _DistMatvecPlan:
+    def __init__(self, A: "DistributedBlockHessenbergMatrix", rows, cols):
+        grid = A.grid
+        rlo, rhi = rows
+        clo, chi = cols
+        words = (grid.N + 31) // 32
+        where = A.dev.plan.where
+        terms: dict = {}
+        for kt in range(rlo, rhi + 1):
+            for it in range(max(clo, kt - grid.N), min(chi, kt + 1) + 1):
+                if is_zero_position(grid, A.diameter, kt, it):
+                    continue
+                c = canonical_position(grid, kt, it)
+                loc = where.get(c) if c is not None else None
+                if loc is None:
+                    continue
+                key = (loc[0], loc[1], kt - it)
+                m = terms.get(key)
+                if m is None:
+                    m = terms[key] = np.zeros(words, dtype=np.uint32)
+                m[(kt - 1) // 32] |= np.uint32(1 << ((kt - 1) % 32))
+        keys = sorted(terms)
+        self.handle = None
+        self.ncols = (chi - clo + 1) * (grid.p + 1)
+        if not keys:
+            return
+        tf = np.array([k[0] for k in keys], dtype=np.int32)
+        ts = np.array([k[1] for k in keys], dtype=np.int32)
+        td = np.array([k[2] for k in keys], dtype=np.int32)
+        tm = np.ascontiguousarray(np.stack([terms[k] for k in keys]))
+        self.xmap = gathered_x_map(A.rows_per_rank, A.M_global, self.ncols, A.nmax)
+        desc = _lib.TdbMatvecDesc()
+        desc.N, desc.rlo, desc.rhi, desc.clo, desc.chi = grid.N, rlo, rhi, clo, chi
+        desc.nterms, desc.words = len(keys), words
+        desc.term_family, desc.term_pos = _lib.ptr(tf, C.c_int32), _lib.ptr(ts, C.c_int32)
+        desc.term_d, desc.term_mask = _lib.ptr(td, C.c_int32), _lib.ptr(tm, C.c_uint32)
+        desc.x_stride = A.nmax
+        desc.x_map = _lib.ptr(self.xmap, C.c_int64)
+        h = C.c_void_p()
+        _lib.check(_lib.LIB.tdb_matvec_plan_create(A.dev.handle, C.byref(desc), C.byref(h)), "matvec_plan_create")
+        self.handle = h
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            _lib.LIB.tdb_matvec_plan_destroy(h)
+            self.handle = None
+
+
+class DistributedBlockHessenbergMatrix:
+    """This rank's rows of the block Hessenberg matrix (duck-types BlockHessenbergMatrix
+    for the solvers: .grid, .M (local rows), .matvec(x_local, rows, cols))."""
+
+    def __init__(self, mesh, grid, rows_per_rank, rank: int, ctx=None, tables=None,
+                 config: QuadratureConfig = QuadratureConfig(), gather=None):
+        mesh, grid = as_product_inputs(mesh, grid)
+        self.grid = grid
+        self.diameter = mesh.diameter
+        self.rank = rank
+        self.rows_per_rank = rows_per_rank
+        self.nparts = len(rows_per_rank)
+        self.rows = rows_per_rank[rank]
+        self.M_global = mesh.num_vertices
+        self.M = len(self.rows)  # local rows (what the solvers' half-splits use)
+        self.nmax = max(len(r) for r in rows_per_rank)
+        tables = tables_for(grid) if tables is None else tables
+        plan = build_plan(mesh, grid, tables, canonical_positions(grid, mesh.diameter), config)
+        self.dev = DeviceAssembly(mesh, plan, ctx or _lib.default_context(), rows=self.rows)
+        self._plans: dict = {}
+        # gather(local_padded (ncols, nmax) tensor) -> (nparts, ncols, nmax) tensor
+        self._gather = gather
+
+    @property
+    def shape_local(self):
+        return (self.grid.L * self.M, self.grid.L * self.M_global)
+
+    def _plan(self, rows, cols):
+        key = (tuple(rows), tuple(cols))
+        p = self._plans.get(key)
+        if p is None:
+            p = self._plans[key] = _DistMatvecPlan(self, rows, cols)
+        return p
+
+    def allgather(self, x_local: torch.Tensor, ncols: int) -> torch.Tensor:
+        pad = torch.zeros((ncols, self.nmax), dtype=x_local.dtype, device=x_local.device)
+        pad[:, : self.M] = x_local.view(ncols, self.M)
+        if self._gather is not None:
+            return self._gather(pad)
+        import torch.distributed as dist
+
+        out = torch.empty((self.nparts, ncols, self.nmax), dtype=x_local.dtype, device=x_local.device)
+        dist.all_gather_into_tensor(out, pad.contiguous())
+        return out
+
+    def matvec(self, x_local: torch.Tensor, rows=None, cols=None) -> torch.Tensor:
+        np1 = self.grid.p + 1
+        rlo, rhi = rows if rows is not None else (1, self.grid.N)
+        clo, chi = cols if cols is not None else (1, self.grid.N)
+        ncols = (chi - clo + 1) * np1
+        if x_local.numel() != ncols * self.M:
+            raise ValueError("matvec dimension mismatch")
+        plan = self._plan((rlo, rhi), (clo, chi))
+        xg = self.allgather(x_local.contiguous(), ncols).contiguous()
+        nrow = (rhi - rlo + 1) * np1 * self.M
+        y = torch.zeros(nrow, dtype=x_local.dtype, device=x_local.device)
+        if plan.handle is not None and nrow:
+            self.dev.ctx.set_stream(torch.cuda.current_stream(x_local.device).cuda_stream)
+            _lib.check(_lib.LIB.tdb_matvec(plan.handle, C.c_void_p(xg.data_ptr()), C.c_void_p(y.data_ptr())),
+                       "matvec")
+        return y
+
+    def __matmul__(self, x):
+        return self.matvec(x)
+
+    def local_of(self, x_full: np.ndarray, ncols: int | None = None) -> np.ndarray:
+        """This rank's piece [column][J_r] of a time-major global vector."""
+        ncols = ncols or self.grid.L
+        return np.ascontiguousarray(np.asarray(x_full).reshape(ncols, self.M_global)[:, self.rows]).ravel()
+
+    def stats(self) -> dict:
+        return self.dev.stats()
+
+
+def assemble_system_distributed(mesh, grid, rank: int, world: int, ctx=None, tables=None,
+                                config: QuadratureConfig = QuadratureConfig()):
+    """Assemble this rank's row block (torch.distributed must be initialised for matvecs)."""
+    mesh, grid = as_product_inputs(mesh, grid)
+    rows, _ = partition_rows(mesh, world)
+    return DistributedBlockHessenbergMatrix(mesh, grid, rows, rank, ctx=ctx, tables=tables, config=config)

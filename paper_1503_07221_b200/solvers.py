@@ -28,6 +28,8 @@ import scipy.linalg as sla
 import torch
 
 __all__ = [
+    "set_comm",
+    "TorchDistComm",
     "SolverConfig",
     "DeflationState",
     "BreakdownError",
@@ -63,8 +65,49 @@ class SolverConfig:
             raise ValueError("deflation counts must satisfy 0 <= l <= r")
 
 
+class _LocalComm:
+    """Single device: vectors are whole, reductions are no-ops."""
+
+    size = 1
+
+    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        return t
+
+
+class TorchDistComm:
+    """Row-block distributed vectors: every Krylov vector holds this
+    rank's vertex rows for all time steps; dot products and norms are
+    all-reduced (NCCL on CUDA tensors, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.size = dist.get_world_size(group)
+
+    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        self.dist.all_reduce(t, group=self.group)
+        return t
+
+
+_COMM = _LocalComm()
+
+
+def set_comm(comm) -> None:
+    """Select the communicator used by every solver (None -> single device)."""
+    global _COMM
+    _COMM = comm if comm is not None else _LocalComm()
+
+
+def _dot(u: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
+    return _COMM.allreduce_(torch.dot(u, v).reshape(1))[0]
+
+
 def _norm(v: torch.Tensor) -> torch.Tensor:
-    return torch.linalg.vector_norm(v)
+    if _COMM.size == 1:
+        return torch.linalg.vector_norm(v)
+    return torch.sqrt(_COMM.allreduce_(torch.dot(v, v).reshape(1))[0])
 
 
 class DeflationState:
@@ -81,14 +124,14 @@ class DeflationState:
         return self.U.shape[1]
 
     def t_small(self) -> np.ndarray:
-        return (self.U.T @ self.AU).cpu().numpy()
+        return _COMM.allreduce_((self.U.T @ self.AU).contiguous()).cpu().numpy()
 
     def apply_minv(self, v: torch.Tensor) -> torch.Tensor:
         if self.rank == 0:
             return v
         if self._lu is None:
             self._lu = sla.lu_factor(self.t_small())
-        w = self.U.T @ v
+        w = _COMM.allreduce_((self.U.T @ v).contiguous())
         y = sla.lu_solve(self._lu, w.cpu().numpy())
         y = torch.as_tensor(y, dtype=v.dtype, device=v.device)
         return v + self.U @ (self.lambda_max * y - w)
@@ -143,7 +186,7 @@ def _orthonormal_extend(U: torch.Tensor, W: torch.Tensor, drop_tol: float = 1e-1
         w = W[:, j].clone()
         for _ in range(2):
             for u in cols:
-                w = w - torch.dot(u, w) * u
+                w = w - _dot(u, w) * u
         nw = float(_norm(w))
         if nw > drop_tol:
             cols.append(w / nw)
@@ -183,6 +226,8 @@ def _gmres_cycle_raw(apply_A, b, x0, m, tol_abs, precond, history):
         # modified Gram-Schmidt: h_j computed and subtracted one vector at a time
         for j in range(k + 1):
             torch.dot(V[j], w, out=hcol[j])
+            if _COMM.size > 1:
+                _COMM.allreduce_(hcol[j : j + 1])
             w.addcmul_(V[j], hcol[j : j + 1], value=-1.0)
         hcol[k + 1] = _norm(w)
         col = hcol[: k + 2].cpu().numpy()

@@ -267,3 +267,51 @@ def test_reference_lookalike_inputs(G, two_tri):
     grid = types.SimpleNamespace(T=2.0, N=4, p=1)
     A = G[2].assemble_system(mesh, grid)
     assert np.linalg.norm(A @ g["x7"] - g["y7"]) <= 1e-12 * np.linalg.norm(g["y7"])
+
+
+def test_row_partition_bitwise_and_emulated_allgather(G, cfg1_mesh):
+    # every row block's CSR rows and matvec rows are bit-identical to the
+    # full system's; the all-gathered x layout is read through the x_map (ranks emulated
+    # on one device, the gather is the concatenation an ncclAllGather would produce)
+    import torch
+
+    from paper_1503_07221_b200.distributed import DistributedBlockHessenbergMatrix, partition_rows
+    from paper_1503_07221_b200.temporal_basis import TimeGrid
+
+    grid = TimeGrid(T=3.9, N=40, p=0)
+    A = G[2].assemble_system(cfg1_mesh, grid)
+    M = cfg1_mesh.num_vertices
+    R = 3
+    rows, _ = partition_rows(cfg1_mesh, R)
+    parts = [DistributedBlockHessenbergMatrix(cfg1_mesh, grid, rows, r) for r in range(R)]
+    assert sum(p.stats()["units_primary"] for p in parts) == A.stats()["units"]
+    # CSR rows identical
+    for f in range(A._dev.num_families):
+        ip, ix, dv = A._dev.family_arrays(f)
+        npos = len(A._dev.plan.families[f].positions)
+        for r, p in enumerate(parts):
+            lip, lix, ldv = p.dev.family_arrays(f)
+            for s in range(0, npos, max(1, npos // 5)):
+                for k, j in enumerate(rows[r][:: max(1, len(rows[r]) // 7)]):
+                    kk = int(np.searchsorted(rows[r], j))
+                    a0, a1 = ip[s * M + j], ip[s * M + j + 1]
+                    b0, b1 = lip[s * len(rows[r]) + kk], lip[s * len(rows[r]) + kk + 1]
+                    assert np.array_equal(ix[a0:a1], lix[b0:b1]) and np.array_equal(dv[a0:a1], ldv[b0:b1])
+    x = np.random.default_rng(5).standard_normal(A.shape[1])
+    for rws, cls in ((None, None), ((3, 17), (2, 20)), ((21, 40), (1, 40))):
+        rlo, rhi = rws or (1, 40)
+        clo, chi = cls or (1, 40)
+        xs = x[(clo - 1) * M : chi * M]
+        y_full = A.matvec(xs, rows=rws, cols=cls)
+        ncols = chi - clo + 1
+        nmax = max(len(r) for r in rows)
+        stacked = torch.zeros((R, ncols, nmax), dtype=torch.float64, device="cuda")
+        for r in range(R):
+            stacked[r, :, : len(rows[r])] = torch.as_tensor(xs.reshape(ncols, M)[:, rows[r]])
+        y = np.zeros(((rhi - rlo + 1), M))
+        for r, p in enumerate(parts):
+            p._gather = lambda pad, st=stacked: st
+            xl = torch.as_tensor(p.local_of(xs, ncols)).cuda()
+            yl = p.matvec(xl, rows=rws, cols=cls).cpu().numpy().reshape(rhi - rlo + 1, len(rows[r]))
+            y[:, rows[r]] = yl
+        assert np.array_equal(y.ravel(), y_full)
