@@ -402,3 +402,61 @@ def tri_distance_bounds(mesh: SurfaceMesh, rows=None, ctx: _lib.Context | None =
         ctx.handle, _lib.C.byref(_mesh_c(mesh, keep)), len(rows), _lib.ptr(rows, _lib.C.c_int64),
         _lib.ptr(tmin), _lib.ptr(tmax)), "tri_distance_bounds")
     return tmin, tmax
+
+
+def assemble_rhs(mesh: SurfaceMesh, grid: TimeGrid, g, config: QuadratureConfig = QuadratureConfig()):
+    """Load vector b[(k-1) M + l] = int int g(x, t) phi_l(x) bdot_k(t) dx dt (host).
+
+    Restates assembly.py:314-355 of the reference: regular q_reg triangle rule in
+    space; in time, Gauss panels of 2(p+4) points over quarter steps of each
+    basis function's support.  g(X (n,3), t) -> (n,).  (the
+    device version is the next step.)
+    """
+    from .quadrature import gauss_rule, triangle_rule
+    from .temporal_basis import basis_b, flat_index, support_interval
+
+    mesh, grid = as_product_inputs(mesh, grid)
+    m = mesh.num_vertices
+    pts, w = triangle_rule(config.q_reg)
+    c = mesh.corners
+    X = (c[:, None, 0, :] + pts[None, :, 0, None] * (c[:, 1] - c[:, 0])[:, None, :]
+         + pts[None, :, 1, None] * (c[:, 2] - c[:, 1])[:, None, :]).reshape(-1, 3)
+    wx = (w[None, :] * 2.0 * mesh.areas[:, None]).reshape(-1)
+    sh = np.column_stack([1.0 - pts[:, 0], pts[:, 0] - pts[:, 1], pts[:, 1]])
+    dofs = np.repeat(mesh.triangles, len(pts), axis=0).reshape(-1)
+    shw = np.tile(sh, (mesh.num_triangles, 1)) * wx[:, None]
+    xg, wg = gauss_rule(2 * (grid.p + 4))
+    out = np.zeros(grid.L * m)
+    for k in range(1, grid.L + 1):
+        idx = flat_index(grid, (k - 1) // (grid.p + 1) + 1, (k - 1) % (grid.p + 1))
+        lo, hi = support_interval(grid, idx.timestep)
+        nhalf = max(1, round((hi - lo) / (0.25 * grid.dt)))
+        comp = np.zeros(m)
+        for panel in range(nhalf):
+            a = lo + (hi - lo) * panel / nhalf
+            b = lo + (hi - lo) * (panel + 1) / nhalf
+            tq = 0.5 * (a + b) + 0.5 * (b - a) * xg
+            tw = 0.5 * (b - a) * wg * basis_b(grid, idx, tq, deriv=1)
+            for ts, ws in zip(tq, tw):
+                if ws == 0.0:
+                    continue
+                gv = np.asarray(g(X, ts), dtype=float)
+                comp += np.bincount(dofs, weights=(shw * gv[:, None] * ws).reshape(-1), minlength=m)
+        out[(k - 1) * m : k * m] = comp
+    return out
+
+
+def gaussian_pulse_neumann(mesh: SurfaceMesh, sigma: float = 0.2, t0: float = 1.0):
+    """g = -d_n u_inc for u_inc = f(t - t0 - (z - z_min)), f(s) = exp(-s^2/(2 sigma^2))
+    (plane wave along +z with a Gaussian envelope; g = n_z f'(s)).
+    Points are the triangle-rule points in element order, as assemble_rhs passes them."""
+    zmin = float(mesh.vertices[:, 2].min())
+    nz = mesh.normals[:, 2]
+
+    def g(X, t):
+        nq = len(X) // mesh.num_triangles
+        s = t - t0 - (X[:, 2] - zmin)
+        f = np.exp(-s * s / (2.0 * sigma * sigma))
+        return np.repeat(nz, nq) * (-s / sigma**2) * f
+
+    return g

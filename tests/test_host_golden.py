@@ -85,3 +85,18 @@ def test_tables_match_reference(T, N, p):
         assert np.max(np.abs(tbl.coeffs - ref)) <= 1e-14 * max(1.0, np.max(np.abs(ref)))
         seen += 1
     assert seen > 0
+
+
+def test_rhs_matches_reference(two_tri):
+    from paper_1503_07221_b200.assembly import assemble_rhs, gaussian_pulse_neumann
+
+    g = golden("rhs.npz")
+    m = M.icosphere(2)
+    b = assemble_rhs(m, TimeGrid(T=3.9, N=40, p=0), gaussian_pulse_neumann(m))
+    assert np.max(np.abs(b - g["cfg1_pulse"])) <= 1e-14 * np.max(np.abs(g["cfg1_pulse"]))
+
+    def gs(X, t):
+        return (X[:, 0] + 2 * X[:, 1] - X[:, 2]) * np.sin(3 * t) * t * t * np.exp(-t)
+
+    b2 = assemble_rhs(two_tri, TimeGrid(T=3.0, N=5, p=1), gs)
+    assert np.max(np.abs(b2 - g["two_tri_smooth"])) <= 1e-14 * np.max(np.abs(g["two_tri_smooth"]))
