@@ -13,8 +13,10 @@ units = admissible (triangle pair, block position) quadratures.  `e2e` is the
 same metric through the public API (assemble_system from host arrays, all
 blocks copied back to host as CSR).
 
-N > 1 (torchrun, one process per GPU): every rank assembles the full system
-(replicas, weak scaling); times are the max over ranks.  --impl reference
+N > 1 (torchrun, one process per GPU): SURVEY 8e row-block sharding - each rank
+assembles its own test-vertex rows of every block with no communication (strong
+scaling over the fixed config); times are the max over ranks; value counts each
+global unit once (halo duplicates reported separately).  --impl reference
 times the reference's own compiled kernel (oracle/_ref) on the host cores on a
 stratified sample of the same workload (rank 0 only).
 """
@@ -93,9 +95,15 @@ def dist_init():
     if world > 1:
         import torch.distributed as dist
 
+        import torch
+
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         backend = "nccl" if os.environ.get("TDB_BENCH_BACKEND", "nccl") == "nccl" else "gloo"
-        dist.init_process_group(backend)
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group(backend, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
@@ -214,6 +222,43 @@ def unit_counts_host(mesh, plan):
     return out
 
 
+def sum_over_ranks(world, v: float, device) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def time_matvec(A, grid, dev, stream, reps=20):
+    """Full block-Hessenberg matvec (incl. the all-gather when sharded): ms per call."""
+    import torch
+
+    n_local = grid.L * A.M
+    x = torch.randn(n_local, dtype=torch.float64, device=dev)
+    for _ in range(3):
+        A.matvec(x)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        A.matvec(x)
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -224,8 +269,9 @@ def main():
     ap.add_argument("--ref-sample", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-solve", action="store_true")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 0)
+    args.warmup = max(args.warmup, 3)
     world, rank, local = dist_init()
     if args.impl == "reference":
         return run_reference(args, world, rank)
@@ -236,6 +282,7 @@ def main():
     from paper_1503_07221_b200.assembly import DeviceAssembly, build_plan
     from paper_1503_07221_b200.block_system import assemble_system, canonical_positions
     from paper_1503_07221_b200.configs import get_config
+    from paper_1503_07221_b200.distributed import DistributedBlockHessenbergMatrix, partition_rows
     from paper_1503_07221_b200.kernel_weights import tables_for
 
     torch.cuda.set_device(local)
@@ -249,8 +296,17 @@ def main():
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
 
-    # device-resident system: inputs uploaded + buffers sized once (untimed)
-    sys_ = DeviceAssembly(mesh, plan, ctx)
+    # device-resident system: inputs uploaded + buffers sized once (untimed).
+    # N > 1: SURVEY 8e row-block sharding - this rank assembles its own test-vertex
+    # rows of every block (no communication), strong scaling over a fixed config.
+    rows_per_rank = None
+    A_mv = None
+    if world > 1:
+        rows_per_rank, _ = partition_rows(mesh, world)
+        A_mv = DistributedBlockHessenbergMatrix(mesh, grid, rows_per_rank, rank, ctx=ctx, tables=tables)
+        sys_ = A_mv.dev
+    else:
+        sys_ = DeviceAssembly(mesh, plan, ctx)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)  # 256 MB > L2
     for _ in range(args.warmup):
         sys_.rerun()
@@ -262,6 +318,7 @@ def main():
     clocks.start()
     for _ in range(args.steps):
         flush.fill_(1.0)  # L2 flush between timed steps (outside the events)
+        barrier(world)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -275,8 +332,9 @@ def main():
     barrier(world)
     clk = clocks.stop()
     ms = max_over_ranks(world, float(np.mean(step_ms)), dev)
-    units = int(stats["units"])
-    value = world * units / (ms * 1e-3)
+    units = int(round(sum_over_ranks(world, float(stats["units_primary"]), dev)))
+    units_computed = int(round(sum_over_ranks(world, float(stats["units"]), dev)))
+    value = units / (ms * 1e-3)
 
     # roofline of the dominant kernel (the quadrature kernel), FP64-bound
     fl = flops_per_launch(stats, grid.p)
@@ -289,9 +347,26 @@ def main():
                 "peak_source": "measured in-run DFMA microbenchmark (tdb_fp64_peak); "
                                "MEASURED_PEAKS.json has no FP64 entry",
                 "peak_nominal": 37.2, "frac_of_nominal": achieved / 37.2,
-                "traffic": traffic, "kernel": "k_quad", "kernel_ms": q_ms,
+                "traffic": traffic if world == 1 else None, "kernel": "k_quad", "kernel_ms": q_ms,
                 "kernel_share_of_step": q_ms / float(np.mean(step_ms)),
-                "flops_per_launch": fl, "n_in": stats["n_in"], "n_geom": stats["n_geom"]}
+                "flops_per_launch": fl, "n_in": stats["n_in"], "n_geom": stats["n_geom"],
+                "note": "rank 0's kernel" if world > 1 else "single GPU"}
+
+    # block Hessenberg matvec (the solve's hot op): HBM roofline on algorithmic bytes
+    if A_mv is None:
+        from paper_1503_07221_b200.block_system import BlockHessenbergMatrix
+
+        A_mv = BlockHessenbergMatrix(grid=grid, M=mesh.num_vertices, diameter=mesh.diameter, _dev=sys_)
+    mv_ms = max_over_ranks(world, time_matvec(A_mv, grid, dev, stream), dev)
+    mvp = A_mv._plan((1, grid.N), (1, grid.N)) if world > 1 else A_mv.matvec_plan()
+    mv_bytes = sum_over_ranks(world, mvp.bytes if hasattr(mvp, "bytes") else 0.0, dev)
+    mv_flops = sum_over_ranks(world, mvp.flops if hasattr(mvp, "flops") else 0.0, dev)
+    hbm, hbm_src = hbm_peak()
+    matvec = {"ms": mv_ms, "algorithmic_bytes": mv_bytes, "flops": mv_flops,
+              "achieved_GBps": mv_bytes / (mv_ms * 1e-3) / 1e9 / max(1, world),
+              "hbm_peak_GBps": hbm, "frac_hbm_per_gpu": mv_bytes / (mv_ms * 1e-3) / 1e9 / world / hbm,
+              "peak_source": hbm_src,
+              "includes": "ncclAllGather of the iterate" if world > 1 else "transpose + SpMM + reduce"}
 
     # end to end through the public API (host mesh in, every block back on the host)
     e2e = None
@@ -302,8 +377,12 @@ def main():
             barrier(world)
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
-            A = assemble_system(mesh, grid, tables=tables, device=local)
-            host = [A._dev.family_arrays(f) for f in range(A._dev.num_families)]
+            if world > 1:
+                B = DistributedBlockHessenbergMatrix(mesh, grid, rows_per_rank, rank, ctx=ctx, tables=tables)
+                host = [B.dev.family_arrays(f) for f in range(B.dev.num_families)]
+            else:
+                B = assemble_system(mesh, grid, tables=tables, device=local)
+                host = [B._dev.family_arrays(f) for f in range(B._dev.num_families)]
             torch.cuda.synchronize(dev)
             t1 = time.perf_counter()
             if i > 0:  # first call warms the allocator / plan caches
@@ -313,12 +392,38 @@ def main():
                    + mesh.triangles.nbytes + 2 * mesh.triangles.nbytes
                    + sum(f.pack.coeffs.nbytes for f in plan.families)
                    + sum(sum(a.nbytes for a in plan.rules[c]) for c in plan.rules))
-            del A, host
+            del B, host
         ems = max_over_ranks(world, float(np.mean(e2e_ms)), dev)
-        e2e = {"value": world * units / (ems * 1e-3), "unit": UNIT, "ms_per_step": ems,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "path": "block_system.assemble_system (C ABI tdb_system_assemble) + "
+        e2e = {"value": units / (ems * 1e-3), "unit": UNIT, "ms_per_step": ems,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(sum_over_ranks(world, d2h, dev)),
+               "path": ("distributed.DistributedBlockHessenbergMatrix" if world > 1 else
+                        "block_system.assemble_system") + " (C ABI tdb_system_assemble) + "
                        "tdb_system_copy_family for every family"}
+
+    # FGMRES(50, 2(2,10)) solve, eps = 1e-5, Gaussian-pulse RHS
+    solve = None
+    if not args.no_solve:
+        from paper_1503_07221_b200 import solvers as S
+        from paper_1503_07221_b200.assembly import assemble_rhs, gaussian_pulse_neumann
+
+        b = assemble_rhs(mesh, grid, gaussian_pulse_neumann(mesh))
+        if world > 1:
+            S.set_comm(S.TorchDistComm())
+            bl = torch.as_tensor(A_mv.local_of(b)).to(dev)
+        else:
+            bl = torch.as_tensor(b).to(dev)
+        cfgS = S.SolverConfig(method="fgmres-recursive", restart=50, tol=1e-5, max_iter=2000,
+                              recursion_depth=2, inner_iterations=(2, 10))
+        barrier(world)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        x, hist = S.fgmres(lambda v: A_mv.matvec(v), bl, cfgS, precond=S.recursive_preconditioner(A_mv, cfgS))
+        torch.cuda.synchronize(dev)
+        ts = max_over_ranks(world, time.perf_counter() - t0, dev)
+        S.set_comm(None)
+        solve = {"method": "FGMRES(50, 2(2,10)) recursive block preconditioner", "tol": 1e-5,
+                 "seconds": ts, "iterations": len(hist), "final_rel_residual": float(hist[-1]),
+                 "rhs": "Gaussian-pulse plane wave (sigma 0.2, t0 1.0), assemble_rhs (host)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -335,13 +440,18 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8d meshes)",
             "config": {"workload": cfg.name, "units_per_step": units, "p": grid.p,
                        "positions": len(plan.where), "nnz": stats["nnz_total"],
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"row blocks x{world} (NCCL all-gather per matvec)" if world > 1
+                                       else "1 GPU"),
+                       "units_computed_incl_halo": units_computed,
                        "l2": "flushed between timed steps (256 MB write)"},
             "roofline": roofline,
+            "matvec": matvec,
+            "solve": solve,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(stats["launches"]) * args.steps,

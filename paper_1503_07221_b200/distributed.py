@@ -81,6 +81,8 @@ class _DistMatvecPlan:
                 m[(kt - 1) // 32] |= np.uint32(1 << ((kt - 1) % 32))
         keys = sorted(terms)
         self.handle = None
+        self.bytes = 0.0
+        self.flops = 0.0
         self.ncols = (chi - clo + 1) * (grid.p + 1)
         if not keys:
             return
@@ -99,6 +101,9 @@ class _DistMatvecPlan:
         h = C.c_void_p()
         _lib.check(_lib.LIB.tdb_matvec_plan_create(A.dev.handle, C.byref(desc), C.byref(h)), "matvec_plan_create")
         self.handle = h
+        b, f = C.c_double(), C.c_double()
+        _lib.check(_lib.LIB.tdb_matvec_plan_work(h, C.byref(b), C.byref(f)), "matvec_plan_work")
+        self.bytes, self.flops = b.value, f.value
 
     def __del__(self):
         h = getattr(self, "handle", None)

@@ -93,10 +93,14 @@ def _worker(rank, world, port, out):
 
 
 def test_distributed_krylov_matches_single_process():
-    mgr = mp.Manager()
+    # spawn-context manager: a forked manager process leaves the parent's BLAS
+    # thread pool deadlocked for later tests
+    mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
     port = free_port()
     mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
+    out = dict(out)
+    mgr.shutdown()
     rng = np.random.default_rng(3)
     n = 240
     D = np.eye(n) + (0.4 / np.sqrt(n)) * rng.standard_normal((n, n))
