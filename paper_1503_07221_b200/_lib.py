@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtdb.so")
+LIB_PATH = os.environ.get("TDB_LIBRARY") or os.path.join(HERE, "libtdb.so")  # override: tuning variants
 
 i32, i64, f64p, i64p, i32p, u8p = C.c_int32, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_uint8)
 
@@ -177,7 +177,7 @@ class Context:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and h.value:
+        if h is not None and h.value and LIB is not None:  # LIB is None at interpreter exit
             LIB.tdb_ctx_destroy(h)
             self.handle = None
 

@@ -356,7 +356,7 @@ class DeviceAssembly:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib.LIB is not None:  # LIB is None at interpreter exit
             _lib.LIB.tdb_system_destroy(h)
             self.handle = None
 

@@ -44,14 +44,17 @@ struct MvArgs {
   const int* term_s;
   const int* term_d;
   const unsigned* term_mask;
+  const int* term_kt;       // (nterms, 4): block rows of a "single" term, padded with 0;
+                            // kt[0] == -1 marks a lag term, 0 an empty mask
   const int* group_begin;   // (G+1,) term ranges
-  const double* xt;         // [M][nc*NP1]
+  const double* xt;         // [M][xs]: row l = x[l][block col][m1], then NP1 zeros
+  int xs;                   // row stride of xt = nc*NP1 + NP1
   double* ypart;            // [G][M][nr*NP1]
 };
 
 __global__ void k_transpose_in(const double* __restrict__ x, double* __restrict__ xt, int M,
-                               int ncols, const long long* __restrict__ xmap, long long xstride) {
-  // x[xmap[l] + c*xstride] -> xt[l*ncols + c], c = (block col)*NP1 + m1
+                               int ncols, int xs, const long long* __restrict__ xmap, long long xstride) {
+  // x[xmap[l] + c*xstride] -> xt[l*xs + c], c = (block col)*NP1 + m1 (pad columns stay 0)
   __shared__ double tile[32][33];
   const int c0 = blockIdx.y * 32, l0 = blockIdx.x * 32;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
@@ -62,70 +65,280 @@ __global__ void k_transpose_in(const double* __restrict__ x, double* __restrict_
   __syncthreads();
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int l = l0 + k, c = c0 + threadIdx.x;
-    if (c < ncols && l < M) xt[(long long)l * ncols + c] = tile[threadIdx.x][k];
+    if (c < ncols && l < M) xt[(long long)l * xs + c] = tile[threadIdx.x][k];
   }
 }
 
-template <int NP1>
-__global__ void __launch_bounds__(256) k_matvec(MvArgs a) {
+// ---- asynchronous staging of a warp's CSR stream (cp.async, double-buffered) ----
+__device__ __forceinline__ void cp_async4(void* smem, const void* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+template <int NM>
+struct MvStage {
+  static constexpr int CAP = NM <= 1 ? 256 : NM <= 4 ? 128 : 64;  // entries per buffer
+  static constexpr size_t BYTES = 2 * (size_t)CAP * (4 + 8 * NM);
+};
+
+// One chunk of a CSR row segment: term t, entries [b, b + n) (n <= CAP).
+struct MvChunk {
+  int t, n;
+  int64_t b;
+};
+
+// Producer cursor over the warp's (term, row j) CSR segments, split into chunks.
+struct MvCursor {
+  int t, te;           // next term to open, end of the group's term range
+  int cur;             // term of the open segment
+  int64_t e, e1;       // remaining entries of the open segment
+  int64_t ne0, ne1;    // prefetched row bounds of term t (valid if t < te)
+};
+
+template <int NM>
+__device__ __forceinline__ void mv_row_bounds(const MvArgs& a, int t, int j, int64_t& e0, int64_t& e1) {
+  const FamCsr* fc = a.fam + __ldg(a.term_f + t);
+  const long long row = (long long)__ldg(a.term_s + t) * a.nrows + j;
+  const int kt0 = __ldg(a.term_kt + 4 * t);
+  if (kt0 == 0) {  // empty mask: nothing to do
+    e0 = e1 = 0;
+    return;
+  }
+  const int64_t* ip = fc->indptr;
+  e0 = __ldg(ip + row);
+  e1 = __ldg(ip + row + 1);
+}
+
+template <int NM>
+__device__ __forceinline__ bool mv_next_chunk(const MvArgs& a, int j, MvCursor& c, MvChunk& out) {
+  constexpr int CAP = MvStage<NM>::CAP;
+  while (c.e >= c.e1) {
+    if (c.t >= c.te) return false;
+    c.cur = c.t;
+    c.e = c.ne0;
+    c.e1 = c.ne1;
+    ++c.t;
+    if (c.t < c.te) mv_row_bounds<NM>(a, c.t, j, c.ne0, c.ne1);  // look one term ahead
+  }
+  out.t = c.cur;
+  out.b = c.e;
+  out.n = (int)min((int64_t)CAP, c.e1 - c.e);
+  c.e += out.n;
+  return true;
+}
+
+template <int NM>
+__device__ __forceinline__ void mv_stage(const MvArgs& a, const MvChunk& ch, int* s_idx, double* s_val, int lane) {
+  const FamCsr* fc = a.fam + __ldg(a.term_f + ch.t);
+  const int32_t* gi = fc->indices + ch.b;
+  const double* gv = fc->data + ch.b * NM;
+  for (int q = lane; q < ch.n; q += 32) cp_async4(s_idx + q, gi + q);
+  for (int q = lane; q < ch.n * NM; q += 32) cp_async8(s_val + q, gv + q);
+}
+
+// Two inner loops, chosen per term (warp-uniform):
+//  * "lag" terms (a stored block reused at > kSpmvMaxKt block rows, the
+//    Toeplitz part): lanes own block rows kt.  Each staged entry (column l,
+//    value v) is broadcast from shared memory and multiplies the x strip
+//    xt[l][kt - d] of every valid lane; U entries' strips are loaded before any
+//    FMA (U * NC * NP1 independent loads in flight).  Invalid block rows load 0.
+//  * "single" terms (boundary blocks used at <= kSpmvMaxKt block rows, e.g. the
+//    first block column and last block row): lanes own entries (CSR SpMV, each
+//    entry read once), partial sums reduced with a fixed xor butterfly and added
+//    by the lane that owns the output block row.
+// The CSR stream (column indices + values) of the warp's terms is staged into
+// shared memory with cp.async one chunk ahead, so the HBM latency of the matrix
+// stream overlaps the FMAs of the previous chunk.  Accumulation order is fixed
+// by the plan (deterministic run to run).
+constexpr int kSpmvMaxKt = 4;
+
+template <int NP1, int NC>
+struct MvShape {
+  static constexpr int NM = NP1 * NP1;
+  static constexpr int LOADS = NC * NP1;
+#ifndef TDB_MV_LOADS_IN_FLIGHT
+#define TDB_MV_LOADS_IN_FLIGHT 8
+#endif
+  static constexpr int U0 = TDB_MV_LOADS_IN_FLIGHT / LOADS;
+  static constexpr int U = U0 >= 8 ? 8 : U0 >= 4 ? 4 : U0 >= 2 ? 2 : 1;
+};
+
+template <int NP1, int NC>
+__device__ __forceinline__ void mv_single_chunk(const MvArgs& a, int t, int n, const int* s_idx,
+                                                const double* s_val, int lane, double (&acc)[NC][NP1]) {
   constexpr int NM = NP1 * NP1;
-  const int lane = threadIdx.x & 31;
-  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  if (w >= (long long)a.nrows * a.G) return;
-  const int j = (int)(w % a.nrows), g = (int)(w / a.nrows);  // j = local row
+  const int4 k4 = __ldg(reinterpret_cast<const int4*>(a.term_kt) + t);
+  const int kts[4] = {k4.x, k4.y, k4.z, k4.w};
+  const int d = __ldg(a.term_d + t);
   const int ncol = a.nc * NP1;
-  double acc[kMaxRowChunks][NP1];
+  int xo[kSpmvMaxKt];
 #pragma unroll
-  for (int c = 0; c < kMaxRowChunks; ++c)
+  for (int k = 0; k < kSpmvMaxKt; ++k) xo[k] = kts[k] > 0 ? (kts[k] - d - a.clo) * NP1 : -1;
+  double part[kSpmvMaxKt][NP1];
 #pragma unroll
-    for (int m = 0; m < NP1; ++m) acc[c][m] = 0.0;
-  const int nchunks = (a.nr + 31) >> 5;
-  for (int t = a.group_begin[g]; t < a.group_begin[g + 1]; ++t) {
-    const FamCsr fc = a.fam[a.term_f[t]];
-    const int s = a.term_s[t], d = a.term_d[t];
-    const unsigned* mask = a.term_mask + (long long)t * a.words;
-    // lane validity per row chunk (bit kt-1)
-    unsigned valid = 0;
+  for (int k = 0; k < kSpmvMaxKt; ++k)
 #pragma unroll
-    for (int c = 0; c < kMaxRowChunks; ++c) {
-      if (c < nchunks) {
-        const int kt = a.rlo + lane + 32 * c;
-        const bool v = (lane + 32 * c < a.nr) && ((mask[(kt - 1) >> 5] >> ((kt - 1) & 31)) & 1u);
-        valid |= (v ? 1u : 0u) << c;
-      }
-    }
-    if (__ballot_sync(0xffffffffu, valid != 0) == 0) continue;
-    const long long row = (long long)s * a.nrows + j;
-    const int64_t e0 = fc.indptr[row], e1 = fc.indptr[row + 1];
-    for (int64_t e = e0; e < e1; ++e) {
-      const int l = fc.indices[e];
-      double v[NM];
+    for (int m = 0; m < NP1; ++m) part[k][m] = 0.0;
+  for (int q = lane; q < n; q += 32) {
+    const double* xl = a.xt + (size_t)((unsigned)s_idx[q] * (unsigned)a.xs);
+    double v[NM];
 #pragma unroll
-      for (int m = 0; m < NM; ++m) v[m] = fc.data[e * NM + m];
-      const double* xl = a.xt + (long long)l * ncol;
+    for (int m = 0; m < NM; ++m) v[m] = s_val[q * NM + m];
 #pragma unroll
-      for (int c = 0; c < kMaxRowChunks; ++c) {
-        if ((valid >> c) & 1u) {
-          const int kt = a.rlo + lane + 32 * c;
-          const double* xv = xl + (kt - d - a.clo) * NP1;
+    for (int k = 0; k < kSpmvMaxKt; ++k) {
+      if (xo[k] >= 0) {
 #pragma unroll
-          for (int m1 = 0; m1 < NP1; ++m1) {
-            const double xm = xv[m1];
+        for (int m1 = 0; m1 < NP1; ++m1) {
+          const double xv = __ldg(xl + xo[k] + m1);
 #pragma unroll
-            for (int m2 = 0; m2 < NP1; ++m2) acc[c][m2] = fma(v[m2 * NP1 + m1], xm, acc[c][m2]);
-          }
+          for (int m2 = 0; m2 < NP1; ++m2) part[k][m2] = fma(v[m2 * NP1 + m1], xv, part[k][m2]);
         }
       }
     }
   }
+#pragma unroll
+  for (int k = 0; k < kSpmvMaxKt; ++k) {
+    if (xo[k] < 0) continue;  // warp-uniform
+    const int r = kts[k] - a.rlo, owner = r & 31, chunk = r >> 5;
+#pragma unroll
+    for (int m2 = 0; m2 < NP1; ++m2) {
+      const double sum = warp_allsum(part[k][m2]);
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (c == chunk && lane == owner) acc[c][m2] += sum;
+    }
+  }
+}
+
+template <int NP1, int NC>
+__device__ __forceinline__ void mv_lag_chunk(const MvArgs& a, int t, int n, const int* s_idx, const double* s_val,
+                                             int lane, double (&acc)[NC][NP1]) {
+  using S = MvShape<NP1, NC>;
+  constexpr int NM = S::NM, U = S::U;
+  const int d = __ldg(a.term_d + t);
+  const unsigned* mask = a.term_mask + (long long)t * a.words;
+  // lane validity per row chunk (bit kt-1).  Invalid lanes point at the zero
+  // pad that ends every xt row, so loads and FMAs need no predicate and every
+  // address is one 32-bit add + one IMAD.WIDE.U32.
+  const unsigned xs = (unsigned)a.xs;
+  unsigned offc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int kt = a.rlo + lane + 32 * c;
+    const bool ok = (lane + 32 * c < a.nr) && ((__ldg(mask + ((kt - 1) >> 5)) >> ((kt - 1) & 31)) & 1u);
+    offc[c] = ok ? (unsigned)((kt - d - a.clo) * NP1) : xs - NP1;
+  }
+  const double* __restrict__ xt = a.xt;
+  // n is padded to a multiple of U by the caller (weight 0, a real column)
+  for (int i = 0; i < n; i += U) {
+    double xr[U][NC][NP1];
+    double v[U][NM];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned xo = (unsigned)s_idx[i + u] * xs;
+#pragma unroll
+      for (int m = 0; m < NM; ++m) v[u][m] = s_val[(i + u) * NM + m];
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int m1 = 0; m1 < NP1; ++m1) xr[u][c][m1] = __ldg(xt + (xo + offc[c] + m1));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int m1 = 0; m1 < NP1; ++m1)
+#pragma unroll
+            for (int m2 = 0; m2 < NP1; ++m2) acc[c][m2] = fma(v[u][m2 * NP1 + m1], xr[u][c][m1], acc[c][m2]);
+  }
+}
+
+template <int NP1, int NC>
+#ifndef TDB_MV_MIN_BLOCKS
+#define TDB_MV_MIN_BLOCKS 16
+#endif
+__global__ void __launch_bounds__(32, TDB_MV_MIN_BLOCKS) k_matvec(MvArgs a) {
+  // one warp per CTA: the warp index is blockIdx.x, so every loop bound below is
+  // provably warp-uniform (plain SHFL / no divergence handling)
+  constexpr int NM = NP1 * NP1;
+  constexpr int CAP = MvStage<NM>::CAP;
+  extern __shared__ __align__(16) unsigned char mv_smem[];
+  double* s_val = reinterpret_cast<double*>(mv_smem);          // [2][CAP*NM]
+  int* s_idx = reinterpret_cast<int*>(s_val + 2 * CAP * NM);   // [2][CAP]
+  const int lane = threadIdx.x;
+  const long long w = blockIdx.x;
+  const int j = (int)(w % a.nrows), g = (int)(w / a.nrows);  // j = local row
+  double acc[NC][NP1];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int m = 0; m < NP1; ++m) acc[c][m] = 0.0;
+  MvCursor cur;
+  cur.t = __ldg(a.group_begin + g);
+  cur.te = __ldg(a.group_begin + g + 1);
+  cur.cur = -1;
+  cur.e = cur.e1 = 0;
+  cur.ne0 = cur.ne1 = 0;
+  if (cur.t < cur.te) mv_row_bounds<NM>(a, cur.t, j, cur.ne0, cur.ne1);
+  MvChunk c0, c1;
+  bool h0 = mv_next_chunk<NM>(a, j, cur, c0);
+  if (h0) mv_stage<NM>(a, c0, s_idx, s_val, lane);
+  cp_async_commit();
+  bool h1 = h0 && mv_next_chunk<NM>(a, j, cur, c1);
+  if (h1) mv_stage<NM>(a, c1, s_idx + CAP, s_val + CAP * NM, lane);
+  cp_async_commit();
+  int buf = 0;
+  while (h0) {
+    cp_async_wait1();
+    __syncwarp();
+    int* bi = s_idx + buf * CAP;
+    double* bv = s_val + buf * CAP * NM;
+    if (__ldg(a.term_kt + 4 * c0.t) > 0) {
+      mv_single_chunk<NP1, NC>(a, c0.t, c0.n, bi, bv, lane, acc);
+    } else {
+      constexpr int U = MvShape<NP1, NC>::U;
+      const int nU = (c0.n + U - 1) / U * U;  // pad: weight 0 on the chunk's first column
+      for (int q = c0.n + lane; q < nU; q += 32) {
+        bi[q] = bi[0];
+#pragma unroll
+        for (int m = 0; m < NM; ++m) bv[q * NM + m] = 0.0;
+      }
+      __syncwarp();
+      mv_lag_chunk<NP1, NC>(a, c0.t, nU, bi, bv, lane, acc);
+    }
+    __syncwarp();
+    c0 = c1;
+    h0 = h1;
+    h1 = h1 && mv_next_chunk<NM>(a, j, cur, c1);
+    if (h1) mv_stage<NM>(a, c1, s_idx + buf * CAP, s_val + buf * CAP * NM, lane);
+    cp_async_commit();
+    buf ^= 1;
+  }
   double* yp = a.ypart + ((long long)g * a.nrows + j) * (a.nr * NP1);
 #pragma unroll
-  for (int c = 0; c < kMaxRowChunks; ++c) {
+  for (int c = 0; c < NC; ++c) {
     const int r = lane + 32 * c;
-    if (c < nchunks && r < a.nr)
+    if (r < a.nr)
 #pragma unroll
       for (int m = 0; m < NP1; ++m) yp[r * NP1 + m] = acc[c][m];
   }
+}
+
+template <int NP1, int NC>
+static void launch_mv_nc(const MvArgs& a, int nchunks, int blocks, cudaStream_t st) {
+  if constexpr (NC < kMaxRowChunks) {
+    if (nchunks > NC) return launch_mv_nc<NP1, NC + 1>(a, nchunks, blocks, st);
+  }
+  constexpr size_t smem = MvStage<NP1 * NP1>::BYTES;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_matvec<NP1, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_matvec<NP1, NC><<<blocks, 32, smem, st>>>(a);
 }
 
 __global__ void k_reduce_out(const double* __restrict__ ypart, double* __restrict__ y, int M, int nrow,
@@ -190,6 +403,8 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   const int nt = d->nterms;
   // work per term, for grouping and for the roofline bookkeeping
   std::vector<long long> tnnz(nt);
+  std::vector<double> tcost(nt);
+  std::vector<int> term_kt(4 * (size_t)nt, 0);
   std::vector<std::vector<int64_t>> famptr(sys->F);
   double bytes = 0.0, flops = 0.0;
   for (int t = 0; t < nt; ++t) {
@@ -199,32 +414,52 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
       set_error("matvec: term references a missing family/position");
       return TDB_E_INVALID;
     }
-    int64_t b[2];
-    cudaMemcpy(b, sys->fam[f].indptr + (long long)s * NR, sizeof(int64_t), cudaMemcpyDeviceToHost);
-    cudaMemcpy(b + 1, sys->fam[f].indptr + (long long)(s + 1) * NR, sizeof(int64_t), cudaMemcpyDeviceToHost);
-    tnnz[t] = b[1] - b[0];
+    std::vector<int64_t>& fp = famptr[f];
+    if (fp.empty()) {  // one D2H copy of each referenced family's row pointers
+      fp.resize((size_t)sys->fam[f].npos * NR + 1);
+      TDB_CUDA_CHECK(cudaMemcpy(fp.data(), sys->fam[f].indptr, fp.size() * sizeof(int64_t),
+                                cudaMemcpyDeviceToHost));
+    }
+    tnnz[t] = fp[(size_t)(s + 1) * NR] - fp[(size_t)s * NR];
     int nlog = 0;
     for (int w = 0; w < d->words; ++w) nlog += __builtin_popcount(d->term_mask[(long long)t * d->words + w]);
     bytes += (double)tnnz[t] * (8.0 * NM + 4.0);
     flops += 2.0 * NM * (double)tnnz[t] * nlog;
+    int* k4 = &term_kt[4 * (size_t)t];
+    if (nlog <= kSpmvMaxKt) {
+      int q = 0;
+      for (int kt = 1; kt <= d->N; ++kt)
+        if ((d->term_mask[(long long)t * d->words + ((kt - 1) >> 5)] >> ((kt - 1) & 31)) & 1u) {
+          if (kt < d->rlo || kt > d->rhi) {
+            delete p;
+            set_error("matvec: term mask has a block row outside the plan's row range");
+            return TDB_E_INVALID;
+          }
+          k4[q++] = kt;
+        }
+      tcost[t] = (double)tnnz[t] * (10.0 + 3.0 * nlog) / 32.0;
+    } else {
+      k4[0] = -1;
+      tcost[t] = (double)tnnz[t] * (3.0 + 3.0 * ((d->rhi - d->rlo + 32) / 32) * NP1);
+    }
   }
   const int nr = d->rhi - d->rlo + 1, nc = d->chi - d->clo + 1;
   bytes += 8.0 * ((double)nr * NR + (double)nc * M) * NP1;
   p->bytes = bytes;
   p->flops = flops;
   // groups: enough warps to fill the chip on small meshes
-  const int want_warps = sys->ctx->num_sms * 32;
+  const int want_warps = sys->ctx->num_sms * 48;
   int G = std::max(1, std::min(nt, (want_warps + NR - 1) / NR));
   G = std::min(G, 64);
   std::vector<int> gb(G + 1, nt);
   {
-    long long total = 0;
-    for (long long v : tnnz) total += v;
-    long long acc = 0;
+    double total = 0;
+    for (double v : tcost) total += v;
+    double acc = 0;
     int g = 0;
     gb[0] = 0;
     for (int t = 0; t < nt && g < G - 1; ++t) {
-      acc += tnnz[t];
+      acc += tcost[t];
       if (acc * G >= total * (g + 1)) gb[++g] = t + 1;
     }
     for (int k = g + 1; k <= G; ++k) gb[k] = nt;
@@ -236,6 +471,9 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   ints.insert(ints.end(), d->term_pos, d->term_pos + nt);
   ints.insert(ints.end(), d->term_d, d->term_d + nt);
   ints.insert(ints.end(), gb.begin(), gb.end());
+  const size_t kt_off = (ints.size() + 3) & ~size_t(3);  // 16-byte aligned int4 rows
+  ints.resize(kt_off, 0);
+  ints.insert(ints.end(), term_kt.begin(), term_kt.end());
   cudaStream_t st = sys->ctx->stream;
 #define ALLOC_COPY(dst, src, n, T)                                                                 \
   do {                                                                                             \
@@ -251,7 +489,8 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   ALLOC_COPY(p->d_fam, fam.data(), sys->F, FamCsr);
   ALLOC_COPY(p->d_ints, ints.data(), ints.size(), int);
   ALLOC_COPY(p->d_mask, d->term_mask, (size_t)nt * d->words, unsigned);
-  ALLOC_COPY(p->d_xt, (const double*)nullptr, (size_t)M * nc * NP1, double);
+  ALLOC_COPY(p->d_xt, (const double*)nullptr, (size_t)M * (nc + 1) * NP1, double);
+  cudaMemsetAsync(p->d_xt, 0, (size_t)M * (nc + 1) * NP1 * sizeof(double), st);  // zero pads
   ALLOC_COPY(p->d_ypart, (const double*)nullptr, (size_t)G * NR * nr * NP1, double);
   if (d->x_map) ALLOC_COPY(p->d_xmap, reinterpret_cast<const long long*>(d->x_map), M, long long);
   p->xstride = d->x_map ? d->x_stride : M;
@@ -273,8 +512,10 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   a.term_s = p->d_ints + nt;
   a.term_d = p->d_ints + 2 * nt;
   a.group_begin = p->d_ints + 3 * nt;
+  a.term_kt = p->d_ints + kt_off;
   a.term_mask = p->d_mask;
   a.xt = p->d_xt;
+  a.xs = (nc + 1) * NP1;
   a.ypart = p->d_ypart;
   *out = p;
   return TDB_OK;
@@ -294,16 +535,17 @@ extern "C" int tdb_matvec(TdbMatvecPlan* p, const double* x, double* y) {
   const int ncols = a.nc * a.NP1, nrows = a.nr * a.NP1;
   {
     dim3 blk(32, 8), grd((a.M + 31) / 32, (ncols + 31) / 32);
-    k_transpose_in<<<grd, blk, 0, st>>>(x, p->d_xt, a.M, ncols, p->d_xmap, p->xstride);
+    k_transpose_in<<<grd, blk, 0, st>>>(x, p->d_xt, a.M, ncols, a.xs, p->d_xmap, p->xstride);
   }
   {
     const long long warps = (long long)a.nrows * a.G;
-    const int blocks = (int)((warps * 32 + 255) / 256);
+    const int blocks = (int)warps;
+    const int nchunks = (a.nr + 31) >> 5;
     switch (a.NP1) {
-      case 1: k_matvec<1><<<blocks, 256, 0, st>>>(a); break;
-      case 2: k_matvec<2><<<blocks, 256, 0, st>>>(a); break;
-      case 3: k_matvec<3><<<blocks, 256, 0, st>>>(a); break;
-      default: k_matvec<4><<<blocks, 256, 0, st>>>(a); break;
+      case 1: launch_mv_nc<1, 1>(a, nchunks, blocks, st); break;
+      case 2: launch_mv_nc<2, 1>(a, nchunks, blocks, st); break;
+      case 3: launch_mv_nc<3, 1>(a, nchunks, blocks, st); break;
+      default: launch_mv_nc<4, 1>(a, nchunks, blocks, st); break;
     }
   }
   {

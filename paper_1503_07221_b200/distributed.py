@@ -107,7 +107,7 @@ class _DistMatvecPlan:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib.LIB is not None:  # LIB is None at interpreter exit
             _lib.LIB.tdb_matvec_plan_destroy(h)
             self.handle = None
 
