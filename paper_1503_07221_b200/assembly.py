@@ -244,6 +244,21 @@ def _mesh_c(mesh: SurfaceMesh, keep: list) -> _lib.TdbMesh:
     return m
 
 
+def _host_empty(shape, dtype):
+    """Host array for device->host copies: page-locked memory from torch's caching
+    host allocator (DMA at full PCIe/C2C speed, no first-touch page faults; blocks
+    are recycled once the caller drops the array).  numpy fallback without CUDA."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            t = torch.empty(int(np.prod(shape)), dtype=getattr(torch, np.dtype(dtype).name), pin_memory=True)
+            return t.numpy().reshape(shape)
+    except (ImportError, RuntimeError, AttributeError):
+        pass
+    return np.empty(shape, dtype=dtype)
+
+
 class DeviceAssembly:
     """Owner of a device-resident assembled system (TdbSystem handle).
 
@@ -308,9 +323,9 @@ class DeviceAssembly:
         nnz = _lib.C.c_int64()
         _lib.check(_lib.LIB.tdb_system_family_nnz(self.handle, f, _lib.C.byref(nnz)), "family_nnz")
         npos = len(self.plan.families[f].positions)
-        indptr = np.empty(npos * self.nrows + 1, dtype=np.int64)
-        indices = np.empty(max(1, nnz.value), dtype=np.int32)
-        data = np.empty((max(1, nnz.value), (self.p + 1) ** 2))
+        indptr = _host_empty((npos * self.nrows + 1,), np.int64)
+        indices = _host_empty((max(1, nnz.value),), np.int32)
+        data = _host_empty((max(1, nnz.value), (self.p + 1) ** 2), np.float64)
         _lib.check(_lib.LIB.tdb_system_copy_family(
             self.handle, f, _lib.ptr(indptr, _lib.C.c_int64), _lib.ptr(indices, _lib.C.c_int32),
             _lib.ptr(data)), "copy_family")

@@ -287,8 +287,44 @@ def touching_pairs(mesh: SurfaceMesh):
 
     Returns dict case -> (ex, ey, lx, ly) int arrays, rows sorted by (ex, ey):
     lx/ly are the chart permutations that bring the shared vertices first in
-    ascending global order (assembly.py:130-152 semantics).
+    ascending global order (assembly.py:130-152 semantics).  Vectorised over
+    the vertex stars (no per-pair Python work).
     """
+    tri = np.asarray(mesh.triangles, dtype=np.int64)
+    off, ids = mesh.star_csr
+    E = mesh.num_triangles
+    # candidates: (e, f) for every f in the star of each vertex of e
+    v = tri.ravel()
+    cnt = off[v + 1] - off[v]
+    ex = np.repeat(np.repeat(np.arange(E, dtype=np.int64), 3), cnt)
+    starts = np.repeat(off[v], cnt)
+    within = np.arange(len(ex), dtype=np.int64) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    ey = np.asarray(ids, dtype=np.int64)[starts + within]
+    key = np.unique(ex * E + ey)
+    ex, ey = key // E, key % E
+    tx, ty = tri[ex], tri[ey]
+    eq = tx[:, :, None] == ty[:, None, :]
+    nshared = eq.sum(axis=(1, 2))
+    big = np.int64(np.iinfo(np.int64).max // 4)
+
+    def lead(t, shared):
+        # shared vertices first in ascending global id, then the rest in local order
+        k = np.where(shared, t, big + np.arange(3, dtype=np.int64)[None, :])
+        return np.argsort(k, axis=1, kind="stable").astype(np.int64)
+
+    lx = lead(tx, eq.any(axis=2))
+    ly = lead(ty, eq.any(axis=1))
+    coinc = ex == ey
+    lx[coinc] = (0, 1, 2)
+    ly[coinc] = (0, 1, 2)
+    res = {}
+    for case, sel in (("coincident", coinc), ("edge", ~coinc & (nshared == 2)), ("vertex", ~coinc & (nshared == 1))):
+        res[case] = (ex[sel], ey[sel], lx[sel].reshape(-1, 3), ly[sel].reshape(-1, 3))
+    return res
+
+
+def _touching_pairs_loop(mesh: SurfaceMesh):
+    """Per-pair reference restatement of touching_pairs (kept for tests)."""
     tri = mesh.triangles
     off, ids = mesh.star_csr
     E = mesh.num_triangles

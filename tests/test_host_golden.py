@@ -100,3 +100,13 @@ def test_rhs_matches_reference(two_tri):
 
     b2 = assemble_rhs(two_tri, TimeGrid(T=3.0, N=5, p=1), gs)
     assert np.max(np.abs(b2 - g["two_tri_smooth"])) <= 1e-14 * np.max(np.abs(g["two_tri_smooth"]))
+
+
+def test_touching_pairs_vectorised_matches_loop():
+    from paper_1503_07221_b200.mesh import _touching_pairs_loop, icosphere, jittered_cube, touching_pairs
+
+    for m in (icosphere(2), jittered_cube(4, 0.05, 1)):
+        a, b = touching_pairs(m), _touching_pairs_loop(m)
+        for case in ("coincident", "edge", "vertex"):
+            for x, y in zip(a[case], b[case]):
+                assert np.array_equal(x, y)
