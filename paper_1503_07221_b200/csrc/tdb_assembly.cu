@@ -303,13 +303,24 @@ __global__ void k_fill_items(long long E2, const long long* __restrict__ item_ba
 // ---------------------------------------------------------------------------
 // 3. quadrature kernel
 // ---------------------------------------------------------------------------
+// Per-launch family descriptor of the quadrature kernel, passed by value in the
+// kernel parameters (constant bank): warp-uniform fields cost no shared-memory
+// wavefronts and no registers across the round loop.
+struct QFam {
+  int nsub, fold, coeff_off, coef_global, deg, khead, tail_off;
+  unsigned sp_neg, sn_neg;  // bit t: sign of table t is -1 for a >= 0 / a < 0 (fold)
+  double lo, w, inv_w, amin, amax;
+  const double* delta;
+  const double* coeffs;
+};
+
 struct QuadArgs {
   int E;
   long long npair;            // Et * E
   const int* tt;              // test triangle of pair-row k
   int fam_count;
   int fam_ids[kMaxFamilies];  // global family index of each launch family (frange slices)
-  const FamDev* fams;         // this launch's descriptors (coeff_off into `blob`)
+  QFam fam[kMaxFamilies];     // this launch's descriptors (coeff_off into `blob`)
   const double* blob;      // coefficients of the launch's families, concatenated
   int blob_doubles;
   int coef_in_smem;
@@ -329,6 +340,7 @@ struct QuadArgs {
 
 constexpr int kQuadWarps = 12;
 constexpr int kNK = kChunk / 32;
+constexpr int kGroupChunks = 16;  // chunks of one (singular) pair handled by one work item
 constexpr int kBuckets = 256;
 // per-warp scratch: r, c, x1, x2, y1, y2 (FP64, r-sorted order) + bucket cursors
 constexpr int kWarpScratchBytes = 6 * kChunk * 8 + (kBuckets + 1) * 4 + 12;  // 16-byte multiple
@@ -477,7 +489,7 @@ struct SortedPts {
 
 // In-support index range [i0, i1) of the r-sorted points for table offset delta
 // (r in [amin - delta, amax - delta], bucket bounds are monotone in r).
-__device__ __forceinline__ void position_range(const FamDev& fd, const SortedPts& pt, double delta, int& i0,
+__device__ __forceinline__ void position_range(const QFam& fd, const SortedPts& pt, double delta, int& i0,
                                                int& i1) {
   const double rlo = fd.amin - delta, rhi = fd.amax - delta;
   i0 = 0;
@@ -496,7 +508,7 @@ __device__ __forceinline__ void position_range(const FamDev& fd, const SortedPts
 // Only this loop is specialised per (subintervals, degree split); the range
 // search and the reduction live once in the caller (instruction-cache footprint).
 template <int P, bool GLOBAL, int D, int K>
-__device__ __forceinline__ void eval_rounds(const FamDev& fd, const double* __restrict__ cf,
+__device__ __forceinline__ void eval_rounds(const QFam& fd, const double* __restrict__ cf,
                                             const SortedPts& pt, int i0, int i1, double delta, int lane,
                                             double (&acc)[10 * (P + 1) * (P + 1)], unsigned& n_act) {
   constexpr int NM = (P + 1) * (P + 1);
@@ -524,9 +536,10 @@ __device__ __forceinline__ void eval_rounds(const FamDev& fd, const double* __re
     for (int m = 0; m < NM; ++m) {
       double v0, v1;
       eval_pair<NT, GLOBAL, D, K>(cf, fd.tail_off, idx, m, X, v0, v1);
-      if (fd.fold) {
-        v0 *= neg ? fd.sn[2 * m] : fd.sp[2 * m];
-        v1 *= neg ? fd.sn[2 * m + 1] : fd.sp[2 * m + 1];
+      {
+        const unsigned sg = neg ? fd.sn_neg : fd.sp_neg;
+        if ((sg >> (2 * m)) & 1u) v0 = -v0;
+        if ((sg >> (2 * m + 1)) & 1u) v1 = -v1;
       }
       const double cp = c * v0;
       const double u0 = cp * shy0, u1 = cp * shy1, u2 = cp * y2;
@@ -550,9 +563,8 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
   constexpr int NM = (P + 1) * (P + 1);
   constexpr int NACC = 10 * NM;
   extern __shared__ __align__(16) double smem[];
-  // layout: [fam descriptors][coef blob][per warp scratch]
-  FamDev* sfam = reinterpret_cast<FamDev*>(smem);
-  double* sblob = smem + (sizeof(FamDev) * a.fam_count + 15) / 16 * 2;
+  // layout: [coef blob][per warp scratch]
+  double* sblob = smem;
   char* swarp = reinterpret_cast<char*>(sblob + (SMEM_COEF ? (a.blob_doubles + 1) / 2 * 2 : 0));
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* sr = reinterpret_cast<double*>(swarp + (size_t)wid * kWarpScratchBytes);
@@ -563,10 +575,7 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
   double* sy2 = sy1 + kChunk;
   unsigned* cur = reinterpret_cast<unsigned*>(sy2 + kChunk);  // kBuckets + 1
 
-  {  // stage family descriptors and coefficients
-    const int nwords = (int)((sizeof(FamDev) * a.fam_count + 7) / 8);
-    const double* src = reinterpret_cast<const double*>(a.fams);
-    for (int i = threadIdx.x; i < nwords; i += blockDim.x) smem[i] = src[i];
+  {  // stage the coefficients
     if (SMEM_COEF)
       for (int i = threadIdx.x; i < a.blob_doubles; i += blockDim.x) sblob[i] = a.blob[i];
     __syncthreads();
@@ -582,7 +591,7 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
     it = __shfl_sync(0xffffffffu, it, 0);
     if (it >= a.nitems) break;
     const int2 item = a.items[it];
-    const int Pp = item.x, isub = item.y;
+    const int Pp = item.x, grp = item.y;
     // any unit of this item in the launch's families?
     bool any = false;
     for (int fi = 0; fi < a.fam_count; ++fi)
@@ -592,14 +601,21 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
     int lx[3], ly[3];
     const int cs = pair_topology(a.tri, ex, ey, lx, ly);
     const RuleDev& R = a.rules[cs];
-    const long long q0 = (long long)isub * kChunk;
-    const int nq = (int)min((long long)kChunk, R.nq - q0);
     const V3 X0 = corner(a.corners, ex, lx[0]), X1 = corner(a.corners, ex, lx[1]),
              X2 = corner(a.corners, ex, lx[2]);
     const V3 Y0 = corner(a.corners, ey, ly[0]), Y1 = corner(a.corners, ey, ly[1]),
              Y2 = corner(a.corners, ey, ly[2]);
     const V3 e1 = sub(X1, X0), e2 = sub(X2, X1), f1 = sub(Y1, Y0), f2 = sub(Y2, Y1);
     const double scale = kInv4Pi * a.a2[ex] * a.a2[ey];
+    const int nunits = a.units[Pp];
+    // this item's chunks [c_begin, c_end); their partials are summed into the
+    // group's slots in chunk order (the first chunk stores, later ones add)
+    const int c_begin = grp * kGroupChunks, c_end = min(R.nitems, c_begin + kGroupChunks);
+    const long long slot0 = a.pair_base[Pp] + (long long)grp * nunits;
+    for (int ci = c_begin; ci < c_end; ++ci) {
+    const bool first = ci == c_begin;
+    const long long q0 = (long long)ci * kChunk;
+    const int nq = (int)min((long long)kChunk, R.nq - q0);
     // geometry of this lane's points (q = lane + 32 k)
     double rk[kNK], ck[kNK], px1[kNK], px2[kNK], py1[kNK], py2[kNK];
     double rmin = 1e300, rmax = -1e300;
@@ -682,8 +698,6 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
       __syncwarp();
     }
     // now cur[b] = end of bucket b in the sorted arrays
-    const int nunits = a.units[Pp];
-    const long long slot0 = a.pair_base[Pp] + (long long)isub * nunits;
 
     SortedPts pt;
     pt.r = sr;
@@ -700,7 +714,7 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
       const FRange fr = a.frange[(long long)a.fam_ids[fi] * E2 + Pp];
       const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
       if (cnt == 0) continue;
-      const FamDev& fd = sfam[fi];
+      const QFam& fd = a.fam[fi];
       // keep the shared-memory pointer provably shared (LDS, not generic LD)
       const double* cf_s = coef_base + fd.coeff_off;
       const double* cf_g = fd.coeffs;
@@ -709,6 +723,11 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
         const double delta = fd.delta[s_lo + si];
         int i0, i1;
         position_range(fd, pt, delta, i0, i1);
+        if (i0 >= i1) {  // no rule point of this chunk in the position's support (warp-uniform)
+          if (first)
+            for (int k = lane; k < NACC; k += 32) dst[k] = 0.0;
+          continue;
+        }
         double acc[NACC];
 #pragma unroll
         for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
@@ -737,9 +756,11 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
         warp_reduce_scatter<NACC>(acc, lane, outv, base, valid);
 #pragma unroll
         for (int k = 0; k < RS<NACC>::H5; ++k)
-          if (k < valid) dst[base + k] = outv[k];
+          if (k < valid) dst[base + k] = first ? outv[k] : dst[base + k] + outv[k];
       }
     }
+    __syncwarp();
+    }  // chunks of the group
   }
   if (lane == 0) atomicAdd(a.n_in, my_in);
 }
@@ -1148,6 +1169,7 @@ struct AsmWorkspace {
   size_t cub_bytes = 0;
   struct Launch {
     std::vector<int> fams;
+    std::vector<QFam> qfam;
     bool in_smem = false;
     size_t bytes = 0, smem = 0;
     FamDev* d_fam = nullptr;
@@ -1324,7 +1346,7 @@ int tdb_system_run_impl(TdbSystem* sys) {
     qa.tt = ws->tt;
     qa.fam_count = (int)L.fams.size();
     for (int i = 0; i < qa.fam_count; ++i) qa.fam_ids[i] = L.fams[i];
-    qa.fams = L.d_fam;
+    for (int i = 0; i < qa.fam_count; ++i) qa.fam[i] = L.qfam[i];
     qa.blob = L.d_blob;
     qa.blob_doubles = L.in_smem ? L.blob_doubles : 0;
     qa.coef_in_smem = L.in_smem;
@@ -1606,7 +1628,7 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
     RuleDev& rd = ws->rules[c];
     rd.nq = r.nq;
     rd.nitems = (int)((r.nq + kChunk - 1) / kChunk);
-    ws->nitems_case[c] = std::max(1, rd.nitems);
+    ws->nitems_case[c] = std::max(1, (rd.nitems + kGroupChunks - 1) / kGroupChunks);
     std::vector<double> x1(r.nq), x2(r.nq), y1(r.nq), y2(r.nq);
     for (long long q = 0; q < r.nq; ++q) {
       x1[q] = r.xhat[2 * q];
@@ -1669,12 +1691,33 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
           lb.insert(lb.end(), blob_all.begin() + ws->fam_blob_off[f],
                     blob_all.begin() + ws->fam_blob_off[f] + ws->fam_blob_len[f]);
         fdv.push_back(fd);
+        QFam q{};
+        q.nsub = fd.nsub;
+        q.fold = fd.fold;
+        q.coeff_off = fd.coeff_off;
+        q.coef_global = fd.coef_global;
+        q.deg = fd.deg;
+        q.khead = fd.khead;
+        q.tail_off = fd.tail_off;
+        q.sp_neg = q.sn_neg = 0u;
+        for (int t = 0; t < nt; ++t) {
+          if (fd.fold && fd.sp[t] < 0.0) q.sp_neg |= 1u << t;
+          if (fd.fold && fd.sn[t] < 0.0) q.sn_neg |= 1u << t;
+        }
+        q.lo = fd.lo;
+        q.w = fd.w;
+        q.inv_w = fd.inv_w;
+        q.amin = fd.amin;
+        q.amax = fd.amax;
+        q.delta = fd.delta;
+        q.coeffs = fd.coeffs;
+        L.qfam.push_back(q);
       }
       L.blob_doubles = (int)lb.size();
       L.bytes = lb.size() * 8;
       if ((rc = dupload(&L.d_blob, lb.data(), lb.size(), st))) return rc;
       if ((rc = dupload(&L.d_fam, fdv.data(), fdv.size(), st))) return rc;
-      L.smem = ((sizeof(FamDev) * L.fams.size() + 15) / 16) * 16 + (L.bytes + 15) / 16 * 16 + warp_bytes;
+      L.smem = (L.bytes + 15) / 16 * 16 + warp_bytes;
       ws->launches.push_back(std::move(L));
     }
   }
