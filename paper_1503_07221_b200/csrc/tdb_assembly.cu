@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "tdb_common.cuh"
@@ -419,6 +420,11 @@ __device__ __forceinline__ XPow xpowers(double x) {
 // (D, K) are chosen per family on the host so that the result stays within
 // 3e-15 of the table max of the reference's full Clenshaw evaluation.
 // Coefficient layout: head [sub][k][t] double, tail [sub][k-K][t] float.
+// float2 per FP32-tail row of one subinterval: (D - K + 1) coefficients x NT / 2
+// table pairs, rounded up to odd so rows of consecutive subintervals fall in
+// distinct shared-memory bank pairs
+__host__ __device__ constexpr int tail_row_f2(int D, int K, int NT) { return ((D - K + 1) * NT / 2) | 1; }
+
 template <int NT, bool GLOBAL, int D, int K>
 __device__ __forceinline__ void eval_pair(const double* __restrict__ cf, int tail_off, int idx, int m,
                                           const XPow& X, double& v0, double& v1) {
@@ -457,8 +463,9 @@ __device__ __forceinline__ void eval_pair(const double* __restrict__ cf, int tai
     v0 = fma(ra1, X.x4, ra0);
     v1 = fma(rb1, X.x4, rb0);
     if constexpr (D >= K) {
-      const float2* tp = reinterpret_cast<const float2*>(
-                             reinterpret_cast<const float*>(cf + tail_off) + (idx * (D - K + 1)) * NT + 2 * m);
+      // tail rows are padded to an odd number of float2 (bank-conflict free)
+      constexpr int TROW = tail_row_f2(D, K, NT);
+      const float2* tp = reinterpret_cast<const float2*>(cf + tail_off) + idx * TROW + m;
       float2 b[D - K + 1];
 #pragma unroll
       for (int k = 0; k <= D - K; ++k) b[k] = GLOBAL ? __ldg(tp + k * stride) : tp[k * stride];
@@ -1469,17 +1476,65 @@ static double emulate_split(const long double* a, int D, int K, double x) {
   return v;
 }
 
-// Cheapest (degree D, FP64 head size K) keeping every table of the pack within
-// 3e-15 of its max of the reference's full degree-16 Clenshaw evaluation.
-static void select_split(const TdbPsiPack& pk, int nt, int nsub, int* D_out, int* K_out) {
-  static const int cands[4][2] = {{12, 7}, {14, 7}, {16, 7}, {16, 17}};
-  if (pk.deg != kDeg) {
-    *D_out = 16;
-    *K_out = 17;
-    return;
+// Exact re-expansion of one subinterval polynomial sum_k a_k x^k on R equal
+// sub-subintervals: piece i has x = y / R + (2i + 1) / R - 1, y in [-1, 1]
+// (Taylor shift in 80-bit).  Refining by a power of two keeps the device's
+// subinterval index consistent with the reference's: (a - lo) * (R / w) is
+// exactly R times (a - lo) / w, so floor() of it lies in piece i of the
+// reference's subinterval floor((a - lo) / w).
+static void refine_piece(const long double* a, int R, int i, long double* b) {
+  const long double h = 1.0L / R, c0 = (long double)(2 * i + 1) / R - 1.0L;
+  long double out[kDeg + 1] = {};
+  for (int k = kDeg; k >= 0; --k) {
+    long double nw[kDeg + 1] = {};
+    for (int j = 0; j <= kDeg; ++j) {
+      nw[j] += out[j] * c0;
+      if (j + 1 <= kDeg) nw[j + 1] += out[j] * h;
+    }
+    nw[0] += a[k];
+    for (int j = 0; j <= kDeg; ++j) out[j] = nw[j];
   }
+  for (int j = 0; j <= kDeg; ++j) b[j] = out[j];
+}
+
+// Monomial coefficients of every (table, refined subinterval) of a family:
+// mono[((t * nsub * R) + s') * (kDeg + 1) + k].
+static void family_monomials(const TdbPsiPack& pk, int nt, int nsub, int R, std::vector<long double>& mono) {
+  mono.assign((size_t)nt * nsub * R * (kDeg + 1), 0.0L);
+  for (int t = 0; t < nt; ++t)
+    for (int k = 0; k < nsub; ++k) {
+      const double* cc = pk.coeffs + ((size_t)t * pk.max_nsub + k) * (kDeg + 1);
+      long double a[kDeg + 1];
+      cheb_to_monomial(cc, kDeg, a);
+      for (int i = 0; i < R; ++i) {
+        long double* b = mono.data() + (((size_t)t * nsub * R) + (size_t)k * R + i) * (kDeg + 1);
+        if (R == 1)
+          for (int j = 0; j <= kDeg; ++j) b[j] = a[j];
+        else
+          refine_piece(a, R, i, b);
+      }
+    }
+}
+
+// Cheapest (refinement R, degree D, FP64 head size K) keeping every table of the
+// pack within 3e-15 of its max of the reference's full degree-16 Clenshaw
+// evaluation (checked on 65 points per refined subinterval).  Candidates in
+// cost order: FP64 head of 7 + FP32 tail on the reference's subintervals, then
+// on 2x / 4x refined subintervals (fewer significant monomials: the shift
+// scales coefficient k by R^-k), then the full FP64 degree-16 head.
+static void select_split(const TdbPsiPack& pk, int nt, int nsub, int* R_out, int* D_out, int* K_out,
+                         std::vector<long double>& mono_out) {
+  static const int cands[][3] = {{1, 12, 7}, {1, 14, 7}, {1, 16, 7}, {2, 12, 7}, {4, 12, 7},
+                                 {2, 14, 7}, {4, 14, 7}, {2, 16, 7}, {4, 16, 7}, {1, 16, 17}};
+  std::vector<long double> mono;
+  int cached_R = 0;
   for (const auto& cd : cands) {
-    const int D = cd[0], K = cd[1];
+    const int R = cd[0], D = cd[1], K = cd[2];
+    if (pk.deg != kDeg && !(R == 1 && D == 16 && K == 17)) continue;
+    if (R != cached_R) {
+      family_monomials(pk, nt, nsub, R, mono);
+      cached_R = R;
+    }
     bool ok = true;
     for (int t = 0; t < nt && ok; ++t) {
       double tmax = 0.0;
@@ -1488,24 +1543,30 @@ static void select_split(const TdbPsiPack& pk, int nt, int nsub, int* D_out, int
           tmax = std::max(tmax, std::fabs(pk.coeffs[((size_t)t * pk.max_nsub + k) * (kDeg + 1) + c]));
       for (int k = 0; k < nsub && ok; ++k) {
         const double* cc = pk.coeffs + ((size_t)t * pk.max_nsub + k) * (kDeg + 1);
-        long double mono[kDeg + 1];
-        cheb_to_monomial(cc, D, mono);
-        for (int sidx = 0; sidx <= 64 && ok; ++sidx) {
-          const double x = -1.0 + 2.0 * sidx / 64.0;
-          const long double ref = clenshaw_ld(cc, x);
-          const double err = std::fabs((double)((long double)emulate_split(mono, D, K, x) - ref));
-          if (err > 3e-15 * tmax) ok = false;
+        for (int i = 0; i < R && ok; ++i) {
+          const long double* b = mono.data() + (((size_t)t * nsub * R) + (size_t)k * R + i) * (kDeg + 1);
+          for (int sidx = 0; sidx <= 64 && ok; ++sidx) {
+            const double y = -1.0 + 2.0 * sidx / 64.0;
+            const long double x = (long double)y / R + (long double)(2 * i + 1) / R - 1.0L;
+            const long double ref = clenshaw_ld(cc, x);
+            const double err = std::fabs((double)((long double)emulate_split(b, D, K, y) - ref));
+            if (err > 3e-15 * tmax) ok = false;
+          }
         }
       }
     }
     if (ok) {
+      *R_out = R;
       *D_out = D;
       *K_out = K;
+      mono_out.swap(mono);
       return;
     }
   }
+  *R_out = 1;
   *D_out = 16;
   *K_out = 17;
+  family_monomials(pk, nt, nsub, 1, mono_out);
 }
 
 int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDesc* desc,
@@ -1591,12 +1652,21 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
     // small high-order monomials go to an FP32 tail (k >= K) - chosen so every
     // table stays within 3e-15 of its max of the reference's full Clenshaw value
     // (select_split, checked on 65 points per subinterval).
-    int D = 16, K = 17;
-    select_split(pk, nt, fd.nsub, &D, &K);
+    int R = 1, D = 16, K = 17;
+    std::vector<long double> mono_all;
+    select_split(pk, nt, fd.nsub, &R, &D, &K, mono_all);
+    const int nsub_ref = fd.nsub;
+    fd.nsub = nsub_ref * R;  // refined subintervals (R a power of two: exact w / R)
+    fd.w = pk.width[0] / R;
+    fd.inv_w = R / pk.width[0];
     fd.deg = D;
     fd.khead = K;
+    if (std::getenv("TDB_VERBOSE"))
+      std::fprintf(stderr, "tdb: family %d npos %d nsub %d -> refine %d, degree %d, fp64 head %d\n", f,
+                   hf.npos, nsub_ref, R, D, K);
     const int head_len = K * fd.nsub * nt;
-    const int tail_floats = (K <= D) ? (D - K + 1) * fd.nsub * nt : 0;
+    const int trow = (K <= D) ? tail_row_f2(D, K, nt) : 0;  // float2 per subinterval row
+    const int tail_floats = 2 * trow * fd.nsub;
     const int tail_len = ((tail_floats + 1) / 2 + 1) / 2 * 2;  // doubles, even (16-byte aligned)
     const int len = head_len + tail_len;
     fd.tail_off = head_len;
@@ -1607,11 +1677,9 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
     float* dstt = reinterpret_cast<float*>(dstb + head_len);
     for (int t = 0; t < nt; ++t)
       for (int k = 0; k < fd.nsub; ++k) {
-        const double* cc = pk.coeffs + ((size_t)t * pk.max_nsub + k) * (kDeg + 1);
-        long double mono[kDeg + 1];
-        cheb_to_monomial(cc, D, mono);
+        const long double* mono = mono_all.data() + ((size_t)t * fd.nsub + k) * (kDeg + 1);
         for (int c = 0; c < K && c <= kDeg; ++c) dstb[((size_t)k * K + c) * nt + t] = (double)mono[c];
-        for (int c = K; c <= D; ++c) dstt[((size_t)k * (D - K + 1) + (c - K)) * nt + t] = (float)mono[c];
+        for (int c = K; c <= D; ++c) dstt[(size_t)k * 2 * trow + (size_t)(c - K) * nt + t] = (float)mono[c];
       }
     fd.delta = fs.delta;
     fd.slo = fs.slo;
