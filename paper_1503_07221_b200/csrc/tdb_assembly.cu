@@ -434,7 +434,13 @@ __device__ __forceinline__ void eval_pair(const double* __restrict__ cf, int tai
   constexpr int stride = NT / 2;  // in double2
   double2 a[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) a[k] = GLOBAL ? __ldg(p + k * stride) : p[k * stride];
+  for (int k = 0; k < K; ++k) {
+#ifdef TDB_ABL_NOCOEF
+    a[k] = make_double2(idx * 1e-3 + k, idx * 2e-3 - k);
+#else
+    a[k] = GLOBAL ? __ldg(p + k * stride) : p[k * stride];
+#endif
+  }
   if constexpr (K == 17) {
     double qa[8], qb[8];
 #pragma unroll
@@ -468,7 +474,13 @@ __device__ __forceinline__ void eval_pair(const double* __restrict__ cf, int tai
       const float2* tp = reinterpret_cast<const float2*>(cf + tail_off) + idx * TROW + m;
       float2 b[D - K + 1];
 #pragma unroll
-      for (int k = 0; k <= D - K; ++k) b[k] = GLOBAL ? __ldg(tp + k * stride) : tp[k * stride];
+      for (int k = 0; k <= D - K; ++k) {
+#ifdef TDB_ABL_NOCOEF
+        b[k] = make_float2(idx * 1e-3f + k, idx * 2e-3f - k);
+#else
+        b[k] = GLOBAL ? __ldg(tp + k * stride) : tp[k * stride];
+#endif
+      }
       const float xf = (float)X.x;
       float ta = b[D - K].x, tb = b[D - K].y;
 #pragma unroll
@@ -520,47 +532,79 @@ __device__ __forceinline__ void eval_rounds(const QFam& fd, const double* __rest
                                             double (&acc)[10 * (P + 1) * (P + 1)], unsigned& n_act) {
   constexpr int NM = (P + 1) * (P + 1);
   constexpr int NT = 2 * NM;
-  const unsigned FULL = 0xffffffffu;
+#ifndef TDB_NS
+#define TDB_NS 1
+#endif
+  constexpr int NS = TDB_NS;  // independent round streams per iteration (ILP)
   const int nround = (i1 - i0 + 31) >> 5;
-  for (int rr = 0; rr < nround; ++rr) {
-    const int i = i0 + lane + 32 * rr;
-    const bool in = i < i1;
-    const double r = in ? pt.r[i] : 1e300;
-    const double av = r + delta;
-    const bool act = in && av >= fd.amin && av <= fd.amax;
-    n_act += __popc(__ballot_sync(FULL, act));
-    if (!act) continue;
-    const double c = pt.c[i];
-    const double x1 = pt.x1[i], x2 = pt.x2[i], y1 = pt.y1[i], y2 = pt.y2[i];
-    const double aa = fd.fold ? fabs(av) : av;
-    double x;
-    const int idx = cheb_locate(aa, fd.lo, fd.w, fd.inv_w, fd.nsub, x);
-    const bool neg = av < 0.0;
-    const double shx0 = 1.0 - x1, shx1 = x1 - x2;
-    const double shy0 = 1.0 - y1, shy1 = y1 - y2;
-    const XPow X = xpowers(x);
+  const int h = (nround + NS - 1) / NS;  // stream u walks rounds [u h, (u + 1) h)
+  const int ilast = i1 - 1;
+  const double amin = fd.amin, amax = fd.amax, lo = fd.lo, w = fd.w, inv_w = fd.inv_w;
+  const int nsub = fd.nsub, fold = fd.fold, tail_off = fd.tail_off;
+  const unsigned sp_neg = fd.sp_neg, sn_neg = fd.sn_neg;
+  for (int rr = 0; rr < h; ++rr) {
+    // Branch-free: lanes past the range or outside the support evaluate a valid
+    // (clamped) point with weight 0 - no divergence barriers in the body.
+    double r[NS], c[NS], x1[NS], x2[NS], y1[NS], y2[NS];
+    bool in[NS];
+#pragma unroll
+    for (int u = 0; u < NS; ++u) {
+      const int i = i0 + lane + 32 * (rr + u * h);
+      in[u] = i < i1;
+      const int j = min(i, ilast);
+#ifdef TDB_ABL_NOPT
+      r[u] = pt.rmin + j * 1e-4; c[u] = 1.0 + j; x1[u] = 0.5; x2[u] = 0.25 + j * 1e-3; y1[u] = 0.3; y2[u] = 0.1;
+#else
+      r[u] = pt.r[j];
+      c[u] = pt.c[j];
+      x1[u] = pt.x1[j];
+      x2[u] = pt.x2[j];
+      y1[u] = pt.y1[j];
+      y2[u] = pt.y2[j];
+#endif
+    }
+    double cw[NS], xl[NS];
+    int idx[NS];
+    bool neg[NS];
+#pragma unroll
+    for (int u = 0; u < NS; ++u) {
+      const double av = r[u] + delta;
+      const bool act = in[u] && av >= amin && av <= amax;
+      n_act += act ? 1u : 0u;
+      cw[u] = act ? c[u] : 0.0;
+      const double aa = fold ? fabs(av) : av;
+      idx[u] = max(0, cheb_locate(aa, lo, w, inv_w, nsub, xl[u]));
+      neg[u] = av < 0.0;
+    }
 #pragma unroll
     for (int m = 0; m < NM; ++m) {
-      double v0, v1;
-      eval_pair<NT, GLOBAL, D, K>(cf, fd.tail_off, idx, m, X, v0, v1);
-      {
-        const unsigned sg = neg ? fd.sn_neg : fd.sp_neg;
-        if ((sg >> (2 * m)) & 1u) v0 = -v0;
-        if ((sg >> (2 * m + 1)) & 1u) v1 = -v1;
+      double v0[NS], v1[NS];
+#pragma unroll
+      for (int u = 0; u < NS; ++u) {
+        const XPow X = xpowers(xl[u]);
+        eval_pair<NT, GLOBAL, D, K>(cf, tail_off, idx[u], m, X, v0[u], v1[u]);
+        const unsigned sg = neg[u] ? sn_neg : sp_neg;
+        if ((sg >> (2 * m)) & 1u) v0[u] = -v0[u];
+        if ((sg >> (2 * m + 1)) & 1u) v1[u] = -v1[u];
       }
-      const double cp = c * v0;
-      const double u0 = cp * shy0, u1 = cp * shy1, u2 = cp * y2;
       double* S = acc + 10 * m;
-      S[0] = fma(u0, shx0, S[0]);
-      S[1] = fma(u0, shx1, S[1]);
-      S[2] = fma(u0, x2, S[2]);
-      S[3] = fma(u1, shx0, S[3]);
-      S[4] = fma(u1, shx1, S[4]);
-      S[5] = fma(u1, x2, S[5]);
-      S[6] = fma(u2, shx0, S[6]);
-      S[7] = fma(u2, shx1, S[7]);
-      S[8] = fma(u2, x2, S[8]);
-      S[9] = fma(c, v1, S[9]);
+#pragma unroll
+      for (int u = 0; u < NS; ++u) {
+        const double shx0 = 1.0 - x1[u], shx1 = x1[u] - x2[u];
+        const double shy0 = 1.0 - y1[u], shy1 = y1[u] - y2[u];
+        const double cp = cw[u] * v0[u];
+        const double u0 = cp * shy0, u1 = cp * shy1, u2 = cp * y2[u];
+        S[0] = fma(u0, shx0, S[0]);
+        S[1] = fma(u0, shx1, S[1]);
+        S[2] = fma(u0, x2[u], S[2]);
+        S[3] = fma(u1, shx0, S[3]);
+        S[4] = fma(u1, shx1, S[4]);
+        S[5] = fma(u1, x2[u], S[5]);
+        S[6] = fma(u2, shx0, S[6]);
+        S[7] = fma(u2, shx1, S[7]);
+        S[8] = fma(u2, x2[u], S[8]);
+        S[9] = fma(cw[u], v1[u], S[9]);
+      }
     }
   }
 }
@@ -760,7 +804,11 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
         my_in += n_act;
         double outv[RS<NACC>::H5];
         int base, valid;
+#ifdef TDB_ABL_NORED
+        outv[0] = acc[lane % NACC]; base = lane; valid = lane < NACC ? 1 : 0;
+#else
         warp_reduce_scatter<NACC>(acc, lane, outv, base, valid);
+#endif
 #pragma unroll
         for (int k = 0; k < RS<NACC>::H5; ++k)
           if (k < valid) dst[base + k] = first ? outv[k] : dst[base + k] + outv[k];
@@ -769,6 +817,8 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
     __syncwarp();
     }  // chunks of the group
   }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) my_in += __shfl_xor_sync(0xffffffffu, my_in, o);
   if (lane == 0) atomicAdd(a.n_in, my_in);
 }
 
