@@ -309,6 +309,7 @@ __global__ void k_fill_items(long long E2, const long long* __restrict__ item_ba
 // wavefronts and no registers across the round loop.
 struct QFam {
   int nsub, fold, coeff_off, coef_global, deg, khead, tail_off;
+  int npos, delta_off;      // positions; offset of the delta table in the smem copy
   unsigned sp_neg, sn_neg;  // bit t: sign of table t is -1 for a >= 0 / a < 0 (fold)
   double lo, w, inv_w, amin, amax;
   const double* delta;
@@ -325,6 +326,7 @@ struct QuadArgs {
   const double* blob;      // coefficients of the launch's families, concatenated
   int blob_doubles;
   int coef_in_smem;
+  int delta_doubles;          // sum of npos over the launch's families (smem delta tables)
   const int* tri;
   const double* corners;
   const double* a2;
@@ -339,7 +341,10 @@ struct QuadArgs {
   unsigned long long* n_in;
 };
 
-constexpr int kQuadWarps = 12;
+#ifndef TDB_QW
+#define TDB_QW 12
+#endif
+constexpr int kQuadWarps = TDB_QW;
 constexpr int kNK = kChunk / 32;
 constexpr int kGroupChunks = 16;  // chunks of one (singular) pair handled by one work item
 constexpr int kBuckets = 256;
@@ -572,6 +577,10 @@ __device__ __forceinline__ void eval_rounds(const QFam& fd, const double* __rest
       const bool act = in[u] && av >= amin && av <= amax;
       n_act += act ? 1u : 0u;
       cw[u] = act ? c[u] : 0.0;
+      if constexpr (P == 0) {  // psi and psi~ of a (fold) family share the sign: apply it to the weight
+        const unsigned sg = av < 0.0 ? sn_neg : sp_neg;
+        if (sg & 1u) cw[u] = -cw[u];
+      }
       const double aa = fold ? fabs(av) : av;
       idx[u] = max(0, cheb_locate(aa, lo, w, inv_w, nsub, xl[u]));
       neg[u] = av < 0.0;
@@ -583,9 +592,11 @@ __device__ __forceinline__ void eval_rounds(const QFam& fd, const double* __rest
       for (int u = 0; u < NS; ++u) {
         const XPow X = xpowers(xl[u]);
         eval_pair<NT, GLOBAL, D, K>(cf, tail_off, idx[u], m, X, v0[u], v1[u]);
-        const unsigned sg = neg[u] ? sn_neg : sp_neg;
-        if ((sg >> (2 * m)) & 1u) v0[u] = -v0[u];
-        if ((sg >> (2 * m + 1)) & 1u) v1[u] = -v1[u];
+        if constexpr (P > 0) {
+          const unsigned sg = neg[u] ? sn_neg : sp_neg;
+          if ((sg >> (2 * m)) & 1u) v0[u] = -v0[u];
+          if ((sg >> (2 * m + 1)) & 1u) v1[u] = -v1[u];
+        }
       }
       double* S = acc + 10 * m;
 #pragma unroll
@@ -614,9 +625,10 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
   constexpr int NM = (P + 1) * (P + 1);
   constexpr int NACC = 10 * NM;
   extern __shared__ __align__(16) double smem[];
-  // layout: [coef blob][per warp scratch]
+  // layout: [coef blob][position delta tables][per warp scratch]
   double* sblob = smem;
-  char* swarp = reinterpret_cast<char*>(sblob + (SMEM_COEF ? (a.blob_doubles + 1) / 2 * 2 : 0));
+  double* sdelta = sblob + (SMEM_COEF ? (a.blob_doubles + 1) / 2 * 2 : 0);
+  char* swarp = reinterpret_cast<char*>(sdelta + (a.delta_doubles + 1) / 2 * 2);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* sr = reinterpret_cast<double*>(swarp + (size_t)wid * kWarpScratchBytes);
   double* sc = sr + kChunk;
@@ -626,10 +638,20 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
   double* sy2 = sy1 + kChunk;
   unsigned* cur = reinterpret_cast<unsigned*>(sy2 + kChunk);  // kBuckets + 1
 
-  {  // stage the coefficients
+  {  // stage the coefficients and the per-position table offsets
     if (SMEM_COEF)
       for (int i = threadIdx.x; i < a.blob_doubles; i += blockDim.x) sblob[i] = a.blob[i];
+    for (int fi = 0; fi < a.fam_count; ++fi)
+      for (int i = threadIdx.x; i < a.fam[fi].npos; i += blockDim.x) sdelta[a.fam[fi].delta_off + i] = a.fam[fi].delta[i];
     __syncthreads();
+  }
+  // lane -> reduced value indices of the warp reduce-scatter (fixed per lane)
+  int rs_base, rs_valid;
+  {
+    double z[NACC], zo[RS<NACC>::H5];
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) z[k] = 0.0;
+    warp_reduce_scatter<NACC>(z, lane, zo, rs_base, rs_valid);
   }
   const double* coef_base = SMEM_COEF ? sblob : a.blob;
   const long long E2 = a.npair;
@@ -643,11 +665,10 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
     if (it >= a.nitems) break;
     const int2 item = a.items[it];
     const int Pp = item.x, grp = item.y;
-    // any unit of this item in the launch's families?
-    bool any = false;
-    for (int fi = 0; fi < a.fam_count; ++fi)
-      any |= (a.frange[(long long)a.fam_ids[fi] * E2 + Pp].lo_cnt >> 16) != 0;
-    if (!any) continue;
+    // admissible position ranges of the launch's families: lane fi holds family fi's
+    FRange my_fr{0, 0};
+    if (lane < a.fam_count) my_fr = a.frange[(long long)a.fam_ids[lane] * E2 + Pp];
+    if (__ballot_sync(0xffffffffu, (my_fr.lo_cnt >> 16) != 0) == 0u) continue;
     const int ey = a.tt[Pp / a.E], ex = Pp % a.E;
     int lx[3], ly[3];
     const int cs = pair_topology(a.tri, ex, ey, lx, ly);
@@ -762,7 +783,9 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
     pt.rmax = rmax;
     pt.inv_wb = inv_wb;
     for (int fi = 0; fi < a.fam_count; ++fi) {
-      const FRange fr = a.frange[(long long)a.fam_ids[fi] * E2 + Pp];
+      FRange fr;
+      fr.foff = __shfl_sync(0xffffffffu, my_fr.foff, fi);
+      fr.lo_cnt = __shfl_sync(0xffffffffu, my_fr.lo_cnt, fi);
       const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
       if (cnt == 0) continue;
       const QFam& fd = a.fam[fi];
@@ -771,7 +794,7 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
       const double* cf_g = fd.coeffs;
       for (int si = 0; si < cnt; ++si) {
         double* dst = a.part + (slot0 + fr.foff + si) * NACC;
-        const double delta = fd.delta[s_lo + si];
+        const double delta = sdelta[fd.delta_off + s_lo + si];
         int i0, i1;
         position_range(fd, pt, delta, i0, i1);
         if (i0 >= i1) {  // no rule point of this chunk in the position's support (warp-uniform)
@@ -779,6 +802,10 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
             for (int k = lane; k < NACC; k += 32) dst[k] = 0.0;
           continue;
         }
+        // previous chunks' partial sums of this unit: loaded now, used after the rounds
+        double prev[RS<NACC>::H5];
+#pragma unroll
+        for (int k = 0; k < RS<NACC>::H5; ++k) prev[k] = (!first && k < rs_valid) ? dst[rs_base + k] : 0.0;
         double acc[NACC];
 #pragma unroll
         for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
@@ -811,7 +838,7 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
 #endif
 #pragma unroll
         for (int k = 0; k < RS<NACC>::H5; ++k)
-          if (k < valid) dst[base + k] = first ? outv[k] : dst[base + k] + outv[k];
+          if (k < valid) dst[base + k] = first ? outv[k] : prev[k] + outv[k];
       }
     }
     __syncwarp();
@@ -1227,6 +1254,7 @@ struct AsmWorkspace {
   struct Launch {
     std::vector<int> fams;
     std::vector<QFam> qfam;
+    int delta_doubles = 0;
     bool in_smem = false;
     size_t bytes = 0, smem = 0;
     FamDev* d_fam = nullptr;
@@ -1407,6 +1435,7 @@ int tdb_system_run_impl(TdbSystem* sys) {
     qa.blob = L.d_blob;
     qa.blob_doubles = L.in_smem ? L.blob_doubles : 0;
     qa.coef_in_smem = L.in_smem;
+    qa.delta_doubles = L.delta_doubles;
     qa.tri = sys->tri;
     qa.corners = sys->corners;
     qa.a2 = sys->a2;
@@ -1772,7 +1801,9 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
   int max_smem = 0;
   TDB_CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   const size_t warp_bytes = (size_t)kQuadWarps * kWarpScratchBytes;
-  const size_t budget = (size_t)max_smem - warp_bytes - ((sizeof(FamDev) * F + 15) / 16) * 16 - 64;
+  size_t delta_bytes = 0;
+  for (int f = 0; f < F; ++f) delta_bytes += (size_t)sys->fam[f].npos * 8;
+  const size_t budget = (size_t)max_smem - warp_bytes - (delta_bytes + 16) / 16 * 16 - 64;
   {
     std::vector<int> order(F);
     for (int f = 0; f < F; ++f) order[f] = f;
@@ -1817,6 +1848,9 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
         q.deg = fd.deg;
         q.khead = fd.khead;
         q.tail_off = fd.tail_off;
+        q.npos = fd.npos;
+        q.delta_off = L.delta_doubles;
+        L.delta_doubles += fd.npos;
         q.sp_neg = q.sn_neg = 0u;
         for (int t = 0; t < nt; ++t) {
           if (fd.fold && fd.sp[t] < 0.0) q.sp_neg |= 1u << t;
@@ -1829,13 +1863,17 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
         q.amax = fd.amax;
         q.delta = fd.delta;
         q.coeffs = fd.coeffs;
+        if (p == 0 && (((q.sp_neg ^ (q.sp_neg >> 1)) & 1u) || ((q.sn_neg ^ (q.sn_neg >> 1)) & 1u))) {
+          set_error("assemble: p = 0 family with different psi / psi~ fold signs");
+          return TDB_E_INVALID;
+        }
         L.qfam.push_back(q);
       }
       L.blob_doubles = (int)lb.size();
       L.bytes = lb.size() * 8;
       if ((rc = dupload(&L.d_blob, lb.data(), lb.size(), st))) return rc;
       if ((rc = dupload(&L.d_fam, fdv.data(), fdv.size(), st))) return rc;
-      L.smem = (L.bytes + 15) / 16 * 16 + warp_bytes;
+      L.smem = (L.bytes + 15) / 16 * 16 + (size_t)(L.delta_doubles + 1) / 2 * 16 + warp_bytes;
       ws->launches.push_back(std::move(L));
     }
   }

@@ -75,9 +75,8 @@ __device__ __forceinline__ int cheb_locate(double a, double lo, double w, double
   const double t = (a - lo) * inv_w;
   int idx = (int)t;
   idx = idx > nsub - 1 ? nsub - 1 : idx;
-  double xl = 2.0 * (a - lo - (double)idx * w) * inv_w - 1.0;
-  xl = xl < -1.0 ? -1.0 : xl;
-  x = xl > 1.0 ? 1.0 : xl;
+  const double xl = 2.0 * (a - lo - (double)idx * w) * inv_w - 1.0;
+  x = fmin(fmax(xl, -1.0), 1.0);  // xl is never NaN here: same result as the compares
   return idx;
 }
 
