@@ -16,6 +16,8 @@
  *   tdb_system_copy_family        <- the CSR lists of BlockHessenbergMatrix
  *                                    .unique_blocks (block_system.py:145)
  *   tdb_matvec (+ plan)           <- block_system.py:180-216 matvec(x, rows, cols)
+ *   tdb_krylov_*                  <- solvers.py:189-222 (_gmres_cycle_raw's Givens
+ *                                    bookkeeping and final update, on the device)
  */
 #ifndef TDB_H_
 #define TDB_H_
@@ -222,6 +224,32 @@ int tdb_matvec_plan_destroy(TdbMatvecPlan* plan);
 int tdb_matvec(TdbMatvecPlan* plan, const double* x_dev, double* y_dev);
 /* canonical stored bytes and logical flops of one application of this plan */
 int tdb_matvec_plan_work(const TdbMatvecPlan* plan, double* algorithmic_bytes, double* flops);
+
+/* ---- device-side GMRES cycle bookkeeping (solvers.py:172-223) ------------
+ * Replaces the per-Arnoldi-step host round trip of _gmres_cycle_raw
+ * (reference solvers.py:189-215: Hessenberg column, Givens rotations,
+ * convergence and breakdown tests) and the final solve_triangular + Z^T y
+ * update (:217-222) for fixed-iteration inner solves, so a whole preconditioner
+ * application can be captured in a CUDA graph.  All pointers are device
+ * pointers; `stream` is a cudaStream_t (NULL = legacy default stream).
+ * state: TDB_KS_NSTATE doubles.  H is (m+1) x ldh row-major. */
+#define TDB_KS_DONE 0
+#define TDB_KS_KDONE 1
+#define TDB_KS_BREAKDOWN 2
+#define TDB_KS_TOL_ABS 3
+#define TDB_KS_BETA 4
+#define TDB_KS_CONVERGED 5
+#define TDB_KS_NSTATE 8
+/* beta: device scalar ||b|| (x0 = 0); tol_abs = tol_rel * beta; g[0] = beta */
+int tdb_krylov_init(double* state, const double* beta, double tol_rel, double* g, void* stream);
+/* step k: hcol[0..k+1] = (V_j . w for j <= k, ||w||) */
+int tdb_krylov_givens(double* state, int32_t k, const double* hcol, double* H, int32_t ldh, double* cs,
+                      double* sn, double* g, void* stream);
+/* x[0..n) = x0 + sum_{j < k_done} y_j Z[j*ldz + i], H[:k_done,:k_done] y = g (x0 may be NULL) */
+int tdb_krylov_update(double* x, const double* x0, const double* Z, int64_t ldz, int64_t n, const double* state,
+                      const double* H, int32_t ldh, const double* g, int32_t m, void* stream);
+/* *err = 1 if the cycle broke down without converging (BreakdownError) */
+int tdb_krylov_flag(const double* state, double* err, void* stream);
 
 #ifdef __cplusplus
 }

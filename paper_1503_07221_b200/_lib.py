@@ -122,6 +122,11 @@ def _load():
         "tdb_matvec_plan_destroy": (i32, [P]),
         "tdb_matvec": (i32, [P, P, P]),
         "tdb_matvec_plan_work": (i32, [P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+        # device-side GMRES cycle bookkeeping (pointers are device addresses)
+        "tdb_krylov_init": (i32, [P, P, C.c_double, P, P]),
+        "tdb_krylov_givens": (i32, [P, i32, P, P, i32, P, P, P, P]),
+        "tdb_krylov_update": (i32, [P, P, P, i64, i64, P, P, i32, P, i32, P]),
+        "tdb_krylov_flag": (i32, [P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -139,8 +144,11 @@ EXPORTED = (
     "tdb_system_destroy", "tdb_system_stats", "tdb_system_family_nnz", "tdb_system_copy_family",
     "tdb_system_family_device", "tdb_matvec_plan_create", "tdb_matvec_plan_destroy", "tdb_matvec",
     "tdb_matvec_plan_work", "tdb_tri_distance_bounds", "tdb_system_create", "tdb_system_run",
-    "tdb_fp64_peak",
+    "tdb_fp64_peak", "tdb_krylov_init", "tdb_krylov_givens", "tdb_krylov_update", "tdb_krylov_flag",
 )
+
+# TDB_KS_* cycle-state slots (include/tdb.h)
+KS_DONE, KS_KDONE, KS_BREAKDOWN, KS_TOL_ABS, KS_BETA, KS_CONVERGED, KS_NSTATE = 0, 1, 2, 3, 4, 5, 8
 
 
 def check(rc: int, what: str = "") -> None:

@@ -17,6 +17,15 @@ same device, normally BlockHessenbergMatrix.matvec (csrc/tdb_matvec.cu).  The
 (m+1) x m Hessenberg matrix, Givens rotations, the triangular solve and the
 Schur decompositions (at most 50 x 50) stay on the host, one small
 device->host copy per Arnoldi step, exactly as the reference orders them.
+
+The fixed-iteration inner solves of the recursive preconditioner (restart ==
+max_iter, tol 1e-14: one cycle) take a host-sync-free path on CUDA vectors:
+classical Gram-Schmidt with one re-orthogonalisation pass (two GEMVs per pass,
+as accurate as the reference's MGS), and the Hessenberg / Givens / convergence
+bookkeeping on the device (csrc/tdb_krylov.cu).  Early exit is emulated on the
+device, so the iterate equals the one the reference's loop returns.  The whole
+preconditioner application of a single-device solve is then captured once in
+a CUDA graph and replayed per outer step.
 """
 
 from __future__ import annotations
@@ -260,6 +269,66 @@ def _gmres_cycle_raw(apply_A, b, x0, m, tol_abs, precond, history):
     return x, converged, breakdown, dict(V=V, Hraw=Hraw, k=k_done)
 
 
+def _gemv_t(V: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    """h = V w (rows of V are Krylov vectors), all-reduced across row blocks."""
+    h = torch.mv(V, w)
+    return _COMM.allreduce_(h) if _COMM.size > 1 else h
+
+
+def _cycle_fixed_device(apply_A, b: torch.Tensor, m: int, tol: float, precond, err: torch.Tensor):
+    """One GMRES / FGMRES cycle of at most m steps from x0 = 0 with no host
+    synchronisation (the reference's _run_restarted with restart == max_iter,
+    solvers.py:145-169 + :172-223).  Returns x; a breakdown without convergence
+    sets err[0] = 1 (BreakdownError, checked by the caller)."""
+    from . import _lib
+
+    n = b.shape[0]
+    dev, dt = b.device, b.dtype
+    stream = C_void(torch.cuda.current_stream(dev).cuda_stream)
+    st = torch.empty(_lib.KS_NSTATE, dtype=dt, device=dev)
+    H = torch.zeros((m + 1, m), dtype=dt, device=dev)
+    cs = torch.empty(m, dtype=dt, device=dev)
+    sn = torch.empty(m, dtype=dt, device=dev)
+    g = torch.zeros(m + 1, dtype=dt, device=dev)
+    hcol = torch.empty(m + 1, dtype=dt, device=dev)
+    V = torch.empty((m, n), dtype=dt, device=dev)
+    Z = V if precond is None else torch.empty((m, n), dtype=dt, device=dev)
+    beta = _norm(b).reshape(1)
+    L = _lib.LIB
+    _lib.check(L.tdb_krylov_init(_ptr(st), _ptr(beta), float(tol), _ptr(g), stream), "krylov_init")
+    torch.div(b, beta, out=V[0])
+    for k in range(m):
+        if precond is not None:
+            Z[k].copy_(precond(V[k]))
+        w = apply_A(Z[k]).clone()
+        Vk = V[: k + 1]
+        h = _gemv_t(Vk, w)
+        w.sub_(torch.mv(Vk.T, h))
+        h2 = _gemv_t(Vk, w)
+        w.sub_(torch.mv(Vk.T, h2))
+        torch.add(h, h2, out=hcol[: k + 1])
+        hcol[k + 1 : k + 2].copy_(_norm(w).reshape(1))
+        _lib.check(L.tdb_krylov_givens(_ptr(st), k, _ptr(hcol), _ptr(H), m, _ptr(cs), _ptr(sn), _ptr(g),
+                                       stream), "krylov_givens")
+        if k + 1 < m:
+            torch.div(w, hcol[k + 1 : k + 2], out=V[k + 1])
+    x = torch.empty(n, dtype=dt, device=dev)
+    _lib.check(L.tdb_krylov_update(_ptr(x), None, _ptr(Z), n, n, _ptr(st), _ptr(H), m, _ptr(g), m, stream),
+               "krylov_update")
+    _lib.check(L.tdb_krylov_flag(_ptr(st), _ptr(err), stream), "krylov_flag")
+    return x
+
+
+def C_void(v):
+    import ctypes
+
+    return ctypes.c_void_p(v)
+
+
+def _ptr(t: torch.Tensor):
+    return C_void(t.data_ptr())
+
+
 def _run_restarted(apply_A, b, cfg: SolverConfig, precond_factory, per_cycle=None):
     nb = float(_norm(b))
     if nb == 0.0:
@@ -333,7 +402,63 @@ def _inner_cfg(cfg: SolverConfig, level: int) -> SolverConfig:
     return SolverConfig(method="fgmres", restart=iters, tol=1e-14, max_iter=iters)
 
 
-def recursive_preconditioner(A, cfg: SolverConfig, level: int = 1, rows=None):
+class _ErrBox:
+    """Sticky device breakdown flag shared by the inner solves of one preconditioner."""
+
+    def __init__(self):
+        self.t = None
+
+    def on(self, device) -> torch.Tensor:
+        if self.t is None or self.t.device != device:
+            self.t = torch.zeros(1, dtype=torch.float64, device=device)
+        return self.t
+
+
+def _inner_solve(apply_A, r, icfg: SolverConfig, precond, err: _ErrBox):
+    """Fixed-iteration inner FGMRES (one cycle): device path on CUDA vectors."""
+    if r.is_cuda:
+        return _cycle_fixed_device(apply_A, r, icfg.restart, icfg.tol, precond, err.on(r.device))
+    x, _ = fgmres(apply_A, r, icfg, precond=precond)
+    return x
+
+
+class _GraphedPreconditioner:
+    """r -> P r of the recursive preconditioner, captured once in a CUDA graph
+    (single device; two eager warm-up calls create every matvec plan first)."""
+
+    def __init__(self, fn, err: _ErrBox):
+        self.fn = fn
+        self.err = err
+        self.calls = 0
+        self.graph = None
+        self.static_in = self.static_out = None
+
+    def _check(self):
+        if self.err.t is not None and float(self.err.t[0]) != 0.0:
+            raise BreakdownError("inner Arnoldi breakdown before convergence")
+
+    def __call__(self, r):
+        if not r.is_cuda:
+            return self.fn(r)
+        self.calls += 1
+        if _COMM.size > 1 or self.calls <= 2:
+            out = self.fn(r)
+            self._check()
+            return out
+        if self.graph is None:
+            self.static_in = r.clone()
+            torch.cuda.synchronize(r.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.static_out = self.fn(self.static_in)
+            self.graph = g
+        self.static_in.copy_(r)
+        self.graph.replay()
+        self._check()
+        return self.static_out.clone()
+
+
+def recursive_preconditioner(A, cfg: SolverConfig, level: int = 1, rows=None, err=None):
     """Block lower-triangular half-split preconditioner (paper 4.2, reference :276-315).
 
     A.matvec(v, rows, cols) is the device block Hessenberg matvec; each half is
@@ -341,23 +466,25 @@ def recursive_preconditioner(A, cfg: SolverConfig, level: int = 1, rows=None):
     level < m_r.
     """
     lo, hi = rows if rows is not None else (1, A.grid.N)
+    top = err is None
+    if top:
+        err = _ErrBox()
     count = hi - lo + 1
     if count < 2:
         def solo(r):
-            x, _ = fgmres(lambda v: A.matvec(v, rows=(lo, hi), cols=(lo, hi)), r, _inner_cfg(cfg, level))
-            return x
-        return solo
+            return _inner_solve(lambda v: A.matvec(v, rows=(lo, hi), cols=(lo, hi)), r, _inner_cfg(cfg, level),
+                                None, err)
+        return _GraphedPreconditioner(solo, err) if top else solo
     split = lo + (count + 1) // 2 - 1
     n1 = (split - lo + 1) * (A.grid.p + 1) * A.M
     inner_1 = inner_2 = None
     if level < cfg.recursion_depth:
-        inner_1 = recursive_preconditioner(A, cfg, level + 1, rows=(lo, split))
-        inner_2 = recursive_preconditioner(A, cfg, level + 1, rows=(split + 1, hi))
+        inner_1 = recursive_preconditioner(A, cfg, level + 1, rows=(lo, split), err=err)
+        inner_2 = recursive_preconditioner(A, cfg, level + 1, rows=(split + 1, hi), err=err)
 
     def half_solve(r, blo, bhi, prec):
-        x, _ = fgmres(lambda v: A.matvec(v, rows=(blo, bhi), cols=(blo, bhi)), r, _inner_cfg(cfg, level),
-                      precond=prec)
-        return x
+        return _inner_solve(lambda v: A.matvec(v, rows=(blo, bhi), cols=(blo, bhi)), r, _inner_cfg(cfg, level),
+                            prec, err)
 
     def prec(r):
         r1 = r[:n1].contiguous()
@@ -367,7 +494,7 @@ def recursive_preconditioner(A, cfg: SolverConfig, level: int = 1, rows=None):
         x2 = half_solve(r2c.contiguous(), split + 1, hi, inner_2)
         return torch.cat([x1, x2])
 
-    return prec
+    return _GraphedPreconditioner(prec, err) if top else prec
 
 
 def solve(A, b, cfg: SolverConfig, device=None):
