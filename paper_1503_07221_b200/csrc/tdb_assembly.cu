@@ -954,26 +954,34 @@ struct RowStar {  // star of the test vertex j, cached in shared memory per CTA
   int pj[kMaxStar];  // local position of j in triangle e
 };
 
-// Value of CSR entry (j, l) of position s: every contribution of a pair
-// (ex in star(l), ey in star(j)) admissible at s, summed with Kahan's
-// compensation in the reference's canonical order (case groups regular,
-// coincident, edge, vertex; pairs (ex, ey) ascending within a group;
-// assembly.py:261-306 + _kahan_csr :187-214).  Regular contributions are
-// added in the single scan; the few touching pairs are deferred and added
-// case by case afterwards.
-template <int NM>
-__device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s, int j, int l, double* out) {
-  double sum[NM], comp[NM];
+// Values of CSR entry (j, l) at the positions s0 .. s0 + SC - 1 (clipped to s_end):
+// every contribution of a pair (ex in star(l), ey in star(j)) admissible at s,
+// summed with Kahan's compensation in the reference's canonical order (case
+// groups regular, coincident, edge, vertex; pairs (ex, ey) ascending within a
+// group; assembly.py:261-306 + _kahan_csr :187-214).  Each (ex, ey) combo is
+// resolved once (admissible range, partial slot, chart permutation, n_x.n_y,
+// curl product) and then applied to all SC positions of the chunk, so the
+// combo scan is amortised over the positions.  Regular contributions are added
+// in the single scan; the few touching pairs are deferred and added case by
+// case afterwards.
+template <int NM, int SC>
+__device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s0, int s_end, int j, int l,
+                             double (&sum)[SC][NM]) {
+  double comp[SC][NM];
 #pragma unroll
-  for (int m = 0; m < NM; ++m) sum[m] = comp[m] = 0.0;
+  for (int u = 0; u < SC; ++u)
+#pragma unroll
+    for (int m = 0; m < NM; ++m) sum[u][m] = comp[u][m] = 0.0;
   const int lb = a.star_off[l], le = a.star_off[l + 1];
+  const int s1 = min(s0 + SC, s_end);
   constexpr int kDefer = 64;    // touching combos of (star(l), star(j)); 36 for valence 6
   unsigned deferred[kDefer];    // (case << 16) | (kx << 8) | ky, in (ex, ey) order
   int nd = 0;
   bool overflow = false;
-  auto contribute = [&](int ex, int ey, int kx_local, int ky, int cs, const FRange& fr, int s_lo) {
+  auto contribute = [&](int ex, int ey, int ky, int cs, const FRange& fr) {
+    const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
     const long long Pp = (long long)rs.k[ky] * a.E + ex;
-    const long long slot = a.pair_base[Pp] + fr.foff + (s - s_lo);
+    const long long slot0 = a.pair_base[Pp] + fr.foff - s_lo;
     int ca = rs.pj[ky], cb = 0;
     const int* tx = a.tri + 3 * ex;
     cb = (tx[0] == l) ? 0 : ((tx[1] == l) ? 1 : 2);
@@ -993,16 +1001,21 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s, int
     const double* cyv = a.curls + 9 * (long long)ey + 3 * pj;
     const double* cxv = a.curls + 9 * (long long)ex + 3 * pl;
     const double cd = cyv[0] * cxv[0] + cyv[1] * cxv[1] + cyv[2] * cxv[2];
-    const double* pv = a.part + slot * a.nacc;
+    const int ab = 3 * ca + cb;
 #pragma unroll
-    for (int m = 0; m < NM; ++m) {
-      const double v = nd_ * pv[10 * m + 3 * ca + cb] + cd * pv[10 * m + 9];
-      const double y = v - comp[m];
-      const double t = sum[m] + y;
-      comp[m] = (t - sum[m]) - y;
-      sum[m] = t;
+    for (int u = 0; u < SC; ++u) {
+      const int s = s0 + u;
+      if (s >= s1 || s < s_lo || s >= s_lo + cnt) continue;
+      const double* pv = a.part + (slot0 + s) * a.nacc;
+#pragma unroll
+      for (int m = 0; m < NM; ++m) {
+        const double v = nd_ * pv[10 * m + ab] + cd * pv[10 * m + 9];
+        const double y = v - comp[u][m];
+        const double t = sum[u][m] + y;
+        comp[u][m] = (t - sum[u][m]) - y;
+        sum[u][m] = t;
+      }
     }
-    (void)kx_local;
   };
   for (int kx = lb; kx < le; ++kx) {
     const int ex = a.star_ids[kx];
@@ -1011,7 +1024,7 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s, int
       const int ey = rs.e[ky];
       const FRange fr = a.frange[(long long)rs.k[ky] * a.E + ex];
       const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
-      if (s < s_lo || s >= s_lo + cnt) continue;
+      if (s1 <= s_lo || s0 >= s_lo + cnt) continue;
       int cs;
       if (ex == ey) {
         cs = TDB_CASE_COINCIDENT;
@@ -1022,7 +1035,7 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s, int
         cs = nsh == 0 ? TDB_CASE_REGULAR : (nsh == 2 ? TDB_CASE_EDGE : TDB_CASE_VERTEX);
       }
       if (cs == TDB_CASE_REGULAR) {
-        contribute(ex, ey, kx - lb, ky, cs, fr, s_lo);
+        contribute(ex, ey, ky, cs, fr);
       } else if (nd < kDefer) {
         deferred[nd++] = ((unsigned)cs << 16) | ((unsigned)(kx - lb) << 8) | (unsigned)ky;
       } else {
@@ -1036,8 +1049,7 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s, int
         if ((int)(deferred[d] >> 16) != cr) continue;
         const int kxl = (deferred[d] >> 8) & 0xff, ky = deferred[d] & 0xff;
         const int ex = a.star_ids[lb + kxl], ey = rs.e[ky];
-        const FRange fr = a.frange[(long long)rs.k[ky] * a.E + ex];
-        contribute(ex, ey, kxl, ky, cr, fr, fr.lo_cnt & 0xffff);
+        contribute(ex, ey, ky, cr, a.frange[(long long)rs.k[ky] * a.E + ex]);
       }
     } else {  // very high valence: rescan the combos of this case in order
       for (int kx = lb; kx < le; ++kx) {
@@ -1047,21 +1059,26 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s, int
           if (case_of(a.tri, ex, ey) != cr) continue;
           const FRange fr = a.frange[(long long)rs.k[ky] * a.E + ex];
           const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
-          if (s < s_lo || s >= s_lo + cnt) continue;
-          contribute(ex, ey, kx - lb, ky, cr, fr, s_lo);
+          if (s1 <= s_lo || s0 >= s_lo + cnt) continue;
+          contribute(ex, ey, ky, cr, fr);
         }
       }
     }
   }
-#pragma unroll
-  for (int m = 0; m < NM; ++m) out[m] = sum[m];
 }
 
+// CTA per (test vertex j, chunk of positions): bitmap pattern of every position,
+// their union, per-position popcount prefixes; then one thread per union entry
+// (j, l) gathers its values for SC positions at a time and writes the entries
+// that are in each position's pattern.
 template <int NM>
 __global__ void k_pattern_fill(PatternArgs a) {
+  constexpr int SC = NM >= 8 ? 1 : 8 / NM;
   extern __shared__ unsigned smem_u[];
-  unsigned* bm = smem_u;
-  int* pref = reinterpret_cast<int*>(smem_u + a.s_count * a.words);  // words + 1
+  unsigned* bm = smem_u;                                                   // [s_count][words]
+  int* pref = reinterpret_cast<int*>(smem_u + a.s_count * a.words);       // [s_count][words]
+  unsigned* un = reinterpret_cast<unsigned*>(pref + a.s_count * a.words);  // [words] union
+  int* upref = reinterpret_cast<int*>(un + a.words);                       // [words + 1]
   const int rloc = blockIdx.x, j = a.rows[rloc];
   __shared__ RowStar rs;
   if (threadIdx.x == 0) {
@@ -1080,41 +1097,64 @@ __global__ void k_pattern_fill(PatternArgs a) {
   build_bitmaps(a, j, bm);  // (syncs the block)
   typedef cub::BlockScan<int, 256> Scan;
   __shared__ typename Scan::TempStorage tmp;
-  for (int sl = 0; sl < a.s_count; ++sl) {
-    const unsigned* b = bm + sl * a.words;
-    const long long row = (long long)(a.s_begin + sl) * a.nrows + rloc;
-    const int64_t base = a.indptr[row];
-    // exclusive prefix of popcounts over words (chunks of 256 words)
+  // union bitmap
+  for (int w = threadIdx.x; w < a.words; w += blockDim.x) {
+    unsigned u = 0u;
+    for (int sl = 0; sl < a.s_count; ++sl) u |= bm[sl * a.words + w];
+    un[w] = u;
+  }
+  __syncthreads();
+  // exclusive popcount prefixes: per position (write offsets) and of the union (entry list)
+  for (int sl = 0; sl <= a.s_count; ++sl) {
+    const unsigned* b = sl < a.s_count ? bm + sl * a.words : un;
+    int* pr = sl < a.s_count ? pref + sl * a.words : upref;
     int carry = 0;
     for (int w0 = 0; w0 < a.words; w0 += 256) {
       const int w = w0 + threadIdx.x;
       int c = w < a.words ? __popc(b[w]) : 0, ex;
       int agg;
       Scan(tmp).ExclusiveSum(c, ex, agg);
-      if (w < a.words) pref[w] = carry + ex;
+      if (w < a.words) pr[w] = carry + ex;
       carry += agg;
       __syncthreads();
     }
-    if (threadIdx.x == 0) pref[a.words] = carry;
-    __syncthreads();
-    const int nrow = carry;
-    for (int e = threadIdx.x; e < nrow; e += blockDim.x) {
-      int lo = 0, hi = a.words - 1;  // last word with pref[w] <= e
-      while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (pref[mid] <= e) lo = mid; else hi = mid - 1;
-      }
-      unsigned word = b[lo];
-      int rank = e - pref[lo];
-      for (int r = 0; r < rank; ++r) word &= word - 1;
-      const int l = lo * 32 + (__ffs(word) - 1);
-      double vals[NM];
-      gather_entry<NM>(a, rs, a.s_begin + sl, j, l, vals);
-      a.indices[base + e] = l;
-#pragma unroll
-      for (int m = 0; m < NM; ++m) a.data[(base + e) * NM + m] = vals[m];
+    if (sl == a.s_count && threadIdx.x == 0) upref[a.words] = carry;
+  }
+  __syncthreads();
+  const int nent = upref[a.words];
+  const int s_end = a.s_begin + a.s_count;
+  for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+    int lo = 0, hi = a.words - 1;  // last word with upref[w] <= e
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (upref[mid] <= e) lo = mid; else hi = mid - 1;
     }
-    __syncthreads();
+    unsigned word = un[lo];
+    int rank = e - upref[lo];
+    for (int r = 0; r < rank; ++r) word &= word - 1;
+    const int bit = __ffs(word) - 1;
+    const int l = lo * 32 + bit;
+    const unsigned below = (1u << bit) - 1u;
+    for (int s0 = a.s_begin; s0 < s_end; s0 += SC) {
+      // next position whose pattern holds (j, l): chunks start there (an entry is
+      // non-zero at a few consecutive lags only)
+      while (s0 < s_end && !((bm[(s0 - a.s_begin) * a.words + lo] >> bit) & 1u)) ++s0;
+      if (s0 >= s_end) break;
+      double vals[SC][NM];
+      gather_entry<NM, SC>(a, rs, s0, s_end, j, l, vals);
+#pragma unroll
+      for (int u = 0; u < SC; ++u) {
+        const int sl = s0 + u - a.s_begin;
+        if (s0 + u >= s_end) continue;
+        const unsigned bw = bm[sl * a.words + lo];
+        if (!((bw >> bit) & 1u)) continue;
+        const long long row = (long long)(a.s_begin + sl) * a.nrows + rloc;
+        const int64_t pos = a.indptr[row] + pref[sl * a.words + lo] + __popc(bw & below);
+        a.indices[pos] = l;
+#pragma unroll
+        for (int m = 0; m < NM; ++m) a.data[pos * NM + m] = vals[u][m];
+      }
+    }
   }
 }
 
@@ -1472,7 +1512,7 @@ int tdb_system_run_impl(TdbSystem* sys) {
     for (int s0 = 0; s0 < ga.npos; s0 += ws->s_chunk[f]) {
       ga.s_begin = s0;
       ga.s_count = std::min(ws->s_chunk[f], ga.npos - s0);
-      const size_t smem = (size_t)ga.s_count * ws->words * 4 + (ws->words + 1) * 4;
+      const size_t smem = (size_t)ga.s_count * ws->words * 8 + (2 * ws->words + 1) * 4;
       switch (NM) {
         case 1: rc = launch_fill<1>(ga, smem, st); break;
         case 4: rc = launch_fill<4>(ga, smem, st); break;
@@ -1927,7 +1967,7 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
   long long max_rows = 0;
   for (int f = 0; f < F; ++f) {
     const int npos = sys->fam[f].npos;
-    ws->s_chunk[f] = std::max(1, (int)std::min<long long>(npos, (96LL * 1024) / (ws->words * 4)));
+    ws->s_chunk[f] = std::max(1, (int)std::min<long long>(npos, (96LL * 1024) / (ws->words * 8)));
     max_rows = std::max(max_rows, (long long)npos * V + 1);  // >= npos * nrows + 1
   }
   {
