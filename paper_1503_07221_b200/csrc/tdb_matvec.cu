@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "tdb_common.cuh"
@@ -50,6 +51,8 @@ struct MvArgs {
   const double* xt;         // [M][xs]: row l = x[l][block col][m1], then NP1 zeros
   int xs;                   // row stride of xt = nc*NP1 + NP1
   double* ypart;            // [G][M][nr*NP1]
+  double* y;                // output, time-major y[(block row)*NP1 + m][row]
+  unsigned* row_done;       // [nrows] groups finished per row (reset by the last one)
 };
 
 __global__ void k_transpose_in(const double* __restrict__ x, double* __restrict__ xt, int M,
@@ -321,6 +324,18 @@ __global__ void __launch_bounds__(32, TDB_MV_MIN_BLOCKS) k_matvec(MvArgs a) {
     cp_async_commit();
     buf ^= 1;
   }
+  // Partial rows of the G term groups are summed in group order by the warp that
+  // finishes row j last (threadfence reduction: deterministic, no extra launch).
+  if (a.G == 1) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int r = lane + 32 * c;
+      if (r < a.nr)
+#pragma unroll
+        for (int m = 0; m < NP1; ++m) a.y[(long long)(r * NP1 + m) * a.nrows + j] = acc[c][m];
+    }
+    return;
+  }
   double* yp = a.ypart + ((long long)g * a.nrows + j) * (a.nr * NP1);
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
@@ -329,6 +344,27 @@ __global__ void __launch_bounds__(32, TDB_MV_MIN_BLOCKS) k_matvec(MvArgs a) {
 #pragma unroll
       for (int m = 0; m < NP1; ++m) yp[r * NP1 + m] = acc[c][m];
   }
+  __threadfence();
+  unsigned prev = 0;
+  if (lane == 0) prev = atomicAdd(a.row_done + j, 1u);
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if (prev != (unsigned)(a.G - 1)) return;
+  __threadfence();
+  const double* ypj = a.ypart + (long long)j * (a.nr * NP1);
+  const long long gstride = (long long)a.nrows * (a.nr * NP1);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int r = lane + 32 * c;
+    if (r < a.nr) {
+#pragma unroll
+      for (int m = 0; m < NP1; ++m) {
+        double s = 0.0;
+        for (int gg = 0; gg < a.G; ++gg) s += __ldcg(ypj + gg * gstride + r * NP1 + m);
+        a.y[(long long)(r * NP1 + m) * a.nrows + j] = s;
+      }
+    }
+  }
+  if (lane == 0) a.row_done[j] = 0u;
 }
 
 template <int NP1, int NC>
@@ -339,25 +375,6 @@ static void launch_mv_nc(const MvArgs& a, int nchunks, int blocks, cudaStream_t 
   constexpr size_t smem = MvStage<NP1 * NP1>::BYTES;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_matvec<NP1, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_matvec<NP1, NC><<<blocks, 32, smem, st>>>(a);
-}
-
-__global__ void k_reduce_out(const double* __restrict__ ypart, double* __restrict__ y, int M, int nrow,
-                             int G) {
-  // y[c*M + j] = sum_g ypart[g][j][c]; c = (block row)*NP1 + m2
-  __shared__ double tile[32][33];
-  const int c0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
-  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-    const int j = j0 + k, c = c0 + threadIdx.x;
-    double s = 0.0;
-    if (j < M && c < nrow)
-      for (int g = 0; g < G; ++g) s += ypart[((long long)g * M + j) * nrow + c];
-    tile[k][threadIdx.x] = s;
-  }
-  __syncthreads();
-  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-    const int c = c0 + k, j = j0 + threadIdx.x;
-    if (j < M && c < nrow) y[(long long)c * M + j] = tile[threadIdx.x][k];
-  }
 }
 
 }  // namespace tdb
@@ -374,6 +391,7 @@ struct TdbMatvecPlan {
   unsigned* d_mask = nullptr;
   double* d_xt = nullptr;
   double* d_ypart = nullptr;
+  unsigned* d_done = nullptr;
   double bytes = 0.0, flops = 0.0;
 };
 
@@ -384,6 +402,7 @@ extern "C" int tdb_matvec_plan_destroy(TdbMatvecPlan* p) {
   cudaFree(p->d_mask);
   cudaFree(p->d_xt);
   cudaFree(p->d_ypart);
+  cudaFree(p->d_done);
   cudaFree(p->d_xmap);
   delete p;
   return TDB_OK;
@@ -448,7 +467,11 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   p->bytes = bytes;
   p->flops = flops;
   // groups: enough warps to fill the chip on small meshes
-  const int want_warps = sys->ctx->num_sms * 48;
+  static const int warps_per_sm = [] {
+    const char* e = std::getenv("TDB_MV_WARPS_PER_SM");
+    return e ? std::max(1, std::atoi(e)) : 48;
+  }();
+  const int want_warps = sys->ctx->num_sms * warps_per_sm;
   int G = std::max(1, std::min(nt, (want_warps + NR - 1) / NR));
   G = std::min(G, 64);
   std::vector<int> gb(G + 1, nt);
@@ -492,6 +515,8 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   ALLOC_COPY(p->d_xt, (const double*)nullptr, (size_t)M * (nc + 1) * NP1, double);
   cudaMemsetAsync(p->d_xt, 0, (size_t)M * (nc + 1) * NP1 * sizeof(double), st);  // zero pads
   ALLOC_COPY(p->d_ypart, (const double*)nullptr, (size_t)G * NR * nr * NP1, double);
+  ALLOC_COPY(p->d_done, (const unsigned*)nullptr, (size_t)NR, unsigned);
+  cudaMemsetAsync(p->d_done, 0, (size_t)NR * sizeof(unsigned), st);
   if (d->x_map) ALLOC_COPY(p->d_xmap, reinterpret_cast<const long long*>(d->x_map), M, long long);
   p->xstride = d->x_map ? d->x_stride : M;
 #undef ALLOC_COPY
@@ -517,6 +542,7 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   a.xt = p->d_xt;
   a.xs = (nc + 1) * NP1;
   a.ypart = p->d_ypart;
+  a.row_done = p->d_done;
   *out = p;
   return TDB_OK;
 }
@@ -532,11 +558,12 @@ extern "C" int tdb_matvec(TdbMatvecPlan* p, const double* x, double* y) {
   TDB_REQUIRE(p && x && y, "NULL argument");
   const MvArgs& a = p->args;
   cudaStream_t st = p->sys->ctx->stream;
-  const int ncols = a.nc * a.NP1, nrows = a.nr * a.NP1;
+  const int ncols = a.nc * a.NP1;
   {
     dim3 blk(32, 8), grd((a.M + 31) / 32, (ncols + 31) / 32);
     k_transpose_in<<<grd, blk, 0, st>>>(x, p->d_xt, a.M, ncols, a.xs, p->d_xmap, p->xstride);
   }
+  p->args.y = y;
   {
     const long long warps = (long long)a.nrows * a.G;
     const int blocks = (int)warps;
@@ -547,10 +574,6 @@ extern "C" int tdb_matvec(TdbMatvecPlan* p, const double* x, double* y) {
       case 3: launch_mv_nc<3, 1>(a, nchunks, blocks, st); break;
       default: launch_mv_nc<4, 1>(a, nchunks, blocks, st); break;
     }
-  }
-  {
-    dim3 blk(32, 8), grd((a.nrows + 31) / 32, (nrows + 31) / 32);
-    k_reduce_out<<<grd, blk, 0, st>>>(p->d_ypart, y, a.nrows, nrows, a.G);
   }
   TDB_CUDA_CHECK(cudaGetLastError());
   return TDB_OK;
