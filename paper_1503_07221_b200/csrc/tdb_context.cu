@@ -89,6 +89,15 @@ int tdb_system_destroy(TdbSystem* sys) {
     cudaFree(f.slo);
     cudaFree(f.shi);
   }
+  for (auto& b : sys->bsr) {
+    cudaFree(b.col);
+    cudaFree(b.val);
+    cudaFree(b.rbptr);
+  }
+  cudaFree(sys->d_vperm);
+  cudaFree(sys->d_vinv);
+  cudaFree(sys->d_rperm);
+  cudaFree(sys->d_rinv);
   delete sys;
   return TDB_OK;
 }

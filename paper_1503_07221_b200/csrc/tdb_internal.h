@@ -50,6 +50,17 @@ struct FRange {
   int lo_cnt;  // s_lo | (cnt << 16)
 };
 
+// One family's stored blocks as 8 x 4 tiles (p = 0 tensor-core matvec): dofs in
+// Morton order (rows: the system's owned rows; columns: all vertices), tiles of a
+// (position, row block) contiguous and ordered by column block; values in the
+// DMMA m8n8k4 A-fragment order (lane = 4 * row + col).
+struct BsrStore {
+  long long ntiles = 0;
+  int32_t* col = nullptr;     // (ntiles,) column block
+  double* val = nullptr;      // (ntiles, 32)
+  int64_t* rbptr = nullptr;   // (npos * nRB + 1,)
+};
+
 struct FamilyStore {
   int npos = 0;
   long long nnz = 0;
@@ -92,5 +103,15 @@ struct TdbSystem {
   std::vector<tdb::FamilyStore> fam;
   std::vector<tdb::FamDev> famdev_host;
   tdb::FamDev* famdev = nullptr;
+  // Morton orders for the tensor-core matvec (built at create time):
+  // vperm[new] = old vertex, vinv[old] = new; rperm[new] = old local row, rinv[old] = new
+  std::vector<int> vperm, vinv, rperm, rinv;
+  int* d_vperm = nullptr;
+  int* d_vinv = nullptr;
+  int* d_rperm = nullptr;
+  int* d_rinv = nullptr;
+  int nRB = 0, nCB = 0;  // ceil(nrows / 8), ceil(V / 4)
+  std::vector<tdb::BsrStore> bsr;
+  bool bsr_built = false;
   TdbStats stats{};
 };

@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "tdb_bsr.h"
 #include "tdb_common.cuh"
 #include "tdb_internal.h"
 
@@ -393,6 +394,15 @@ struct TdbMatvecPlan {
   double* d_ypart = nullptr;
   unsigned* d_done = nullptr;
   double bytes = 0.0, flops = 0.0;
+  // p = 0 tensor-core path (tdb_bsr.cu)
+  bool bsr = false;
+  BsrMvArgs bargs{};
+  BsrFam* d_bfam = nullptr;
+  int* d_bgroups = nullptr;
+  long long* d_xmap_p = nullptr;  // permuted row l' -> offset of vertex vperm[l'] in x
+  double* d_xp = nullptr;
+  double* d_bypart = nullptr;
+  unsigned* d_bdone = nullptr;
 };
 
 extern "C" int tdb_matvec_plan_destroy(TdbMatvecPlan* p) {
@@ -404,6 +414,12 @@ extern "C" int tdb_matvec_plan_destroy(TdbMatvecPlan* p) {
   cudaFree(p->d_ypart);
   cudaFree(p->d_done);
   cudaFree(p->d_xmap);
+  cudaFree(p->d_bfam);
+  cudaFree(p->d_bgroups);
+  cudaFree(p->d_xmap_p);
+  cudaFree(p->d_xp);
+  cudaFree(p->d_bypart);
+  cudaFree(p->d_bdone);
   delete p;
   return TDB_OK;
 }
@@ -543,6 +559,97 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   a.xs = (nc + 1) * NP1;
   a.ypart = p->d_ypart;
   a.row_done = p->d_done;
+  // ---- p = 0: optional tensor-core BSR path (TDB_MV_BSR=1; measured slower than the
+  // CSR lanes-over-time kernel on configs 2 and 4) ----
+  static const bool use_bsr = std::getenv("TDB_MV_BSR") != nullptr && std::atoi(std::getenv("TDB_MV_BSR")) != 0;
+  if (NP1 == 1 && use_bsr) {
+    int rc = bsr_build(sys);
+    if (rc) {
+      tdb_matvec_plan_destroy(p);
+      return rc;
+    }
+    const int nRB = sys->nRB, nCB = sys->nCB;
+    // tiles per term (row blocks of its position)
+    std::vector<double> tcost_b(nt, 0.0);
+    std::vector<std::vector<int64_t>> rbp(sys->F);
+    for (int t = 0; t < nt; ++t) {
+      const int f = d->term_family[t], s_ = d->term_pos[t];
+      if (rbp[f].empty()) {
+        rbp[f].resize((size_t)sys->fam[f].npos * nRB + 1);
+        TDB_CUDA_CHECK(cudaMemcpy(rbp[f].data(), sys->bsr[f].rbptr, rbp[f].size() * sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost));
+      }
+      const double tiles = (double)(rbp[f][(size_t)(s_ + 1) * nRB] - rbp[f][(size_t)s_ * nRB]);
+      tcost_b[t] = tiles * (1.0 + (term_kt[4 * (size_t)t] < 0 ? (nr + 7) / 8 : 1));
+    }
+    // time tiles per CTA: the largest T in {8, 4, 2, 1} that still gives >= 2 CTAs per SM
+    const int ntile = (nr + 7) / 8;
+    int T = 8;
+    while (T > 1 && (long long)nRB * ((ntile + T - 1) / T) < 2LL * sys->ctx->num_sms) T /= 2;
+    const int KG = (ntile + T - 1) / T;
+    const int Gb = kBsrWarps;
+    std::vector<int> gbb(Gb + 1, nt);
+    {
+      double total = 0;
+      for (double v : tcost_b) total += v;
+      double acc_ = 0;
+      int g = 0;
+      gbb[0] = 0;
+      for (int t = 0; t < nt && g < Gb - 1; ++t) {
+        acc_ += tcost_b[t];
+        if (acc_ * Gb >= total * (g + 1)) gbb[++g] = t + 1;
+      }
+      for (int k = g + 1; k <= Gb; ++k) gbb[k] = nt;
+    }
+    std::vector<BsrFam> bf(sys->F);
+    for (int f = 0; f < sys->F; ++f) bf[f] = {sys->bsr[f].col, sys->bsr[f].val, sys->bsr[f].rbptr};
+    std::vector<long long> xmp(M);
+    for (int lp = 0; lp < M; ++lp) {
+      const int l = sys->vperm[lp];
+      xmp[lp] = d->x_map ? (long long)d->x_map[l] : (long long)l;
+    }
+    const int xs_b = nc + 8;
+    const size_t xp_n = (size_t)nCB * 4 * xs_b;
+#define ALLOC_COPY2(dst, src, n, T_)                                                               \
+  do {                                                                                             \
+    size_t nn = std::max<size_t>(1, (size_t)(n));                                                  \
+    if (cudaMalloc((void**)&(dst), nn * sizeof(T_)) != cudaSuccess) {                             \
+      tdb_matvec_plan_destroy(p);                                                                  \
+      set_error("matvec plan: cudaMalloc failed");                                                 \
+      return TDB_E_NOMEM;                                                                          \
+    }                                                                                              \
+    if ((n) > 0 && (src) != nullptr)                                                               \
+      cudaMemcpyAsync((dst), (src), (size_t)(n) * sizeof(T_), cudaMemcpyHostToDevice, st);         \
+  } while (0)
+    ALLOC_COPY2(p->d_bfam, bf.data(), sys->F, BsrFam);
+    ALLOC_COPY2(p->d_bgroups, gbb.data(), Gb + 1, int);
+    ALLOC_COPY2(p->d_xmap_p, xmp.data(), M, long long);
+    ALLOC_COPY2(p->d_xp, (const double*)nullptr, xp_n, double);
+    cudaMemsetAsync(p->d_xp, 0, xp_n * sizeof(double), st);
+#undef ALLOC_COPY2
+    TDB_CUDA_CHECK(cudaStreamSynchronize(st));
+    BsrMvArgs& b = p->bargs;
+    b.nrows = NR;
+    b.nRB = nRB;
+    b.KG = KG;
+    b.T = T;
+    b.rlo = d->rlo;
+    b.nr = nr;
+    b.clo = d->clo;
+    b.nc = nc;
+    b.words = d->words;
+    b.fam = p->d_bfam;
+    b.term_f = a.term_f;
+    b.term_s = a.term_s;
+    b.term_d = a.term_d;
+    b.term_mask = a.term_mask;
+    b.group_begin = p->d_bgroups;
+    b.rperm = sys->d_rperm;
+    b.xp = p->d_xp;
+    b.xs = xs_b;
+    p->bsr = true;
+    // stored bytes of the tile format (the canonical CSR figure stays in p->bytes)
+  }
   *out = p;
   return TDB_OK;
 }
@@ -559,6 +666,13 @@ extern "C" int tdb_matvec(TdbMatvecPlan* p, const double* x, double* y) {
   const MvArgs& a = p->args;
   cudaStream_t st = p->sys->ctx->stream;
   const int ncols = a.nc * a.NP1;
+  if (p->bsr) {
+    dim3 blk(32, 8), grd((a.M + 31) / 32, (ncols + 31) / 32);
+    k_transpose_in<<<grd, blk, 0, st>>>(x, p->d_xp, a.M, ncols, p->bargs.xs, p->d_xmap_p, p->xstride);
+    TDB_CUDA_CHECK(cudaGetLastError());
+    p->bargs.y = y;
+    return bsr_mv_launch(p->bargs, st);
+  }
   {
     dim3 blk(32, 8), grd((a.M + 31) / 32, (ncols + 31) / 32);
     k_transpose_in<<<grd, blk, 0, st>>>(x, p->d_xt, a.M, ncols, a.xs, p->d_xmap, p->xstride);
