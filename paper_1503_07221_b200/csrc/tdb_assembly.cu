@@ -406,6 +406,15 @@ __device__ __forceinline__ void warp_reduce_scatter(const double (&v)[N], int la
 // (psi_m, psi~_m) are the adjacent tables 2m, 2m+1: one 16-byte load per
 // Chebyshev coefficient for both.  Lanes of a warp evaluate r-sorted points, so
 // their subintervals idx are clustered and the loads coalesce to few wavefronts.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+
 struct XPow {
   double x, x2, x4, x8, x16;
 };
@@ -486,16 +495,16 @@ __device__ __forceinline__ void eval_pair(const double* __restrict__ cf, int tai
         b[k] = GLOBAL ? __ldg(tp + k * stride) : tp[k * stride];
 #endif
       }
+      // (psi, psi~) tails together: one packed fma.rn.f32x2 (FFMA2) per coefficient;
+      // each half is an IEEE fp32 FMA, so the result equals two scalar Horner chains
       const float xf = (float)X.x;
-      float ta = b[D - K].x, tb = b[D - K].y;
+      const float2 xx = make_float2(xf, xf);
+      float2 tt = b[D - K];
 #pragma unroll
-      for (int k = D - K - 1; k >= 0; --k) {
-        ta = fmaf(ta, xf, b[k].x);
-        tb = fmaf(tb, xf, b[k].y);
-      }
+      for (int k = D - K - 1; k >= 0; --k) tt = ffma2(tt, xx, b[k]);
       const double x7 = X.x4 * X.x2 * X.x;
-      v0 = fma(x7, (double)ta, v0);
-      v1 = fma(x7, (double)tb, v1);
+      v0 = fma(x7, (double)tt.x, v0);
+      v1 = fma(x7, (double)tt.y, v1);
     }
   }
 }
