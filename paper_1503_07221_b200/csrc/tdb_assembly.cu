@@ -1080,8 +1080,11 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s0, in
 // their union, per-position popcount prefixes; then one thread per union entry
 // (j, l) gathers its values for SC positions at a time and writes the entries
 // that are in each position's pattern.
+#ifndef TDB_FILL_MINB
+#define TDB_FILL_MINB 3
+#endif
 template <int NM>
-__global__ void k_pattern_fill(PatternArgs a) {
+__global__ void __launch_bounds__(256, TDB_FILL_MINB) k_pattern_fill(PatternArgs a) {
   constexpr int SC = NM >= 8 ? 1 : 8 / NM;
   extern __shared__ unsigned smem_u[];
   unsigned* bm = smem_u;                                                   // [s_count][words]
