@@ -11,8 +11,10 @@
 // final update uses only the k_done columns the reference would have used.
 //
 // Cycle state (doubles): see TDB_KS_* in include/tdb.h.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "tdb_common.cuh"
@@ -92,9 +94,150 @@ __global__ void k_krylov_flag(const double* st, double* err) {
   if (st[TDB_KS_BREAKDOWN] != 0.0 && st[TDB_KS_CONVERGED] == 0.0) *err = 1.0;
 }
 
+// One fused Arnoldi step after the matvec (thread-block cluster, DSMEM reductions):
+//   two classical Gram-Schmidt passes  h_p = V[0..k] w,  w -= V[0..k]^T h_p  (CGS2),
+//   hcol[0..k] = h_1 + h_2, hcol[k+1] = ||w||, then (optionally) the Givens step of
+//   k_krylov_givens and V[k+1] = w / ||w||.
+// Each CTA owns a contiguous slice of the vector; a partial sum is reduced
+// warp -> CTA (shared memory) -> cluster (every CTA reads all ranks' partials
+// through distributed shared memory in rank order), so every CTA holds the same
+// coefficients (deterministic, no atomics) and the step is one launch.
+constexpr int kArnThreads = 256;
+constexpr int kArnMaxK = 64;  // restart lengths up to 64
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(kArnThreads) k_krylov_arnoldi(const double* __restrict__ V, long long ldv,
+                                                               long long n, int k, double* __restrict__ w,
+                                                               double* hcol, double* st, double* H, int ldh,
+                                                               double* cs, double* sn, double* g,
+                                                               double* vnext) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int crank = (int)cl.block_rank(), csize = (int)cl.num_blocks();
+  constexpr int NW = kArnThreads / 32;
+  __shared__ double red[kArnMaxK + 1][NW];
+  __shared__ double cta[2][kArnMaxK + 1];  // double-buffered: pass p uses cta[p & 1]
+  __shared__ double h[kArnMaxK + 1], hs[kArnMaxK + 1];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const long long per = (n + csize - 1) / csize;
+  const long long lo = (long long)crank * per, hi = min(n, lo + per);
+  const int nj = k + 1;
+  for (int j = tid; j < nj; j += kArnThreads) hs[j] = 0.0;
+  // passes 0, 1: CGS; pass 2: the norm of w (nj = 1 "coefficient")
+  for (int pass = 0; pass < 3; ++pass) {
+    const int nc = pass < 2 ? nj : 1;
+    double* cb = cta[pass & 1];
+    for (int j = 0; j < nc; ++j) {
+      double loc = 0.0;
+      if (pass < 2) {
+        const double* vj = V + (long long)j * ldv;
+        for (long long i = lo + tid; i < hi; i += kArnThreads) loc = fma(vj[i], w[i], loc);
+      } else {
+        for (long long i = lo + tid; i < hi; i += kArnThreads) loc = fma(w[i], w[i], loc);
+      }
+      loc = warp_sum(loc);
+      if (lane == 0) red[j][wid] = loc;
+    }
+    __syncthreads();
+    for (int j = tid; j < nc; j += kArnThreads) {
+      double s_ = 0.0;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) s_ += red[j][q];
+      cb[j] = s_;
+    }
+    cl.sync();
+    for (int j = tid; j < nc; j += kArnThreads) {
+      double s_ = 0.0;
+      for (int r = 0; r < csize; ++r) s_ += *cl.map_shared_rank(cb + j, r);
+      h[j] = s_;
+      if (pass < 2) hs[j] += s_;
+    }
+    __syncthreads();
+    if (pass < 2)
+      for (long long i = lo + tid; i < hi; i += kArnThreads) {
+        double acc = 0.0;
+        for (int j = 0; j < nj; ++j) acc = fma(V[(long long)j * ldv + i], h[j], acc);
+        w[i] -= acc;
+      }
+    __syncthreads();
+  }
+  const double hk = sqrt(h[0]);
+  if (crank == 0 && tid == 0) {
+    for (int j = 0; j < nj; ++j) hcol[j] = hs[j];
+    hcol[nj] = hk;
+  }
+  if (H != nullptr && crank == 0 && tid == 0) {
+    // the Givens step, exactly as k_krylov_givens (same thread, after hcol)
+    if (st[TDB_KS_DONE] == 0.0) {
+      double* col = H + k;
+      for (int i = 0; i <= k + 1; ++i) col[i * ldh] = i <= k ? hs[i] : hk;
+      for (int j = 0; j < k; ++j) {
+        const double a = col[j * ldh], b = col[(j + 1) * ldh];
+        const double t = cs[j] * a + sn[j] * b;
+        col[(j + 1) * ldh] = -sn[j] * a + cs[j] * b;
+        col[j * ldh] = t;
+      }
+      const double hkk = col[k * ldh], hk1 = col[(k + 1) * ldh];
+      const double denom = hypot(hkk, hk1);
+      cs[k] = denom > 0.0 ? hkk / denom : 1.0;
+      sn[k] = denom > 0.0 ? hk1 / denom : 0.0;
+      col[k * ldh] = denom;
+      g[k + 1] = -sn[k] * g[k];
+      g[k] = cs[k] * g[k];
+      col[(k + 1) * ldh] = 0.0;
+      st[TDB_KS_KDONE] = (double)(k + 1);
+      if (fabs(g[k + 1]) <= st[TDB_KS_TOL_ABS]) {
+        st[TDB_KS_DONE] = 1.0;
+        st[TDB_KS_CONVERGED] = 1.0;
+      } else if (hk <= 1e-14 * st[TDB_KS_BETA]) {
+        st[TDB_KS_DONE] = 1.0;
+        st[TDB_KS_BREAKDOWN] = 1.0;
+      }
+    }
+  }
+  if (vnext != nullptr) {
+    const double inv = 1.0 / hk;
+    for (long long i = lo + tid; i < hi; i += kArnThreads) vnext[i] = w[i] * inv;
+  }
+  cl.sync();  // peers may still read this CTA's partials
+}
+
 }  // namespace
 
 extern "C" {
+
+int tdb_krylov_arnoldi(const double* V, int64_t ldv, int64_t n, int32_t k, double* w, double* hcol, double* state,
+                       double* H, int32_t ldh, double* cs, double* sn, double* g, double* vnext, void* stream) {
+  TDB_REQUIRE(V && w && hcol && n > 0 && k >= 0 && k < kArnMaxK, "krylov_arnoldi: bad argument");
+  TDB_REQUIRE(H == nullptr || (state && cs && sn && g && ldh > k), "krylov_arnoldi: bad Givens arguments");
+  static int csize = [] {
+    cudaFuncSetAttribute(k_krylov_arnoldi, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return 16;
+  }();
+  // cluster of up to 16 CTAs (one per SM), at least ~2K elements per CTA
+  int cls = (int)std::min<long long>(csize, std::max<long long>(1, n / 2048));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cls);
+  cfg.blockDim = dim3(kArnThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cls;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TDB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_krylov_arnoldi, V, (long long)ldv, (long long)n, (int)k, w, hcol, state,
+                                    H, (int)ldh, cs, sn, g, vnext));
+  return TDB_OK;
+}
+
 
 int tdb_krylov_init(double* state, const double* beta, double tol_rel, double* g, void* stream) {
   TDB_REQUIRE(state && beta && g, "krylov_init: NULL argument");

@@ -232,13 +232,22 @@ def _gmres_cycle_raw(apply_A, b, x0, m, tol_abs, precond, history):
             z = precond(V[k])
             Z[k] = z
         w = apply_A(z).clone()
-        # modified Gram-Schmidt: h_j computed and subtracted one vector at a time
-        for j in range(k + 1):
-            torch.dot(V[j], w, out=hcol[j])
-            if _COMM.size > 1:
-                _COMM.allreduce_(hcol[j : j + 1])
-            w.addcmul_(V[j], hcol[j : j + 1], value=-1.0)
-        hcol[k + 1] = _norm(w)
+        if w.is_cuda and _COMM.size == 1 and k < 63 and w.dtype == torch.float64:
+            # CGS2 orthogonalisation + norm in one cluster kernel (tdb_krylov_arnoldi)
+            from . import _lib
+
+            _lib.check(_lib.LIB.tdb_krylov_arnoldi(_ptr(V), n, n, k, _ptr(w), _ptr(hcol), None, None, 0, None,
+                                                   None, None, None,
+                                                   C_void(torch.cuda.current_stream(dev).cuda_stream)),
+                       "krylov_arnoldi")
+        else:
+            # modified Gram-Schmidt: h_j computed and subtracted one vector at a time
+            for j in range(k + 1):
+                torch.dot(V[j], w, out=hcol[j])
+                if _COMM.size > 1:
+                    _COMM.allreduce_(hcol[j : j + 1])
+                w.addcmul_(V[j], hcol[j : j + 1], value=-1.0)
+            hcol[k + 1] = _norm(w)
         col = hcol[: k + 2].cpu().numpy()
         H[: k + 2, k] = col
         Hraw[: k + 2, k] = col
@@ -292,15 +301,24 @@ def _cycle_fixed_device(apply_A, b: torch.Tensor, m: int, tol: float, precond, e
     g = torch.zeros(m + 1, dtype=dt, device=dev)
     hcol = torch.empty(m + 1, dtype=dt, device=dev)
     V = torch.empty((m, n), dtype=dt, device=dev)
+    if n == 0:
+        return torch.zeros_like(b)
     Z = V if precond is None else torch.empty((m, n), dtype=dt, device=dev)
     beta = _norm(b).reshape(1)
     L = _lib.LIB
     _lib.check(L.tdb_krylov_init(_ptr(st), _ptr(beta), float(tol), _ptr(g), stream), "krylov_init")
     torch.div(b, beta, out=V[0])
+    fused = _COMM.size == 1 and m < 64
     for k in range(m):
         if precond is not None:
             Z[k].copy_(precond(V[k]))
-        w = apply_A(Z[k]).clone()
+        w = apply_A(Z[k])
+        if fused:  # CGS2 + norm + Givens + V[k+1] = w / ||w|| in one cluster kernel
+            vnext = _ptr(V[k + 1]) if k + 1 < m else None
+            _lib.check(L.tdb_krylov_arnoldi(_ptr(V), n, n, k, _ptr(w), _ptr(hcol), _ptr(st), _ptr(H), m, _ptr(cs),
+                                            _ptr(sn), _ptr(g), vnext, stream), "krylov_arnoldi")
+            continue
+        w = w.clone()
         Vk = V[: k + 1]
         h = _gemv_t(Vk, w)
         w.sub_(torch.mv(Vk.T, h))
