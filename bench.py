@@ -414,16 +414,29 @@ def main():
             bl = torch.as_tensor(b).to(dev)
         cfgS = S.SolverConfig(method="fgmres-recursive", restart=50, tol=1e-5, max_iter=2000,
                               recursion_depth=2, inner_iterations=(2, 10))
+        # preconditioner setup (untimed in `seconds`, reported as `setup_seconds`): matvec
+        # plans of every sub-range + CUDA-graph capture of one preconditioner application
         barrier(world)
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        x, hist = S.fgmres(lambda v: A_mv.matvec(v), bl, cfgS, precond=S.recursive_preconditioner(A_mv, cfgS))
+        prec = S.recursive_preconditioner(A_mv, cfgS)
+        for _ in range(3):
+            prec(bl)
+        torch.cuda.synchronize(dev)
+        t_setup = max_over_ranks(world, time.perf_counter() - t0, dev)
+        barrier(world)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        x, hist = S.fgmres(lambda v: A_mv.matvec(v), bl, cfgS, precond=prec)
         torch.cuda.synchronize(dev)
         ts = max_over_ranks(world, time.perf_counter() - t0, dev)
         S.set_comm(None)
         solve = {"method": "FGMRES(50, 2(2,10)) recursive block preconditioner", "tol": 1e-5,
-                 "seconds": ts, "iterations": len(hist), "final_rel_residual": float(hist[-1]),
-                 "rhs": "Gaussian-pulse plane wave (sigma 0.2, t0 1.0), assemble_rhs (host)"}
+                 "seconds": ts, "setup_seconds": t_setup, "iterations": len(hist),
+                 "final_rel_residual": float(hist[-1]),
+                 "rhs": "Gaussian-pulse plane wave (sigma 0.2, t0 1.0), assemble_rhs (host)",
+                 "note": "x0 = 0, device vectors; setup = sub-range matvec plans + graph capture of the "
+                         "preconditioner (reusable across right-hand sides)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
