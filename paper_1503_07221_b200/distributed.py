@@ -37,9 +37,12 @@ def partition_rows(mesh, nparts: int):
     owner_tri = np.full(V, E, dtype=np.int64)
     for a in range(3):
         np.minimum.at(owner_tri, tri[:, a], np.arange(E))
-    bounds = [(E * r) // nparts for r in range(nparts + 1)]
-    tri_rank = np.minimum(np.searchsorted(bounds, owner_tri, side="right") - 1, nparts - 1)
-    rows = [np.flatnonzero(tri_rank == r).astype(np.int64) for r in range(nparts)]
+    # vertices in owner-triangle order (refinement numbers a parent's children
+    # consecutively, so runs of this order are spatially compact), cut into equal
+    # counts: every rank owns V / nparts rows (+-1)
+    order = np.argsort(owner_tri, kind="stable")
+    cuts = [(V * r) // nparts for r in range(nparts + 1)]
+    rows = [np.sort(order[cuts[r]:cuts[r + 1]]).astype(np.int64) for r in range(nparts)]
     off, ids = mesh.star_csr
     tests = []
     for r in range(nparts):
