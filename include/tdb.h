@@ -141,6 +141,9 @@ typedef struct TdbContext TdbContext;
 typedef struct TdbSystem TdbSystem;
 
 int tdb_abi_version(void);
+/* Device blocks freed by destroyed systems / plans are cached for reuse (up to
+ * 8 GB); this returns them to the driver. */
+int tdb_release_cached_memory(void);
 /* Measured FP64 FMA throughput of the device (TFLOP/s, 2 flops per DFMA):
  * a dependent-chain microbenchmark over all SMs, best of `repeats`. */
 int tdb_fp64_peak(TdbContext* ctx, int repeats, double* tflops);

@@ -101,6 +101,7 @@ def _load():
     P = C.c_void_p
     sig = {
         "tdb_abi_version": (i32, []),
+        "tdb_release_cached_memory": (i32, []),
         "tdb_fp64_peak": (i32, [P, C.c_int, C.POINTER(C.c_double)]),
         "tdb_last_error": (C.c_char_p, []),
         "tdb_device_count": (i32, [C.POINTER(C.c_int)]),
@@ -146,7 +147,7 @@ EXPORTED = (
     "tdb_system_family_device", "tdb_matvec_plan_create", "tdb_matvec_plan_destroy", "tdb_matvec",
     "tdb_matvec_plan_work", "tdb_tri_distance_bounds", "tdb_system_create", "tdb_system_run",
     "tdb_fp64_peak", "tdb_krylov_init", "tdb_krylov_givens", "tdb_krylov_update", "tdb_krylov_flag",
-    "tdb_krylov_arnoldi",
+    "tdb_krylov_arnoldi", "tdb_release_cached_memory",
 )
 
 # TDB_KS_* cycle-state slots (include/tdb.h)

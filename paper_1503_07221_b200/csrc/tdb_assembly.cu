@@ -29,6 +29,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <vector>
@@ -1181,8 +1182,11 @@ namespace {
 
 struct Dev {
   void* p = nullptr;
-  ~Dev() {
-    if (p) cudaFree(p);
+  ~Dev() {  // scoped scratch: make sure no kernel still uses it before it is recycled
+    if (p) {
+      cudaDeviceSynchronize();
+      dev_free(p);
+    }
   }
   template <typename T>
   T* as() const { return static_cast<T*>(p); }
@@ -1191,7 +1195,7 @@ struct Dev {
 template <typename T>
 int dalloc(T** out, size_t n) {
   if (n == 0) n = 1;
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(out), n * sizeof(T));
+  cudaError_t e = dev_malloc(reinterpret_cast<void**>(out), n * sizeof(T));
   if (e != cudaSuccess) {
     set_error(std::string("cudaMalloc(") + std::to_string(n * sizeof(T)) + " B): " +
               cudaGetErrorString(e));
@@ -1320,25 +1324,25 @@ struct AsmWorkspace {
   bool events = false;
   long long launch_count = 0;
   ~AsmWorkspace() {
-    cudaFree(blob);
-    for (void* p : rule_mem) cudaFree(p);
-    cudaFree(d_nitems_case);
-    cudaFree(frange);
-    cudaFree(units);
-    cudaFree(slots);
-    cudaFree(nitems);
-    cudaFree(pcase);
-    cudaFree(items);
-    cudaFree(part);
-    cudaFree(counters);
-    cudaFree(cub_tmp);
-    cudaFree(tt);
-    cudaFree(ey_map);
-    cudaFree(rows);
-    cudaFree(owned);
+    dev_free(blob);
+    for (void* p : rule_mem) dev_free(p);
+    dev_free(d_nitems_case);
+    dev_free(frange);
+    dev_free(units);
+    dev_free(slots);
+    dev_free(nitems);
+    dev_free(pcase);
+    dev_free(items);
+    dev_free(part);
+    dev_free(counters);
+    dev_free(cub_tmp);
+    dev_free(tt);
+    dev_free(ey_map);
+    dev_free(rows);
+    dev_free(owned);
     for (auto& L : launches) {
-      cudaFree(L.d_fam);
-      cudaFree(L.d_blob);
+      dev_free(L.d_fam);
+      dev_free(L.d_blob);
     }
     if (events)
       for (auto& e : ev) cudaEventDestroy(e);
@@ -1736,6 +1740,12 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
   if ((rc = dupload(&sys->star_off, soff.data(), V + 1, st))) return rc;
   if ((rc = dupload(&sys->star_ids, sids.data(), 3 * E, st))) return rc;
 
+  const bool verbose = std::getenv("TDB_VERBOSE") != nullptr;
+  auto clk = [] { return std::chrono::steady_clock::now(); };
+  auto ms_since = [](std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  };
+  auto t_fam = clk();
   // ---- families ----
   sys->fam.resize(F);
   sys->famdev_host.resize(F);
@@ -1820,6 +1830,8 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
   if ((rc = dupload(&ws->blob, blob_all.data(), blob_all.size(), st))) return rc;
   for (int f = 0; f < F; ++f) sys->famdev_host[f].coeffs = ws->blob + ws->fam_blob_off[f];
 
+  if (verbose) std::fprintf(stderr, "tdb: create families (tables, splits) %.2f ms\n", ms_since(t_fam));
+  auto t_rules = clk();
   // ---- rules ----
   for (int c = 0; c < 4; ++c) {
     const TdbRule& r = desc->rules[c];
@@ -2009,6 +2021,8 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
   }
   TDB_REQUIRE(ws->nrows > 0, "assemble: no rows to assemble");
 
+  if (verbose) std::fprintf(stderr, "tdb: create rules+launches+rows %.2f ms\n", ms_since(t_rules));
+  auto t_size = clk();
   // ---- plan buffers and sizes ----
   ws->E2 = (long long)ws->Et * E;
   const long long E2 = ws->E2;
@@ -2081,6 +2095,7 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
   sys->stats.units = units;
   sys->stats.items = ws->total_items;
   sys->stats.nnz_total = nnz_total;
+  if (verbose) std::fprintf(stderr, "tdb: create sizing (plan, pattern counts, allocations) %.2f ms\n", ms_since(t_size));
   return TDB_OK;
 }
 

@@ -1,7 +1,11 @@
 // Context / system lifecycle and the C ABI wrappers (include/tdb.h).
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
 #include <string>
+#include <unordered_map>
+#include <vector>
 
 #include "tdb_common.cuh"
 #include "tdb_internal.h"
@@ -9,6 +13,89 @@
 namespace tdb {
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+// ---- caching device allocator --------------------------------------------
+// Repeated assemble/destroy cycles (the public API builds a fresh system per
+// call) would otherwise pay cudaMalloc/cudaFree of GB-sized workspaces every
+// time.  Freed blocks are kept per device (size-rounded, at most kPoolCap bytes
+// cached) and reused best-fit; an allocation failure releases the cache and
+// retries.  Callers release blocks only after their stream is idle.
+namespace {
+constexpr size_t kPoolCap = 8ull << 30;
+struct Pool {
+  std::mutex mu;
+  std::unordered_map<void*, std::pair<size_t, int>> live;  // ptr -> (bytes, device)
+  std::map<std::pair<int, size_t>, std::vector<void*>> cached;  // (device, bytes) -> blocks
+  size_t cached_bytes = 0;
+};
+Pool& pool() {
+  static Pool* p = new Pool();  // never destroyed (may be used during process teardown)
+  return *p;
+}
+size_t round_bytes(size_t b) {
+  if (b <= (1u << 20)) return (b + 511) & ~size_t(511);
+  return (b + (2u << 20) - 1) & ~size_t((2u << 20) - 1);
+}
+void trim_locked(Pool& P) {
+  for (auto& kv : P.cached)
+    for (void* q : kv.second) cudaFree(q);
+  P.cached.clear();
+  P.cached_bytes = 0;
+}
+}  // namespace
+
+cudaError_t dev_malloc(void** out, size_t bytes) {
+  Pool& P = pool();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const size_t b = round_bytes(bytes == 0 ? 1 : bytes);
+  std::lock_guard<std::mutex> g(P.mu);
+  auto it = P.cached.lower_bound({dev, b});
+  if (it != P.cached.end() && it->first.first == dev && it->first.second <= b + b / 4 && !it->second.empty()) {
+    void* q = it->second.back();
+    const size_t have = it->first.second;
+    it->second.pop_back();
+    if (it->second.empty()) P.cached.erase(it);
+    P.cached_bytes -= have;
+    P.live[q] = {have, dev};
+    *out = q;
+    return cudaSuccess;
+  }
+  cudaError_t e = cudaMalloc(out, b);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    trim_locked(P);
+    e = cudaMalloc(out, b);
+  }
+  if (e == cudaSuccess) P.live[*out] = {b, dev};
+  return e;
+}
+
+void dev_free(void* q) {
+  if (!q) return;
+  Pool& P = pool();
+  std::lock_guard<std::mutex> g(P.mu);
+  auto it = P.live.find(q);
+  if (it == P.live.end()) {  // not ours
+    cudaFree(q);
+    return;
+  }
+  const size_t b = it->second.first;
+  const int dev = it->second.second;
+  P.live.erase(it);
+  if (P.cached_bytes + b > kPoolCap) {
+    cudaFree(q);
+    return;
+  }
+  P.cached[{dev, b}].push_back(q);
+  P.cached_bytes += b;
+}
+
+void dev_pool_trim() {
+  Pool& P = pool();
+  std::lock_guard<std::mutex> g(P.mu);
+  trim_locked(P);
+}
 }  // namespace tdb
 
 int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDesc* desc,
@@ -23,6 +110,11 @@ using namespace tdb;
 extern "C" {
 
 int tdb_abi_version(void) { return TDB_ABI_VERSION; }
+
+int tdb_release_cached_memory(void) {
+  dev_pool_trim();
+  return TDB_OK;
+}
 
 const char* tdb_last_error(void) { return g_last_error.c_str(); }
 
@@ -71,33 +163,36 @@ int tdb_ctx_set_stream(TdbContext* ctx, void* stream) {
 
 int tdb_system_destroy(TdbSystem* sys) {
   if (!sys) return TDB_OK;
-  if (sys->ctx) cudaSetDevice(sys->ctx->device);
+  if (sys->ctx) {
+    cudaSetDevice(sys->ctx->device);
+    cudaStreamSynchronize(sys->ctx->stream);  // blocks go back to the pool
+  }
   tdb_workspace_free(sys);
-  cudaFree(sys->corners);
-  cudaFree(sys->a2);
-  cudaFree(sys->normals);
-  cudaFree(sys->curls);
-  cudaFree(sys->tri);
-  cudaFree(sys->star_off);
-  cudaFree(sys->star_ids);
-  cudaFree(sys->famdev);
+  dev_free(sys->corners);
+  dev_free(sys->a2);
+  dev_free(sys->normals);
+  dev_free(sys->curls);
+  dev_free(sys->tri);
+  dev_free(sys->star_off);
+  dev_free(sys->star_ids);
+  dev_free(sys->famdev);
   for (auto& f : sys->fam) {
-    cudaFree(f.indptr);
-    cudaFree(f.indices);
-    cudaFree(f.data);
-    cudaFree(f.delta);
-    cudaFree(f.slo);
-    cudaFree(f.shi);
+    dev_free(f.indptr);
+    dev_free(f.indices);
+    dev_free(f.data);
+    dev_free(f.delta);
+    dev_free(f.slo);
+    dev_free(f.shi);
   }
   for (auto& b : sys->bsr) {
-    cudaFree(b.col);
-    cudaFree(b.val);
-    cudaFree(b.rbptr);
+    dev_free(b.col);
+    dev_free(b.val);
+    dev_free(b.rbptr);
   }
-  cudaFree(sys->d_vperm);
-  cudaFree(sys->d_vinv);
-  cudaFree(sys->d_rperm);
-  cudaFree(sys->d_rinv);
+  dev_free(sys->d_vperm);
+  dev_free(sys->d_vinv);
+  dev_free(sys->d_rperm);
+  dev_free(sys->d_rinv);
   delete sys;
   return TDB_OK;
 }

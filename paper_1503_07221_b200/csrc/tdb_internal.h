@@ -76,6 +76,14 @@ struct FamilyStore {
 
 }  // namespace tdb
 
+namespace tdb {
+// caching device allocator (tdb_context.cu): freed blocks are reused by later
+// systems / plans; release only after the owning stream is idle
+cudaError_t dev_malloc(void** out, size_t bytes);
+void dev_free(void* p);
+void dev_pool_trim();
+}  // namespace tdb
+
 struct TdbContext {
   int device = 0;
   cudaStream_t stream = nullptr;

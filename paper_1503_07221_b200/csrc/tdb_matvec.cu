@@ -407,19 +407,20 @@ struct TdbMatvecPlan {
 
 extern "C" int tdb_matvec_plan_destroy(TdbMatvecPlan* p) {
   if (!p) return TDB_OK;
-  cudaFree(p->d_fam);
-  cudaFree(p->d_ints);
-  cudaFree(p->d_mask);
-  cudaFree(p->d_xt);
-  cudaFree(p->d_ypart);
-  cudaFree(p->d_done);
-  cudaFree(p->d_xmap);
-  cudaFree(p->d_bfam);
-  cudaFree(p->d_bgroups);
-  cudaFree(p->d_xmap_p);
-  cudaFree(p->d_xp);
-  cudaFree(p->d_bypart);
-  cudaFree(p->d_bdone);
+  cudaDeviceSynchronize();  // the system may already be gone: no p->sys access here
+  dev_free(p->d_fam);
+  dev_free(p->d_ints);
+  dev_free(p->d_mask);
+  dev_free(p->d_xt);
+  dev_free(p->d_ypart);
+  dev_free(p->d_done);
+  dev_free(p->d_xmap);
+  dev_free(p->d_bfam);
+  dev_free(p->d_bgroups);
+  dev_free(p->d_xmap_p);
+  dev_free(p->d_xp);
+  dev_free(p->d_bypart);
+  dev_free(p->d_bdone);
   delete p;
   return TDB_OK;
 }
@@ -517,7 +518,7 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
 #define ALLOC_COPY(dst, src, n, T)                                                                 \
   do {                                                                                             \
     size_t nn = std::max<size_t>(1, (size_t)(n));                                                  \
-    if (cudaMalloc((void**)&(dst), nn * sizeof(T)) != cudaSuccess) {                              \
+    if (dev_malloc((void**)&(dst), nn * sizeof(T)) != cudaSuccess) {                              \
       tdb_matvec_plan_destroy(p);                                                                  \
       set_error("matvec plan: cudaMalloc failed");                                                 \
       return TDB_E_NOMEM;                                                                          \
@@ -613,7 +614,7 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
 #define ALLOC_COPY2(dst, src, n, T_)                                                               \
   do {                                                                                             \
     size_t nn = std::max<size_t>(1, (size_t)(n));                                                  \
-    if (cudaMalloc((void**)&(dst), nn * sizeof(T_)) != cudaSuccess) {                             \
+    if (dev_malloc((void**)&(dst), nn * sizeof(T_)) != cudaSuccess) {                             \
       tdb_matvec_plan_destroy(p);                                                                  \
       set_error("matvec plan: cudaMalloc failed");                                                 \
       return TDB_E_NOMEM;                                                                          \
