@@ -163,7 +163,13 @@ class AssemblyPlan:
 
 
 def _touching_tmax(mesh: SurfaceMesh):
-    """Largest corner distance of every touching pair, per case (mesh.py:366-369)."""
+    """Largest corner distance of every touching pair, per case (mesh.py:366-369).
+
+    Mesh-derived, so it is cached on the mesh object (the reference caches its
+    distance bounds on the mesh the same way, mesh.py:146-153)."""
+    cached = getattr(mesh, "_tdb_touching_tmax", None)
+    if cached is not None:
+        return cached
     out = {}
     for case, (ex, ey, _, _) in touching_pairs(mesh).items():
         if len(ex) == 0:
@@ -171,6 +177,10 @@ def _touching_tmax(mesh: SurfaceMesh):
             continue
         diff = mesh.corners[ex][:, :, None, :] - mesh.corners[ey][:, None, :, :]
         out[case] = np.linalg.norm(diff, axis=3).max(axis=(1, 2))
+    try:
+        object.__setattr__(mesh, "_tdb_touching_tmax", out)  # frozen dataclass: like cached_property
+    except (AttributeError, TypeError):
+        pass
     return out
 
 
