@@ -962,6 +962,8 @@ struct RowStar {  // star of the test vertex j, cached in shared memory per CTA
   int k[kMaxStar];   // pair-row index of e
   int t[kMaxStar][3];
   int pj[kMaxStar];  // local position of j in triangle e
+  double ny[kMaxStar][3];  // normal of e
+  double cy[kMaxStar][3];  // curl of the hat function of j on e
 };
 
 // Values of CSR entry (j, l) at the positions s0 .. s0 + SC - 1 (clipped to s_end):
@@ -988,14 +990,14 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s0, in
   unsigned deferred[kDefer];    // (case << 16) | (kx << 8) | ky, in (ex, ey) order
   int nd = 0;
   bool overflow = false;
-  auto contribute = [&](int ex, int ey, int ky, int cs, const FRange& fr) {
+  // nx / cx: normal of ex and curl of l's hat function on ex (loaded once per ex)
+  auto contribute = [&](int ex, int ey, int ky, int cs, const FRange& fr, int pl, const double (&nx)[3],
+                        const double (&cx)[3]) {
     const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
     const long long Pp = (long long)rs.k[ky] * a.E + ex;
     const long long slot0 = a.pair_base[Pp] + fr.foff - s_lo;
-    int ca = rs.pj[ky], cb = 0;
-    const int* tx = a.tri + 3 * ex;
-    cb = (tx[0] == l) ? 0 : ((tx[1] == l) ? 1 : 2);
-    const int pj = ca, pl = cb;
+    int ca = rs.pj[ky], cb = pl;
+    const int pj = ca;
     if (cs != TDB_CASE_REGULAR) {  // chart permutations of the regularised rules
       int lx[3], ly[3];
       pair_topology(a.tri, ex, ey, lx, ly);
@@ -1005,12 +1007,8 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s0, in
         cb = (lx[t] == pl) ? t : cb;
       }
     }
-    const double* nx = a.normals + 3 * (long long)ex;
-    const double* ny = a.normals + 3 * (long long)ey;
-    const double nd_ = nx[0] * ny[0] + nx[1] * ny[1] + nx[2] * ny[2];
-    const double* cyv = a.curls + 9 * (long long)ey + 3 * pj;
-    const double* cxv = a.curls + 9 * (long long)ex + 3 * pl;
-    const double cd = cyv[0] * cxv[0] + cyv[1] * cxv[1] + cyv[2] * cxv[2];
+    const double nd_ = nx[0] * rs.ny[ky][0] + nx[1] * rs.ny[ky][1] + nx[2] * rs.ny[ky][2];
+    const double cd = rs.cy[ky][0] * cx[0] + rs.cy[ky][1] * cx[1] + rs.cy[ky][2] * cx[2];
     const int ab = 3 * ca + cb;
 #pragma unroll
     for (int u = 0; u < SC; ++u) {
@@ -1027,9 +1025,21 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s0, in
       }
     }
   };
+  auto ex_data = [&](int ex, int& pl, double (&nx)[3], double (&cx)[3]) {
+    const int* tx = a.tri + 3 * ex;
+    pl = (tx[0] == l) ? 0 : ((tx[1] == l) ? 1 : 2);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      nx[c] = a.normals[3 * (long long)ex + c];
+      cx[c] = a.curls[9 * (long long)ex + 3 * pl + c];
+    }
+  };
   for (int kx = lb; kx < le; ++kx) {
     const int ex = a.star_ids[kx];
     const int x0 = a.tri[3 * ex], x1 = a.tri[3 * ex + 1], x2 = a.tri[3 * ex + 2];
+    int pl;
+    double nx[3], cx[3];
+    ex_data(ex, pl, nx, cx);
     for (int ky = 0; ky < rs.n; ++ky) {
       const int ey = rs.e[ky];
       const FRange fr = a.frange[(long long)rs.k[ky] * a.E + ex];
@@ -1045,7 +1055,7 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s0, in
         cs = nsh == 0 ? TDB_CASE_REGULAR : (nsh == 2 ? TDB_CASE_EDGE : TDB_CASE_VERTEX);
       }
       if (cs == TDB_CASE_REGULAR) {
-        contribute(ex, ey, ky, cs, fr);
+        contribute(ex, ey, ky, cs, fr, pl, nx, cx);
       } else if (nd < kDefer) {
         deferred[nd++] = ((unsigned)cs << 16) | ((unsigned)(kx - lb) << 8) | (unsigned)ky;
       } else {
@@ -1059,7 +1069,10 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s0, in
         if ((int)(deferred[d] >> 16) != cr) continue;
         const int kxl = (deferred[d] >> 8) & 0xff, ky = deferred[d] & 0xff;
         const int ex = a.star_ids[lb + kxl], ey = rs.e[ky];
-        contribute(ex, ey, ky, cr, a.frange[(long long)rs.k[ky] * a.E + ex]);
+        int pl;
+        double nx[3], cx[3];
+        ex_data(ex, pl, nx, cx);
+        contribute(ex, ey, ky, cr, a.frange[(long long)rs.k[ky] * a.E + ex], pl, nx, cx);
       }
     } else {  // very high valence: rescan the combos of this case in order
       for (int kx = lb; kx < le; ++kx) {
@@ -1070,7 +1083,10 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s0, in
           const FRange fr = a.frange[(long long)rs.k[ky] * a.E + ex];
           const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
           if (s1 <= s_lo || s0 >= s_lo + cnt) continue;
-          contribute(ex, ey, ky, cr, fr);
+          int pl;
+          double nx[3], cx[3];
+          ex_data(ex, pl, nx, cx);
+          contribute(ex, ey, ky, cr, fr, pl, nx, cx);
         }
       }
     }
@@ -1104,6 +1120,10 @@ __global__ void __launch_bounds__(256, TDB_FILL_MINB) k_pattern_fill(PatternArgs
       for (int t = 0; t < 3; ++t) {
         rs.t[k][t] = a.tri[3 * ey + t];
         if (rs.t[k][t] == j) rs.pj[k] = t;
+      }
+      for (int c = 0; c < 3; ++c) {
+        rs.ny[k][c] = a.normals[3 * (long long)ey + c];
+        rs.cy[k][c] = a.curls[9 * (long long)ey + 3 * rs.pj[k] + c];
       }
     }
   }
