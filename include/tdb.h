@@ -18,6 +18,8 @@
  *   tdb_matvec (+ plan)           <- block_system.py:180-216 matvec(x, rows, cols)
  *   tdb_krylov_*                  <- solvers.py:189-222 (_gmres_cycle_raw's Givens
  *                                    bookkeeping and final update, on the device)
+ *   tdb_dlp_eval                  <- potential.py:53-126 eval_double_layer /
+ *                                    eval_total_field
  */
 #ifndef TDB_H_
 #define TDB_H_
@@ -260,6 +262,17 @@ int tdb_krylov_flag(const double* state, double* err, void* stream);
  * receives w / ||w||.  Replaces the MGS loop of solvers.py:189-194. k < 64. */
 int tdb_krylov_arnoldi(const double* V, int64_t ldv, int64_t n, int32_t k, double* w, double* hcol, double* state,
                        double* H, int32_t ldh, double* cs, double* sn, double* g, double* vnext, void* stream);
+
+/* ---- retarded double-layer potential (potential.py:53-126) ---------------
+ * out[t * npts + x] = u(points[x], times[t]) for the density coefficients
+ * coeffs (L = N (p+1) rows of M vertex values, the solver's layout); the far /
+ * near triangle rules are (x1, x2) chart nodes + weights of triangle_rule(q).
+ * Host buffers; computed on the context's device.  Replaces
+ * tdbem.potential.eval_double_layer for a batch of points and times. */
+int tdb_dlp_eval(TdbContext* ctx, const TdbMesh* mesh, double T, int32_t N, int32_t p, const double* coeffs,
+                 int64_t npts, const double* points, int64_t ntimes, const double* times, int32_t nq_far,
+                 const double* far_xhat, const double* far_w, int32_t nq_near, const double* near_xhat,
+                 const double* near_w, double* out);
 
 #ifdef __cplusplus
 }

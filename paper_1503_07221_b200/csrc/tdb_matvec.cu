@@ -87,7 +87,10 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 
 template <int NM>
 struct MvStage {
-  static constexpr int CAP = NM <= 1 ? 256 : NM <= 4 ? 128 : 64;  // entries per buffer
+#ifndef TDB_MV_CAP1
+#define TDB_MV_CAP1 256
+#endif
+  static constexpr int CAP = NM <= 1 ? TDB_MV_CAP1 : NM <= 4 ? 128 : 64;  // entries per buffer
   static constexpr size_t BYTES = 2 * (size_t)CAP * (4 + 8 * NM);
 };
 
