@@ -20,6 +20,7 @@
  *                                    bookkeeping and final update, on the device)
  *   tdb_dlp_eval                  <- potential.py:53-126 eval_double_layer /
  *                                    eval_total_field
+ *   tdb_rhs_*                     <- assembly.py:314-355 assemble_rhs (contraction)
  */
 #ifndef TDB_H_
 #define TDB_H_
@@ -273,6 +274,17 @@ int tdb_dlp_eval(TdbContext* ctx, const TdbMesh* mesh, double T, int32_t N, int3
                  int64_t npts, const double* points, int64_t ntimes, const double* times, int32_t nq_far,
                  const double* far_xhat, const double* far_w, int32_t nq_near, const double* near_xhat,
                  const double* near_w, double* out);
+
+/* ---- right-hand side contraction (assembly.py:314-355) -------------------
+ * Device pointers.  G: rows j0 .. j0+nj-1 of the datum g(X_p, t_j) at the P
+ * regular-rule points (node-major, row stride P).  Stage 1 writes
+ * H[j][l] = sum_{q in vptr[l]..vptr[l+1]} vw[q] G[j][vpts[q]] (vertex gather of the
+ * shape-weighted rule points); stage 2 writes out[k*M + l] = sum_{j in
+ * kptr[k]..kptr[k+1]} w[j] H[j][l] (the time nodes of basis k are contiguous). */
+int tdb_rhs_vertex_gather(const double* G, int64_t j0, int64_t nj, int64_t P, const int64_t* vptr, const int32_t* vpts,
+                          const double* vw, int64_t M, double* H, void* stream);
+int tdb_rhs_time_sum(const double* H, const int64_t* kptr, const double* w, int64_t L, int64_t M, double* out,
+                     void* stream);
 
 #ifdef __cplusplus
 }

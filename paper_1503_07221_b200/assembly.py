@@ -429,14 +429,27 @@ def tri_distance_bounds(mesh: SurfaceMesh, rows=None, ctx: _lib.Context | None =
     return tmin, tmax
 
 
-def assemble_rhs(mesh: SurfaceMesh, grid: TimeGrid, g, config: QuadratureConfig = QuadratureConfig()):
+def assemble_rhs(mesh: SurfaceMesh, grid: TimeGrid, g, config: QuadratureConfig = QuadratureConfig(),
+                 device: bool | None = None):
     """Load vector b[(k-1) M + l] = int int g(x, t) phi_l(x) bdot_k(t) dx dt (host).
 
     Restates assembly.py:314-355 of the reference: regular q_reg triangle rule in
     space; in time, Gauss panels of 2(p+4) points over quarter steps of each
-    basis function's support.  g(X (n,3), t) -> (n,).  (the
-    device version is the next step.)
+    basis function's support.  g(X (n,3), t) -> (n,).
+
+    A datum with a ``device_eval(X, t)`` method (torch tensors: X (P, 3), t (n,) ->
+    (n, P)), such as gaussian_pulse_neumann's, is integrated on the GPU
+    (``_assemble_rhs_device``: csrc/tdb_rhs.cu) unless device=False; any other
+    callable is a host (numpy) callback and is integrated on the host exactly as
+    the reference does (bit-identical, tests/golden/rhs.npz).
     """
+    if device is not False and hasattr(g, "device_eval"):
+        import torch
+
+        if torch.cuda.is_available():
+            return _assemble_rhs_device(mesh, grid, g, config)
+        if device:
+            raise RuntimeError("assemble_rhs(device=True): no CUDA device")
     from .quadrature import gauss_rule, triangle_rule
     from .temporal_basis import basis_b, flat_index, support_interval
 
@@ -471,17 +484,109 @@ def assemble_rhs(mesh: SurfaceMesh, grid: TimeGrid, g, config: QuadratureConfig 
     return out
 
 
-def gaussian_pulse_neumann(mesh: SurfaceMesh, sigma: float = 0.2, t0: float = 1.0):
+def _rhs_time_nodes(grid: TimeGrid):
+    """Time nodes / weights of every basis function, in the reference's arithmetic
+    (assembly.py:339-349): (kptr (L+1,), t (n,), w (n,)); zero weights are kept."""
+    from .quadrature import gauss_rule
+    from .temporal_basis import basis_b, flat_index, support_interval
+
+    xg, wg = gauss_rule(2 * (grid.p + 4))
+    ts, ws, kptr = [], [], [0]
+    for k in range(1, grid.L + 1):
+        idx = flat_index(grid, (k - 1) // (grid.p + 1) + 1, (k - 1) % (grid.p + 1))
+        lo, hi = support_interval(grid, idx.timestep)
+        nhalf = max(1, round((hi - lo) / (0.25 * grid.dt)))
+        for panel in range(nhalf):
+            a = lo + (hi - lo) * panel / nhalf
+            b = lo + (hi - lo) * (panel + 1) / nhalf
+            tq = 0.5 * (a + b) + 0.5 * (b - a) * xg
+            ts.append(tq)
+            ws.append(0.5 * (b - a) * wg * basis_b(grid, idx, tq, deriv=1))
+        kptr.append(kptr[-1] + nhalf * len(xg))
+    return np.asarray(kptr, dtype=np.int64), np.concatenate(ts), np.concatenate(ws)
+
+
+def _assemble_rhs_device(mesh: SurfaceMesh, grid: TimeGrid, g, config: QuadratureConfig = QuadratureConfig()):
+    """assemble_rhs on the GPU: g.device_eval at every (time node, rule point) in
+    node chunks, vertex gather + per-basis time sum in csrc/tdb_rhs.cu."""
+    import ctypes
+
+    import torch
+
+    from .quadrature import triangle_rule
+
+    mesh, grid = as_product_inputs(mesh, grid)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    m = mesh.num_vertices
+    pts, w = triangle_rule(config.q_reg)
+    c = mesh.corners
+    X = (c[:, None, 0, :] + pts[None, :, 0, None] * (c[:, 1] - c[:, 0])[:, None, :]
+         + pts[None, :, 1, None] * (c[:, 2] - c[:, 1])[:, None, :]).reshape(-1, 3)
+    wx = (w[None, :] * 2.0 * mesh.areas[:, None]).reshape(-1)
+    sh = np.column_stack([1.0 - pts[:, 0], pts[:, 0] - pts[:, 1], pts[:, 1]])
+    shw = np.tile(sh, (mesh.num_triangles, 1)) * wx[:, None]          # (P, 3)
+    dofs = np.repeat(mesh.triangles, len(pts), axis=0)                # (P, 3)
+    P = len(X)
+    # vertex -> (rule point, weight) CSR, points ascending (element order)
+    vert = dofs.reshape(-1)
+    order = np.argsort(vert, kind="stable")
+    vptr = np.zeros(m + 1, dtype=np.int64)
+    np.add.at(vptr, vert + 1, 1)
+    vptr = np.cumsum(vptr)
+    vpts = (order // 3).astype(np.int32)
+    vw = shw.reshape(-1)[order]
+    kptr, ts, ws = _rhs_time_nodes(grid)
+    nn = len(ts)
+    T = lambda a, dt=torch.float64: torch.as_tensor(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
+    Xd, vptr_d, vpts_d, vw_d = T(X), T(vptr, torch.int64), T(vpts, torch.int32), T(vw)
+    ts_d, ws_d, kptr_d = T(ts), T(ws), T(kptr, torch.int64)
+    H = torch.empty((nn, m), dtype=torch.float64, device=dev)
+    out = torch.empty(grid.L * m, dtype=torch.float64, device=dev)
+    stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    p = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    chunk = max(1, min(nn, (1 << 27) // max(P, 1)))  # <= 1 GiB of datum values per chunk
+    for j0 in range(0, nn, chunk):
+        nj = min(chunk, nn - j0)
+        G = g.device_eval(Xd, ts_d[j0 : j0 + nj]).to(torch.float64).contiguous()
+        _lib.check(_lib.LIB.tdb_rhs_vertex_gather(p(G), j0, nj, P, p(vptr_d), p(vpts_d), p(vw_d), m, p(H), stream),
+                   "rhs_vertex_gather")
+    _lib.check(_lib.LIB.tdb_rhs_time_sum(p(H), p(kptr_d), p(ws_d), grid.L, m, p(out), stream), "rhs_time_sum")
+    return out.cpu().numpy()
+
+
+class GaussianPulseNeumann:
     """g = -d_n u_inc for u_inc = f(t - t0 - (z - z_min)), f(s) = exp(-s^2/(2 sigma^2))
     (plane wave along +z with a Gaussian envelope; g = n_z f'(s)).
-    Points are the triangle-rule points in element order, as assemble_rhs passes them."""
-    zmin = float(mesh.vertices[:, 2].min())
-    nz = mesh.normals[:, 2]
+    Points are the triangle-rule points in element order, as assemble_rhs passes them.
+    Callable on numpy arrays (host, the reference's callback contract) and, through
+    device_eval, on CUDA tensors for a whole batch of times."""
 
-    def g(X, t):
-        nq = len(X) // mesh.num_triangles
-        s = t - t0 - (X[:, 2] - zmin)
+    def __init__(self, mesh: SurfaceMesh, sigma: float = 0.2, t0: float = 1.0):
+        self.zmin = float(mesh.vertices[:, 2].min())
+        self.nz = mesh.normals[:, 2]
+        self.E = mesh.num_triangles
+        self.sigma, self.t0 = sigma, t0
+        self._nz_dev = None
+
+    def __call__(self, X, t):
+        nq = len(X) // self.E
+        sigma = self.sigma
+        s = t - self.t0 - (X[:, 2] - self.zmin)
         f = np.exp(-s * s / (2.0 * sigma * sigma))
-        return np.repeat(nz, nq) * (-s / sigma**2) * f
+        return np.repeat(self.nz, nq) * (-s / sigma**2) * f
 
-    return g
+    def device_eval(self, X, t):
+        import torch
+
+        nq = X.shape[0] // self.E
+        if self._nz_dev is None or self._nz_dev.device != X.device or self._nz_dev.numel() != X.shape[0]:
+            self._nz_dev = torch.as_tensor(np.repeat(self.nz, nq)).to(X.device)
+        sigma = self.sigma
+        s = t[:, None] - self.t0 - (X[None, :, 2] - self.zmin)
+        f = torch.exp(-s * s / (2.0 * sigma * sigma))
+        return self._nz_dev[None, :] * (-s / sigma**2) * f
+
+
+def gaussian_pulse_neumann(mesh: SurfaceMesh, sigma: float = 0.2, t0: float = 1.0):
+    """The benchmark datum (SURVEY 8d RHS) as a GaussianPulseNeumann."""
+    return GaussianPulseNeumann(mesh, sigma, t0)
