@@ -21,6 +21,7 @@
  *   tdb_dlp_eval                  <- potential.py:53-126 eval_double_layer /
  *                                    eval_total_field
  *   tdb_rhs_*                     <- assembly.py:314-355 assemble_rhs (contraction)
+ *   tdb_table_node_values         <- kernel_weights.py:243-295 PrototypeTables.build
  */
 #ifndef TDB_H_
 #define TDB_H_
@@ -285,6 +286,17 @@ int tdb_rhs_vertex_gather(const double* G, int64_t j0, int64_t nj, int64_t P, co
                           const double* vw, int64_t M, double* H, void* stream);
 int tdb_rhs_time_sum(const double* H, const int64_t* kptr, const double* w, int64_t L, int64_t M, double* out,
                      void* stream);
+
+/* ---- psi / psi~ prototype tables (kernel_weights.py:243-295) --------------
+ * Node integrals of every table subinterval: for subinterval s (kinds[2s] =
+ * ansatz kind, kinds[2s+1] = test kind: 0 first, 1 inner, 2 last; a0w[2s],
+ * a0w[2s+1] = start, width) and Lobatto node n, out[(((s*2 + v)*(p+1) + m1)*(p+1)
+ * + m2)*nnodes + n] = the v = 0 (psi: b_i'') / v = 1 (psi~: b_i) integral against
+ * the test basis' time derivative over the panels pptr[s]..pptr[s+1] (5 doubles
+ * each: c0, s0, c1, s1, n_split; ends c + s*alpha).  Host buffers. */
+int tdb_table_node_values(TdbContext* ctx, double dt, int32_t p, int32_t nsub, const int32_t* kinds, const double* a0w,
+                          int32_t nnodes, const double* nodes, const int32_t* pptr, const double* panels, int32_t nq,
+                          const double* xq, const double* wq, double* out);
 
 #ifdef __cplusplus
 }

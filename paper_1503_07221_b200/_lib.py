@@ -129,6 +129,8 @@ def _load():
         "tdb_krylov_update": (i32, [P, P, P, i64, i64, P, P, i32, P, i32, P]),
         "tdb_krylov_flag": (i32, [P, P, P]),
         "tdb_krylov_arnoldi": (i32, [P, i64, i64, i32, P, P, P, P, i32, P, P, P, P, P]),
+        "tdb_table_node_values": (i32, [P, C.c_double, i32, i32, i32p, f64p, i32, f64p, i32p, f64p, i32, f64p, f64p,
+                                        f64p]),
         "tdb_rhs_vertex_gather": (i32, [P, i64, i64, i64, P, P, P, i64, P, P]),
         "tdb_rhs_time_sum": (i32, [P, P, P, i64, i64, P, P]),
         "tdb_dlp_eval": (i32, [P, C.POINTER(TdbMesh), C.c_double, i32, i32, f64p, i64, f64p, i64, f64p, i32,
@@ -152,7 +154,7 @@ EXPORTED = (
     "tdb_matvec_plan_work", "tdb_tri_distance_bounds", "tdb_system_create", "tdb_system_run",
     "tdb_fp64_peak", "tdb_krylov_init", "tdb_krylov_givens", "tdb_krylov_update", "tdb_krylov_flag",
     "tdb_krylov_arnoldi", "tdb_release_cached_memory", "tdb_dlp_eval",
-    "tdb_rhs_vertex_gather", "tdb_rhs_time_sum",
+    "tdb_rhs_vertex_gather", "tdb_rhs_time_sum", "tdb_table_node_values",
 )
 
 # TDB_KS_* cycle-state slots (include/tdb.h)

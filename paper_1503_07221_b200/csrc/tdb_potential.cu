@@ -18,89 +18,13 @@
 #include <cmath>
 #include <vector>
 
+#include "tdb_basis.cuh"
 #include "tdb_common.cuh"
 #include "tdb_geometry.cuh"
 #include "tdb_internal.h"
 
 namespace tdb {
 namespace {
-
-constexpr double kTClamp = 1.0 - 1e-14;                    // temporal_basis.py:47
-constexpr double kCErf = 1.1283791670955125738961589031;  // 2 / sqrt(pi)
-
-// smooth step f and f' (temporal_basis.py:105-130)
-__device__ __forceinline__ void cutoff01(double t, double& f0, double& f1) {
-  const double tc = fmin(fmax(t, -kTClamp), kTClamp);
-  const double s = atanh(tc);
-  const double g = exp(-4.0 * s * s);
-  f0 = t >= 1.0 ? 1.0 : (t <= -1.0 ? 0.0 : 0.5 * erf(2.0 * s) + 0.5);
-  const double q = 1.0 - tc * tc;
-  f1 = (fabs(t) < 1.0 && g > 0.0) ? kCErf * g / q : 0.0;
-}
-
-// P_m, P_m' (temporal_basis.py:133-148, Bonnet)
-__device__ __forceinline__ void legendre01(int m, double x, double& P, double& D) {
-  double p0 = 1.0, d0 = 0.0;
-  if (m == 0) {
-    P = p0;
-    D = d0;
-    return;
-  }
-  double p1 = x, d1 = 1.0;
-  for (int k = 2; k <= m; ++k) {
-    const double a = (2.0 * k - 1.0) / k, b = (k - 1.0) / k;
-    const double p2 = a * x * p1 - b * p0;
-    const double d2 = a * (p1 + x * d1) - b * d0;
-    p0 = p1;
-    d0 = d1;
-    p1 = p2;
-    d1 = d2;
-  }
-  P = p1;
-  D = d1;
-}
-
-// b and b' of order m of the canonical prototype of `kind` at offset u
-// (temporal_basis.py:178-260); kind 0 first, 1 inner, 2 last
-__device__ void basis01(int kind, int m, double dt, double u, double& b0, double& b1) {
-  b0 = b1 = 0.0;
-  if (kind == 1) {
-    if (u <= 0.0 || u >= 2.0 * dt) return;
-    const double c = 2.0 / dt;
-    double r0, r1;
-    if (u <= dt) {
-      double f0, f1;
-      cutoff01(c * u - 1.0, f0, f1);
-      r0 = f0;
-      r1 = f1 * c;
-    } else {
-      double f0, f1;
-      cutoff01(c * (u - dt) - 1.0, f0, f1);
-      r0 = 1.0 - f0;
-      r1 = -(f1 * c);
-    }
-    double P, D;
-    legendre01(m, u / dt - 1.0, P, D);
-    b0 = r0 * P;
-    b1 = r1 * P + r0 * D / dt;
-    return;
-  }
-  const double c = 2.0 / dt, x = c * u - 1.0;
-  double P, D, f0, f1;
-  legendre01(m, x, P, D);
-  cutoff01(x, f0, f1);
-  if (kind == 2) {
-    if (u <= 0.0 || u > dt) return;
-    b0 = f0 * P;
-    b1 = c * (f1 * P + f0 * D);
-    return;
-  }
-  if (u <= 0.0 || u >= dt) return;
-  const double g0 = 1.0 - f0, g1 = -c * f1;
-  const double q0 = (u / dt) * (u / dt), q1 = 2.0 * u / (dt * dt);
-  b0 = 8.0 * g0 * q0 * P;
-  b1 = 8.0 * (g1 * q0 * P + g0 * q1 * P + g0 * q0 * D * c);
-}
 
 struct DlpArgs {
   int E, M, N, p;
@@ -159,8 +83,8 @@ __global__ void __launch_bounds__(kDlpThreads) k_dlp(DlpArgs a) {
         for (int m = 0; m < np1; ++m) {
           const double* al = a.alpha + (long long)((k - 1) * np1 + m) * a.M;
           const double dof = sh0 * al[v0] + sh1 * al[v1] + sh2 * al[v2];
-          double b0, b1;
-          basis01(kind, m, dt, tret - o, b0, b1);
+          double b0, b1, b2;
+          basis012(kind, m, dt, tret - o, b0, b1, b2);
           phi = fma(b0, dof, phi);
           phit = fma(b1, dof, phit);
         }

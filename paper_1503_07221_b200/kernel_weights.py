@@ -212,6 +212,64 @@ class PrototypeTables:
                 out[1] += np.einsum("inq,knq->ikn", d0, test)
         return out
 
+    def build_device(self, ctx=None) -> "PrototypeTables":
+        """Same tables with the node integrals evaluated on the GPU (csrc/tdb_tables.cu):
+        the panel structure is decided here per subinterval exactly as in build();
+        the values agree with the host build to rounding (~1e-15 of the table max)."""
+        from . import _lib
+
+        grid = self.grid
+        p = grid.p
+        dt = grid.dt
+        nodes, D = lobatto_transform(self.deg)
+        xq, wq = np.polynomial.legendre.leggauss(self.nq)
+        kind_id = {k: i for i, k in enumerate(KINDS)}
+        kinds, a0w, pptr, panels, fams = [], [], [0], [], []
+        for kind_i in KINDS:
+            for kind_k in KINDS:
+                dom = table_domain(grid, kind_i, kind_k)
+                if dom is None or dom[1] <= dom[0]:
+                    for tilde in (True, False):
+                        for m1 in range(p + 1):
+                            for m2 in range(p + 1):
+                                self.tables[(tilde, kind_i, kind_k, m1, m2)] = None
+                    continue
+                lo, hi = dom
+                boundary = not (kind_i == KIND_INNER and kind_k == KIND_INNER)
+                per = self.n_per_step_boundary if boundary else self.n_per_step
+                n_sub = max(1, round((hi - lo) / grid.dt * per))
+                width = (hi - lo) / n_sub
+                fams.append((kind_i, kind_k, lo, hi, n_sub, len(kinds)))
+                for ks in range(n_sub):
+                    a0 = lo + ks * width
+                    a_mid = a0 + 0.5 * width
+                    pl, at = self._panels(kind_i, kind_k, a_mid)
+                    for e0, e1 in pl:
+                        panels.append((e0[0], e0[1], e1[0], e1[1],
+                                       float(max(1, math.ceil(4.0 * (at(e1) - at(e0)) / dt)))))
+                    kinds.append((kind_id[kind_i], kind_id[kind_k]))
+                    a0w.append((a0, width))
+                    pptr.append(len(panels))
+        nsub = len(kinds)
+        out = np.empty((nsub, 2, p + 1, p + 1, len(nodes)))
+        ctx = ctx or _lib.default_context()
+        arr = dict(kinds=np.ascontiguousarray(kinds, dtype=np.int32), a0w=_lib.f64(a0w), nodes=_lib.f64(nodes),
+                   pptr=np.ascontiguousarray(pptr, dtype=np.int32), panels=_lib.f64(panels), xq=_lib.f64(xq),
+                   wq=_lib.f64(wq))
+        _lib.check(_lib.LIB.tdb_table_node_values(
+            ctx.handle, float(dt), int(p), int(nsub), _lib.ptr(arr["kinds"], _lib.C.c_int32), _lib.ptr(arr["a0w"]),
+            len(nodes), _lib.ptr(arr["nodes"]), _lib.ptr(arr["pptr"], _lib.C.c_int32), _lib.ptr(arr["panels"]),
+            len(xq), _lib.ptr(arr["xq"]), _lib.ptr(arr["wq"]), _lib.ptr(out)), "table_node_values")
+        for kind_i, kind_k, lo, hi, n_sub, s0 in fams:
+            vals = np.moveaxis(out[s0 : s0 + n_sub], 0, 3)  # (2, p+1, p+1, n_sub, nodes)
+            coeffs = np.einsum("ij,vabkj->vabki", D, vals)
+            pairs = [(m1, m2) for m1 in range(p + 1) for m2 in range(p + 1)
+                     if not (kind_i == KIND_INNER and kind_k == KIND_INNER and m1 > m2)]
+            for m1, m2 in pairs:
+                self.tables[(False, kind_i, kind_k, m1, m2)] = PiecewiseCheb(lo, hi, coeffs[0, m1, m2])
+                self.tables[(True, kind_i, kind_k, m1, m2)] = PiecewiseCheb(lo, hi, coeffs[1, m1, m2])
+        return self
+
     def build(self) -> "PrototypeTables":
         grid = self.grid
         p = grid.p
@@ -274,11 +332,24 @@ def build_tables(grid: TimeGrid, **kwargs) -> PrototypeTables:
 _CACHE: dict = {}
 
 
-def tables_for(grid: TimeGrid) -> PrototypeTables:
-    """Default-parameter tables, cached by (dt, p) (independent of N)."""
-    key = (round(grid.dt, 15), grid.p)
+def _device_ok() -> bool:
+    try:
+        import torch
+
+        return bool(torch.cuda.is_available())
+    except ImportError:
+        return False
+
+
+def tables_for(grid: TimeGrid, device: bool | None = None) -> PrototypeTables:
+    """Default-parameter tables, cached by (dt, p) (independent of N).
+
+    device=None: built on the GPU when one is visible (build_device), else on the
+    host (build: bit-identical to the reference's tables)."""
+    use_dev = _device_ok() if device is None else bool(device)
+    key = (round(grid.dt, 15), grid.p, use_dev)
     if key not in _CACHE:
-        _CACHE[key] = build_tables(grid)
+        _CACHE[key] = PrototypeTables(grid).build_device() if use_dev else build_tables(grid)
     return _CACHE[key]
 
 
