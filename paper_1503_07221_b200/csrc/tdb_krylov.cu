@@ -132,16 +132,29 @@ __global__ void __launch_bounds__(kArnThreads) k_krylov_arnoldi(const double* __
   for (int pass = 0; pass < 3; ++pass) {
     const int nc = pass < 2 ? nj : 1;
     double* cb = cta[pass & 1];
-    for (int j = 0; j < nc; ++j) {
-      double loc = 0.0;
+    // up to 8 coefficients per sweep of the slice (independent accumulators and
+    // warp reductions: the dependent-latency chain is one sweep, not k + 1)
+    for (int jb = 0; jb < nc; jb += 8) {
+      double loc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) loc[u] = 0.0;
       if (pass < 2) {
-        const double* vj = V + (long long)j * ldv;
-        for (long long i = lo + tid; i < hi; i += kArnThreads) loc = fma(vj[i], w[i], loc);
+        const double* vb = V + (long long)jb * ldv;
+        const int nu = min(8, nc - jb);
+        for (long long i = lo + tid; i < hi; i += kArnThreads) {
+          const double wi = w[i];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (u < nu) loc[u] = fma(vb[(long long)u * ldv + i], wi, loc[u]);
+        }
       } else {
-        for (long long i = lo + tid; i < hi; i += kArnThreads) loc = fma(w[i], w[i], loc);
+        for (long long i = lo + tid; i < hi; i += kArnThreads) loc[0] = fma(w[i], w[i], loc[0]);
       }
-      loc = warp_sum(loc);
-      if (lane == 0) red[j][wid] = loc;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double r_ = warp_sum(loc[u]);
+        if (lane == 0 && jb + u < nc) red[jb + u][wid] = r_;
+      }
     }
     __syncthreads();
     for (int j = tid; j < nc; j += kArnThreads) {
