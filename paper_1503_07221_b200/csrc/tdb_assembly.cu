@@ -928,11 +928,11 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s0, in
   int nd = 0;
   bool overflow = false;
   // nx / cx: normal of ex and curl of l's hat function on ex (loaded once per ex)
-  auto contribute = [&](int ex, int ey, int ky, int cs, const FRange& fr, int pl, const double (&nx)[3],
-                        const double (&cx)[3]) {
+  // slot0 = pair_base of (ky, ex) + fr.foff - s_lo, i.e. the partial slot of position 0
+  auto contribute_at = [&](int ex, int ey, int ky, int cs, const FRange& fr, long long pbase, int pl,
+                           const double (&nx)[3], const double (&cx)[3]) {
     const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
-    const long long Pp = (long long)rs.k[ky] * a.E + ex;
-    const long long slot0 = a.pair_base[Pp] + fr.foff - s_lo;
+    const long long slot0 = pbase + fr.foff - s_lo;
     int ca = rs.pj[ky], cb = pl;
     const int pj = ca;
     if (cs != TDB_CASE_REGULAR) {  // chart permutations of the regularised rules
@@ -947,20 +947,37 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s0, in
     const double nd_ = nx[0] * rs.ny[ky][0] + nx[1] * rs.ny[ky][1] + nx[2] * rs.ny[ky][2];
     const double cd = rs.cy[ky][0] * cx[0] + rs.cy[ky][1] * cx[1] + rs.cy[ky][2] * cx[2];
     const int ab = 3 * ca + cb;
+    // all partial loads of the chunk first (independent, in flight together), then
+    // the compensated sums in position order
+    double pa[SC][NM], pc[SC][NM];
+    bool ok[SC];
 #pragma unroll
     for (int u = 0; u < SC; ++u) {
       const int s = s0 + u;
-      if (s >= s1 || s < s_lo || s >= s_lo + cnt) continue;
-      const double* pv = a.part + (slot0 + s) * a.nacc;
+      ok[u] = !(s >= s1 || s < s_lo || s >= s_lo + cnt);
+      const double* pv = a.part + (slot0 + (ok[u] ? s : s_lo)) * a.nacc;
 #pragma unroll
       for (int m = 0; m < NM; ++m) {
-        const double v = nd_ * pv[10 * m + ab] + cd * pv[10 * m + 9];
+        pa[u][m] = ok[u] ? __ldg(pv + 10 * m + ab) : 0.0;
+        pc[u][m] = ok[u] ? __ldg(pv + 10 * m + 9) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < SC; ++u) {
+      if (!ok[u]) continue;
+#pragma unroll
+      for (int m = 0; m < NM; ++m) {
+        const double v = nd_ * pa[u][m] + cd * pc[u][m];
         const double y = v - comp[u][m];
         const double t = sum[u][m] + y;
         comp[u][m] = (t - sum[u][m]) - y;
         sum[u][m] = t;
       }
     }
+  };
+  auto contribute = [&](int ex, int ey, int ky, int cs, const FRange& fr, int pl, const double (&nx)[3],
+                        const double (&cx)[3]) {
+    contribute_at(ex, ey, ky, cs, fr, a.pair_base[(long long)rs.k[ky] * a.E + ex], pl, nx, cx);
   };
   auto ex_data = [&](int ex, int& pl, double (&nx)[3], double (&cx)[3]) {
     const int* tx = a.tri + 3 * ex;
@@ -977,26 +994,53 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s0, in
     int pl;
     double nx[3], cx[3];
     ex_data(ex, pl, nx, cx);
-    for (int ky = 0; ky < rs.n; ++ky) {
-      const int ey = rs.e[ky];
-      const FRange fr = a.frange[(long long)rs.k[ky] * a.E + ex];
-      const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
-      if (s1 <= s_lo || s0 >= s_lo + cnt) continue;
-      int cs;
-      if (ex == ey) {
-        cs = TDB_CASE_COINCIDENT;
-      } else {
-        const int nsh = (x0 == rs.t[ky][0]) + (x0 == rs.t[ky][1]) + (x0 == rs.t[ky][2]) +
-                        (x1 == rs.t[ky][0]) + (x1 == rs.t[ky][1]) + (x1 == rs.t[ky][2]) +
-                        (x2 == rs.t[ky][0]) + (x2 == rs.t[ky][1]) + (x2 == rs.t[ky][2]);
-        cs = nsh == 0 ? TDB_CASE_REGULAR : (nsh == 2 ? TDB_CASE_EDGE : TDB_CASE_VERTEX);
+    // the combos (ex, star(j)) in batches of kFB: admissible ranges, then the
+    // partial-slot bases of the regular ones, loaded before any is used
+#ifndef TDB_FILL_FB
+#define TDB_FILL_FB 2
+#endif
+    constexpr int kFB = TDB_FILL_FB;
+    for (int kb = 0; kb < rs.n; kb += kFB) {
+      FRange frs[kFB];
+#pragma unroll
+      for (int q = 0; q < kFB; ++q) {
+        frs[q].foff = 0;
+        frs[q].lo_cnt = 0;
+        if (kb + q < rs.n) frs[q] = a.frange[(long long)rs.k[kb + q] * a.E + ex];
       }
-      if (cs == TDB_CASE_REGULAR) {
-        contribute(ex, ey, ky, cs, fr, pl, nx, cx);
-      } else if (nd < kDefer) {
-        deferred[nd++] = ((unsigned)cs << 16) | ((unsigned)(kx - lb) << 8) | (unsigned)ky;
-      } else {
-        overflow = true;
+      int csq[kFB];
+      long long pbq[kFB];
+#pragma unroll
+      for (int q = 0; q < kFB; ++q) {
+        const int ky = kb + q;
+        const int cnt = frs[q].lo_cnt >> 16, s_lo = frs[q].lo_cnt & 0xffff;
+        csq[q] = -1;  // no contribution to this chunk
+        pbq[q] = 0;
+        if (ky >= rs.n || s1 <= s_lo || s0 >= s_lo + cnt) continue;
+        const int ey = rs.e[ky];
+        int cs;
+        if (ex == ey) {
+          cs = TDB_CASE_COINCIDENT;
+        } else {
+          const int nsh = (x0 == rs.t[ky][0]) + (x0 == rs.t[ky][1]) + (x0 == rs.t[ky][2]) +
+                          (x1 == rs.t[ky][0]) + (x1 == rs.t[ky][1]) + (x1 == rs.t[ky][2]) +
+                          (x2 == rs.t[ky][0]) + (x2 == rs.t[ky][1]) + (x2 == rs.t[ky][2]);
+          cs = nsh == 0 ? TDB_CASE_REGULAR : (nsh == 2 ? TDB_CASE_EDGE : TDB_CASE_VERTEX);
+        }
+        csq[q] = cs;
+        if (cs == TDB_CASE_REGULAR) pbq[q] = a.pair_base[(long long)rs.k[ky] * a.E + ex];
+      }
+#pragma unroll
+      for (int q = 0; q < kFB; ++q) {
+        const int ky = kb + q, cs = csq[q];
+        if (cs < 0) continue;
+        if (cs == TDB_CASE_REGULAR) {
+          contribute_at(ex, rs.e[ky], ky, cs, frs[q], pbq[q], pl, nx, cx);
+        } else if (nd < kDefer) {
+          deferred[nd++] = ((unsigned)cs << 16) | ((unsigned)(kx - lb) << 8) | (unsigned)ky;
+        } else {
+          overflow = true;
+        }
       }
     }
   }

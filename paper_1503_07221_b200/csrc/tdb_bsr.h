@@ -32,6 +32,26 @@ struct BsrMvArgs {
   double* y;
 };
 
+// Toeplitz-ordered tiles of one family (tdb_tbsr.cu)
+struct TbsrMvArgs {
+  int nRB, G, ntg, TT, npos;
+  int nrows, nr;
+  const int32_t* col;
+  const int32_t* pos;
+  const double* val;
+  const int64_t* rbptr;
+  const int* off_tab;        // [ntg][npos][8 (g)][TT] column offset in xp (nc = zero column)
+  const unsigned* act_tab;   // [ntg][npos] active time tiles of the position's term
+  const int* rperm;
+  const double* xp;          // [nCB*4][xs] permuted, transposed x
+  int xs;
+  double* ypart;             // [nRB * ntg][G][TT * 64]
+  double* y;
+};
+
+int tbsr_build(TdbSystem* sys, int f);
+int tbsr_mv_launch(const TbsrMvArgs& a, cudaStream_t st);
+
 int bsr_build(TdbSystem* sys);
 int bsr_mv_launch(const BsrMvArgs& a, cudaStream_t st);
 

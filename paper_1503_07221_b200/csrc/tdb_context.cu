@@ -184,6 +184,12 @@ int tdb_system_destroy(TdbSystem* sys) {
     dev_free(f.slo);
     dev_free(f.shi);
   }
+  for (auto& b : sys->tbsr) {
+    dev_free(b.col);
+    dev_free(b.pos);
+    dev_free(b.val);
+    dev_free(b.rbptr);
+  }
   for (auto& b : sys->bsr) {
     dev_free(b.col);
     dev_free(b.val);

@@ -61,6 +61,17 @@ struct BsrStore {
   int64_t* rbptr = nullptr;   // (npos * nRB + 1,)
 };
 
+// One family's stored blocks as 8 x 4 tiles ordered (row block, column block,
+// position): the lag blocks that reuse one x strip are adjacent (tdb_tbsr.cu).
+struct TbsrStore {
+  bool built = false;
+  long long ntiles = 0;
+  int32_t* col = nullptr;     // (ntiles,) column block
+  int32_t* pos = nullptr;     // (ntiles,) position within the family
+  double* val = nullptr;      // (ntiles, 32) A-fragment order
+  int64_t* rbptr = nullptr;   // (nRB + 1,)
+};
+
 struct FamilyStore {
   int npos = 0;
   long long nnz = 0;
@@ -121,5 +132,6 @@ struct TdbSystem {
   int nRB = 0, nCB = 0;  // ceil(nrows / 8), ceil(V / 4)
   std::vector<tdb::BsrStore> bsr;
   bool bsr_built = false;
+  std::vector<tdb::TbsrStore> tbsr;  // per family, built on first use by a matvec plan
   TdbStats stats{};
 };

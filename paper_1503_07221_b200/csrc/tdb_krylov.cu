@@ -184,27 +184,44 @@ __global__ void __launch_bounds__(kArnThreads) k_krylov_arnoldi(const double* __
     for (int j = 0; j < nj; ++j) hcol[j] = hs[j];
     hcol[nj] = hk;
   }
-  if (H != nullptr && crank == 0 && tid == 0) {
-    // the Givens step, exactly as k_krylov_givens (same thread, after hcol)
-    if (st[TDB_KS_DONE] == 0.0) {
+  if (H != nullptr && crank == 0) {
+    // the Givens step of k_krylov_givens (same arithmetic), with the rotations
+    // staged in shared memory and the rotated column carried in registers: one
+    // thread, no dependent global round trips
+    __shared__ double s_cs[kArnMaxK], s_sn[kArnMaxK];
+    __shared__ double s_g;
+    __shared__ int s_done;
+    for (int j = tid; j < k; j += kArnThreads) {
+      s_cs[j] = cs[j];
+      s_sn[j] = sn[j];
+    }
+    if (tid == 0) {
+      s_done = st[TDB_KS_DONE] != 0.0;
+      s_g = g[k];
+    }
+    __syncthreads();
+    if (tid == 0 && !s_done) {
       double* col = H + k;
-      for (int i = 0; i <= k + 1; ++i) col[i * ldh] = i <= k ? hs[i] : hk;
+      double a = hs[0];
       for (int j = 0; j < k; ++j) {
-        const double a = col[j * ldh], b = col[(j + 1) * ldh];
-        const double t = cs[j] * a + sn[j] * b;
-        col[(j + 1) * ldh] = -sn[j] * a + cs[j] * b;
+        const double b = hs[j + 1];
+        const double t = s_cs[j] * a + s_sn[j] * b;
+        a = -s_sn[j] * a + s_cs[j] * b;
         col[j * ldh] = t;
       }
-      const double hkk = col[k * ldh], hk1 = col[(k + 1) * ldh];
+      const double hkk = a, hk1 = hk;
       const double denom = hypot(hkk, hk1);
-      cs[k] = denom > 0.0 ? hkk / denom : 1.0;
-      sn[k] = denom > 0.0 ? hk1 / denom : 0.0;
+      const double c = denom > 0.0 ? hkk / denom : 1.0;
+      const double sg = denom > 0.0 ? hk1 / denom : 0.0;
+      cs[k] = c;
+      sn[k] = sg;
       col[k * ldh] = denom;
-      g[k + 1] = -sn[k] * g[k];
-      g[k] = cs[k] * g[k];
+      const double gk = s_g;
+      g[k + 1] = -sg * gk;
+      g[k] = c * gk;
       col[(k + 1) * ldh] = 0.0;
       st[TDB_KS_KDONE] = (double)(k + 1);
-      if (fabs(g[k + 1]) <= st[TDB_KS_TOL_ABS]) {
+      if (fabs(-sg * gk) <= st[TDB_KS_TOL_ABS]) {
         st[TDB_KS_DONE] = 1.0;
         st[TDB_KS_CONVERGED] = 1.0;
       } else if (hk <= 1e-14 * st[TDB_KS_BETA]) {
@@ -232,8 +249,8 @@ int tdb_krylov_arnoldi(const double* V, int64_t ldv, int64_t n, int32_t k, doubl
     cudaFuncSetAttribute(k_krylov_arnoldi, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return 16;
   }();
-  // cluster of up to 16 CTAs (one per SM), at least ~2K elements per CTA
-  int cls = (int)std::min<long long>(csize, std::max<long long>(1, n / 2048));
+  // cluster of up to 16 CTAs (one per SM), at least ~512 elements per CTA
+  int cls = (int)std::min<long long>(csize, std::max<long long>(1, n / 512));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cls);
   cfg.blockDim = dim3(kArnThreads);

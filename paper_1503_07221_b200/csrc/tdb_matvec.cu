@@ -397,6 +397,12 @@ struct TdbMatvecPlan {
   double* d_ypart = nullptr;
   unsigned* d_done = nullptr;
   double bytes = 0.0, flops = 0.0;
+  // p = 0 Toeplitz-ordered tensor-core path for the lag terms (tdb_tbsr.cu)
+  bool tbsr = false;
+  TbsrMvArgs targs{};
+  int* d_toff = nullptr;
+  unsigned* d_tact = nullptr;
+  double* d_typart = nullptr;
   // p = 0 tensor-core path (tdb_bsr.cu)
   bool bsr = false;
   BsrMvArgs bargs{};
@@ -411,6 +417,9 @@ struct TdbMatvecPlan {
 extern "C" int tdb_matvec_plan_destroy(TdbMatvecPlan* p) {
   if (!p) return TDB_OK;
   cudaDeviceSynchronize();  // the system may already be gone: no p->sys access here
+  dev_free(p->d_toff);
+  dev_free(p->d_tact);
+  dev_free(p->d_typart);
   dev_free(p->d_fam);
   dev_free(p->d_ints);
   dev_free(p->d_mask);
@@ -428,7 +437,7 @@ extern "C" int tdb_matvec_plan_destroy(TdbMatvecPlan* p) {
   return TDB_OK;
 }
 
-extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, TdbMatvecPlan** out) {
+static int plan_create_impl(TdbSystem* sys, const TdbMatvecDesc* d, TdbMatvecPlan** out) {
   TDB_REQUIRE(sys && d && out, "NULL argument");
   TDB_REQUIRE(d->rlo >= 1 && d->rhi >= d->rlo && d->rhi <= d->N, "bad row range");
   TDB_REQUIRE(d->clo >= 1 && d->chi >= d->clo && d->chi <= d->N, "bad column range");
@@ -658,6 +667,166 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   return TDB_OK;
 }
 
+// Lag terms of the most reused family -> Toeplitz-ordered DMMA tiles (tdb_tbsr.cu);
+// every other term (boundary blocks used at a few block rows, and all terms when
+// p > 0) -> the CSR kernel above, which writes y first; the tile kernel adds.
+extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, TdbMatvecPlan** out) {
+  TDB_REQUIRE(sys && d && out, "NULL argument");
+  static const bool tbsr_on = [] {
+    const char* e = std::getenv("TDB_MV_TBSR");
+    const char* b = std::getenv("TDB_MV_BSR");
+    return !(e && std::atoi(e) == 0) && !(b && std::atoi(b) != 0);
+  }();
+  const int nt = d->nterms;
+  if (!tbsr_on || sys->np1 != 1 || nt <= 0 || d->words != (d->N + 31) / 32) return plan_create_impl(sys, d, out);
+  std::vector<int> nlog(nt, 0), cnt(sys->F, 0);
+  for (int t = 0; t < nt; ++t) {
+    const int f = d->term_family[t];
+    if (f < 0 || f >= sys->F || d->term_pos[t] < 0 || d->term_pos[t] >= sys->fam[f].npos)
+      return plan_create_impl(sys, d, out);  // reports the error
+    for (int w = 0; w < d->words; ++w) nlog[t] += __builtin_popcount(d->term_mask[(long long)t * d->words + w]);
+    if (nlog[t] > kSpmvMaxKt) ++cnt[f];
+  }
+  const int tf = (int)(std::max_element(cnt.begin(), cnt.end()) - cnt.begin());
+  if (cnt[tf] < 2) return plan_create_impl(sys, d, out);
+  const int npos = sys->fam[tf].npos;
+  std::vector<int> term_of(npos, -1);
+  std::vector<char> to_tile(nt, 0);
+  for (int t = 0; t < nt; ++t)
+    if (d->term_family[t] == tf && nlog[t] > kSpmvMaxKt && term_of[d->term_pos[t]] < 0) {
+      term_of[d->term_pos[t]] = t;
+      to_tile[t] = 1;
+    }
+  {  // tile-walk efficiency: useful (block row, time tile) slots over all slots walked
+    const int nr_ = d->rhi - d->rlo + 1, ntt_ = (nr_ + 7) / 8, ntg_ = (ntt_ + 11) / 12;
+    const int TT_ = std::min(12, (((ntt_ + ntg_ - 1) / ntg_) + 1) & ~1);
+    double useful = 0.0;
+    for (int s_ = 0; s_ < npos; ++s_)
+      if (term_of[s_] >= 0) useful += nlog[term_of[s_]];
+    static const double min_eff = [] {
+      const char* e = std::getenv("TDB_TBSR_MIN_EFF");
+      return e ? std::atof(e) : 0.3;
+    }();
+    if (useful < min_eff * (double)npos * ntg_ * TT_ * 8) return plan_create_impl(sys, d, out);
+  }
+  if (tbsr_build(sys, tf) != TDB_OK) {  // e.g. no room for the tile copy: CSR for every term
+    cudaGetLastError();
+    return plan_create_impl(sys, d, out);
+  }
+  // the CSR plan of the remaining terms
+  std::vector<int> cf, cs, cd;
+  std::vector<unsigned> cm;
+  for (int t = 0; t < nt; ++t) {
+    if (to_tile[t]) continue;
+    cf.push_back(d->term_family[t]);
+    cs.push_back(d->term_pos[t]);
+    cd.push_back(d->term_d[t]);
+    cm.insert(cm.end(), d->term_mask + (long long)t * d->words, d->term_mask + (long long)(t + 1) * d->words);
+  }
+  TdbMatvecDesc dc = *d;
+  dc.nterms = (int)cf.size();
+  dc.term_family = cf.data();
+  dc.term_pos = cs.data();
+  dc.term_d = cd.data();
+  dc.term_mask = cm.data();
+  TdbMatvecPlan* p = nullptr;
+  int rc = plan_create_impl(sys, &dc, &p);
+  if (rc != TDB_OK) return rc;
+  // algorithmic bytes / flops of the tiled terms (canonical CSR figures, as for the rest)
+  {
+    std::vector<int64_t> fp((size_t)npos * sys->nrows + 1);
+    TDB_CUDA_CHECK(cudaMemcpy(fp.data(), sys->fam[tf].indptr, fp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    for (int t = 0; t < nt; ++t)
+      if (to_tile[t]) {
+        const double nnz = (double)(fp[(size_t)(d->term_pos[t] + 1) * sys->nrows] - fp[(size_t)d->term_pos[t] * sys->nrows]);
+        p->bytes += nnz * 12.0;
+        p->flops += 2.0 * nnz * nlog[t];
+      }
+  }
+  const int M = (int)sys->V, nRB = sys->nRB, nCB = sys->nCB;
+  const int nr = d->rhi - d->rlo + 1, nc = d->chi - d->clo + 1;
+  const int ntt = (nr + 7) / 8;
+  const int ntg = (ntt + 11) / 12;
+  int TT = (ntt + ntg - 1) / ntg;
+  TT = std::min(12, (TT + 1) & ~1);
+  const int xs_b = nc + 8;
+  std::vector<int> off((size_t)ntg * npos * TT * 8, nc);
+  std::vector<unsigned> act((size_t)ntg * npos, 0u);
+  for (int s_ = 0; s_ < npos; ++s_) {
+    const int t = term_of[s_];
+    if (t < 0) continue;
+    const unsigned* mk = d->term_mask + (long long)t * d->words;
+    for (int tg = 0; tg < ntg; ++tg)
+      for (int u = 0; u < TT; ++u)
+        for (int gq = 0; gq < 8; ++gq) {
+          const int r = 8 * (tg * TT + u) + gq, kt = d->rlo + r;
+          if (r >= nr || !((mk[(kt - 1) >> 5] >> ((kt - 1) & 31)) & 1u)) continue;
+          const int c = kt - d->term_d[t] - d->clo;
+          if (c < 0 || c >= nc) {
+            tdb_matvec_plan_destroy(p);
+            set_error("matvec: term mask has a block column outside the plan's column range");
+            return TDB_E_INVALID;
+          }
+          off[(((size_t)tg * npos + s_) * 8 + gq) * TT + u] = c;
+          act[(size_t)tg * npos + s_] |= 1u << u;
+        }
+  }
+  static const int tb_warps = [] {
+    const char* e = std::getenv("TDB_TBSR_WARPS_PER_SM");
+    return e ? std::max(1, std::atoi(e)) : 32;
+  }();
+  const int G = std::max(1, std::min(256, sys->ctx->num_sms * tb_warps / std::max(1, nRB * ntg)));
+  std::vector<long long> xmp(M);
+  for (int lp = 0; lp < M; ++lp) {
+    const int l = sys->vperm[lp];
+    xmp[lp] = d->x_map ? (long long)d->x_map[l] : (long long)l;
+  }
+  cudaStream_t st = sys->ctx->stream;
+  const size_t xp_n = (size_t)nCB * 4 * xs_b;
+  const size_t yp_n = (size_t)nRB * ntg * G * TT * 64;
+#define ALLOC_COPY3(dst, src, n, T_)                                                               \
+  do {                                                                                             \
+    size_t nn = std::max<size_t>(1, (size_t)(n));                                                  \
+    if (dev_malloc((void**)&(dst), nn * sizeof(T_)) != cudaSuccess) {                             \
+      tdb_matvec_plan_destroy(p);                                                                  \
+      set_error("matvec plan: cudaMalloc failed");                                                 \
+      return TDB_E_NOMEM;                                                                          \
+    }                                                                                              \
+    if ((n) > 0 && (src) != nullptr)                                                               \
+      cudaMemcpyAsync((dst), (src), (size_t)(n) * sizeof(T_), cudaMemcpyHostToDevice, st);         \
+  } while (0)
+  ALLOC_COPY3(p->d_toff, off.data(), off.size(), int);
+  ALLOC_COPY3(p->d_tact, act.data(), act.size(), unsigned);
+  ALLOC_COPY3(p->d_typart, (const double*)nullptr, yp_n, double);
+  ALLOC_COPY3(p->d_xmap_p, xmp.data(), M, long long);
+  ALLOC_COPY3(p->d_xp, (const double*)nullptr, xp_n, double);
+  cudaMemsetAsync(p->d_xp, 0, xp_n * sizeof(double), st);
+#undef ALLOC_COPY3
+  TDB_CUDA_CHECK(cudaStreamSynchronize(st));
+  const TbsrStore& tb = sys->tbsr[tf];
+  TbsrMvArgs& ta = p->targs;
+  ta.nRB = nRB;
+  ta.G = G;
+  ta.ntg = ntg;
+  ta.TT = TT;
+  ta.npos = npos;
+  ta.nrows = sys->nrows;
+  ta.nr = nr;
+  ta.col = tb.col;
+  ta.pos = tb.pos;
+  ta.val = tb.val;
+  ta.rbptr = tb.rbptr;
+  ta.off_tab = p->d_toff;
+  ta.act_tab = p->d_tact;
+  ta.rperm = sys->d_rperm;
+  ta.xp = p->d_xp;
+  ta.xs = xs_b;
+  ta.ypart = p->d_typart;
+  p->tbsr = true;
+  *out = p;
+  return TDB_OK;
+}
+
 extern "C" int tdb_matvec_plan_work(const TdbMatvecPlan* p, double* bytes, double* flops) {
   TDB_REQUIRE(p != nullptr, "NULL plan");
   if (bytes) *bytes = p->bytes;
@@ -694,5 +863,12 @@ extern "C" int tdb_matvec(TdbMatvecPlan* p, const double* x, double* y) {
     }
   }
   TDB_CUDA_CHECK(cudaGetLastError());
+  if (p->tbsr) {  // lag terms on the tensor cores, added to the CSR kernel's y
+    dim3 blk(32, 8), grd((a.M + 31) / 32, (ncols + 31) / 32);
+    k_transpose_in<<<grd, blk, 0, st>>>(x, p->d_xp, a.M, ncols, p->targs.xs, p->d_xmap_p, p->xstride);
+    TDB_CUDA_CHECK(cudaGetLastError());
+    p->targs.y = y;
+    return tbsr_mv_launch(p->targs, st);
+  }
   return TDB_OK;
 }
