@@ -366,7 +366,13 @@ def main():
               "achieved_GBps": mv_bytes / (mv_ms * 1e-3) / 1e9 / max(1, world),
               "hbm_peak_GBps": hbm, "frac_hbm_per_gpu": mv_bytes / (mv_ms * 1e-3) / 1e9 / world / hbm,
               "peak_source": hbm_src,
-              "includes": "ncclAllGather of the iterate" if world > 1 else "transpose + SpMM + reduce"}
+              "achieved_TFLOPs": mv_flops / (mv_ms * 1e-3) / 1e12 / max(1, world),
+              "frac_fp64_per_gpu": mv_flops / (mv_ms * 1e-3) / 1e12 / max(1, world) / peak_meas,
+              "intensity_flop_per_byte": mv_flops / max(mv_bytes, 1.0),
+              "kernels": "lag terms of the inner family: FP64 DMMA tiles (k_tbsr_mv + k_tbsr_reduce); "
+                         "boundary terms: CSR (k_matvec)",
+              "includes": ("ncclAllGather of the iterate" if world > 1 else "transposes + CSR SpMM + DMMA tiles"
+                           " + ordered reduce")}
 
     # end to end through the public API (host mesh in, every block back on the host)
     e2e = None

@@ -183,26 +183,34 @@ __device__ __forceinline__ void mv_single_chunk(const MvArgs& a, int t, int n, c
   const int4 k4 = __ldg(reinterpret_cast<const int4*>(a.term_kt) + t);
   const int kts[4] = {k4.x, k4.y, k4.z, k4.w};
   const int d = __ldg(a.term_d + t);
-  const int ncol = a.nc * NP1;
-  int xo[kSpmvMaxKt];
+  // 32-bit element offsets (row l * xs + column) and one IMAD.WIDE.U32 per load;
+  // block rows outside the mask read the zero pad column and are never reduced
+  const unsigned xs = (unsigned)a.xs, zpad = xs - NP1;
+  bool on[kSpmvMaxKt];
+  unsigned xo[kSpmvMaxKt];
 #pragma unroll
-  for (int k = 0; k < kSpmvMaxKt; ++k) xo[k] = kts[k] > 0 ? (kts[k] - d - a.clo) * NP1 : -1;
+  for (int k = 0; k < kSpmvMaxKt; ++k) {
+    on[k] = kts[k] > 0;
+    xo[k] = on[k] ? (unsigned)((kts[k] - d - a.clo) * NP1) : zpad;
+  }
+  const double* __restrict__ xt = a.xt;
   double part[kSpmvMaxKt][NP1];
 #pragma unroll
   for (int k = 0; k < kSpmvMaxKt; ++k)
 #pragma unroll
     for (int m = 0; m < NP1; ++m) part[k][m] = 0.0;
+#pragma unroll 4
   for (int q = lane; q < n; q += 32) {
-    const double* xl = a.xt + (size_t)((unsigned)s_idx[q] * (unsigned)a.xs);
+    const unsigned rowo = (unsigned)s_idx[q] * xs;
     double v[NM];
 #pragma unroll
     for (int m = 0; m < NM; ++m) v[m] = s_val[q * NM + m];
 #pragma unroll
     for (int k = 0; k < kSpmvMaxKt; ++k) {
-      if (xo[k] >= 0) {
+      if (on[k]) {  // warp-uniform
 #pragma unroll
         for (int m1 = 0; m1 < NP1; ++m1) {
-          const double xv = __ldg(xl + xo[k] + m1);
+          const double xv = __ldg(xt + (rowo + xo[k] + m1));
 #pragma unroll
           for (int m2 = 0; m2 < NP1; ++m2) part[k][m2] = fma(v[m2 * NP1 + m1], xv, part[k][m2]);
         }
@@ -211,7 +219,7 @@ __device__ __forceinline__ void mv_single_chunk(const MvArgs& a, int t, int n, c
   }
 #pragma unroll
   for (int k = 0; k < kSpmvMaxKt; ++k) {
-    if (xo[k] < 0) continue;  // warp-uniform
+    if (!on[k]) continue;  // warp-uniform
     const int r = kts[k] - a.rlo, owner = r & 31, chunk = r >> 5;
 #pragma unroll
     for (int m2 = 0; m2 < NP1; ++m2) {
@@ -773,9 +781,14 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   }
   static const int tb_warps = [] {
     const char* e = std::getenv("TDB_TBSR_WARPS_PER_SM");
-    return e ? std::max(1, std::atoi(e)) : 32;
+    return e ? std::max(1, std::atoi(e)) : 48;
   }();
-  const int G = std::max(1, std::min(256, sys->ctx->num_sms * tb_warps / std::max(1, nRB * ntg)));
+  // parts per (row block, time group): enough warps to hide the B-gather latency,
+  // but >= 64 tiles per warp so the ordered partial reduction stays small
+  const long long tiles_per_rb = sys->tbsr[tf].ntiles / std::max(1, nRB);
+  const int G = (int)std::max<long long>(
+      1, std::min<long long>({256LL, (long long)sys->ctx->num_sms * tb_warps / std::max(1, nRB * ntg),
+                              tiles_per_rb / 64}));
   std::vector<long long> xmp(M);
   for (int lp = 0; lp < M; ++lp) {
     const int l = sys->vperm[lp];
