@@ -1324,7 +1324,20 @@ struct AsmWorkspace {
   cudaEvent_t ev[6];
   bool events = false;
   long long launch_count = 0;
+  // pattern phase: the families' count -> scan -> fill chains run on their own
+  // streams (independent outputs), each with its own cub scratch
+  static constexpr int kFamStreams = 4;
+  cudaStream_t fstream[kFamStreams] = {};
+  cudaEvent_t fevent[kFamStreams] = {};
+  void* fcub[kFamStreams] = {};
+  bool fstreams = false;
   ~AsmWorkspace() {
+    if (fstreams)
+      for (int k = 0; k < kFamStreams; ++k) {
+        cudaStreamDestroy(fstream[k]);
+        cudaEventDestroy(fevent[k]);
+        dev_free(fcub[k]);
+      }
     dev_free(blob);
     for (void* p : rule_mem) dev_free(p);
     dev_free(d_nitems_case);
@@ -1355,14 +1368,14 @@ void tdb_workspace_free(TdbSystem* sys) {
   sys->ws = nullptr;
 }
 
-static int scan_inplace(AsmWorkspace* ws, long long* data, long long n, cudaStream_t st) {
+static int scan_inplace(AsmWorkspace* ws, long long* data, long long n, cudaStream_t st, void* tmp = nullptr) {
   size_t need = 0;
   TDB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, need, data, data, (int64_t)n, st));
   if (need > ws->cub_bytes) {
     set_error("internal: cub workspace too small");
     return TDB_E_CUDA;
   }
-  TDB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ws->cub_tmp, need, data, data, (int64_t)n, st));
+  TDB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp ? tmp : ws->cub_tmp, need, data, data, (int64_t)n, st));
   return TDB_OK;
 }
 
@@ -1440,7 +1453,7 @@ static int run_plan(TdbSystem* sys, cudaStream_t st) {
   return TDB_OK;
 }
 
-static int run_pattern_count(TdbSystem* sys, int f, cudaStream_t st) {
+static int run_pattern_count(TdbSystem* sys, int f, cudaStream_t st, void* tmp = nullptr) {
   AsmWorkspace* ws = sys->ws;
   PatternArgs ga = pattern_args(sys, f);
   const int npos = ga.npos;
@@ -1455,7 +1468,7 @@ static int run_pattern_count(TdbSystem* sys, int f, cudaStream_t st) {
   }
   const long long nrows = (long long)npos * ws->nrows;
   TDB_CUDA_CHECK(cudaMemsetAsync(ga.row_count + nrows, 0, sizeof(long long), st));
-  return scan_inplace(ws, ga.row_count, nrows + 1, st);
+  return scan_inplace(ws, ga.row_count, nrows + 1, st, tmp);
 }
 
 int tdb_system_run_impl(TdbSystem* sys) {
@@ -1523,21 +1536,43 @@ int tdb_system_run_impl(TdbSystem* sys) {
     TDB_CUDA_CHECK(cudaGetLastError());
   }
   TDB_CUDA_CHECK(cudaEventRecord(ws->ev[3], st));
-  for (int f = 0; f < sys->F; ++f) {
-    if ((rc = run_pattern_count(sys, f, st))) return rc;
+  if (!ws->fstreams) {
+    for (int k = 0; k < AsmWorkspace::kFamStreams; ++k) {
+      TDB_CUDA_CHECK(cudaStreamCreateWithFlags(&ws->fstream[k], cudaStreamNonBlocking));
+      TDB_CUDA_CHECK(cudaEventCreateWithFlags(&ws->fevent[k], cudaEventDisableTiming));
+      if (dev_malloc(&ws->fcub[k], ws->cub_bytes) != cudaSuccess) {
+        set_error("pattern streams: cudaMalloc failed");
+        return TDB_E_NOMEM;
+      }
+    }
+    ws->fstreams = true;
+  }
+  // families by decreasing position count, dealt round-robin over the streams
+  std::vector<int> forder(sys->F);
+  for (int f = 0; f < sys->F; ++f) forder[f] = f;
+  std::stable_sort(forder.begin(), forder.end(), [&](int x, int y) { return sys->fam[x].npos > sys->fam[y].npos; });
+  for (int k = 0; k < AsmWorkspace::kFamStreams; ++k) TDB_CUDA_CHECK(cudaStreamWaitEvent(ws->fstream[k], ws->ev[3], 0));
+  for (int fi = 0; fi < sys->F; ++fi) {
+    const int f = forder[fi], sk = fi % AsmWorkspace::kFamStreams;
+    cudaStream_t fst = ws->fstream[sk];
+    if ((rc = run_pattern_count(sys, f, fst, ws->fcub[sk]))) return rc;
     PatternArgs ga = pattern_args(sys, f);
     for (int s0 = 0; s0 < ga.npos; s0 += ws->s_chunk[f]) {
       ga.s_begin = s0;
       ga.s_count = std::min(ws->s_chunk[f], ga.npos - s0);
       const size_t smem = (size_t)ga.s_count * ws->words * 8 + (2 * ws->words + 1) * 4;
       switch (NM) {
-        case 1: rc = launch_fill<1>(ga, smem, st); break;
-        case 4: rc = launch_fill<4>(ga, smem, st); break;
-        case 9: rc = launch_fill<9>(ga, smem, st); break;
-        default: rc = launch_fill<16>(ga, smem, st); break;
+        case 1: rc = launch_fill<1>(ga, smem, fst); break;
+        case 4: rc = launch_fill<4>(ga, smem, fst); break;
+        case 9: rc = launch_fill<9>(ga, smem, fst); break;
+        default: rc = launch_fill<16>(ga, smem, fst); break;
       }
       if (rc) return rc;
     }
+  }
+  for (int k = 0; k < AsmWorkspace::kFamStreams; ++k) {
+    TDB_CUDA_CHECK(cudaEventRecord(ws->fevent[k], ws->fstream[k]));
+    TDB_CUDA_CHECK(cudaStreamWaitEvent(st, ws->fevent[k], 0));
   }
   TDB_CUDA_CHECK(cudaEventRecord(ws->ev[4], st));
   TDB_CUDA_CHECK(cudaEventSynchronize(ws->ev[4]));
