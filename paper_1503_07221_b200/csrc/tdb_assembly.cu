@@ -799,11 +799,24 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
 // ---------------------------------------------------------------------------
 // 4. singular pairs: sum item partials into item 0 (item order, deterministic)
 // ---------------------------------------------------------------------------
-__global__ void k_finalize_items(long long E2, const int* __restrict__ units,
+// list of the pairs with more than one work item (singular cases), built once per
+// system; the finalize walks only those (order-free: pairs are independent)
+__global__ void k_multi_list(long long E2, const int* __restrict__ units, const unsigned char* __restrict__ pcase,
+                             const int* nitems_case, long long cap, long long* __restrict__ list,
+                             unsigned long long* __restrict__ count) {
+  for (long long Pp = blockIdx.x * (long long)blockDim.x + threadIdx.x; Pp < E2; Pp += (long long)gridDim.x * blockDim.x)
+    if (units[Pp] > 0 && nitems_case[pcase[Pp]] > 1) {
+      const unsigned long long i = atomicAdd(count, 1ULL);
+      if ((long long)i < cap) list[i] = Pp;
+    }
+}
+
+__global__ void k_finalize_items(long long nlist, const long long* __restrict__ list, const int* __restrict__ units,
                                  const unsigned char* __restrict__ pcase,
                                  const long long* __restrict__ pair_base, const int* nitems_case,
                                  int nacc, double* __restrict__ part) {
-  for (long long Pp = blockIdx.x; Pp < E2; Pp += gridDim.x) {
+  for (long long li = blockIdx.x; li < nlist; li += gridDim.x) {
+    const long long Pp = list[li];
     const int ni = nitems_case[pcase[Pp]];
     const int U = units[Pp];
     if (ni <= 1 || U == 0) continue;
@@ -1297,6 +1310,8 @@ struct AsmWorkspace {
   std::vector<void*> rule_mem;
   int nitems_case[4] = {1, 1, 1, 1};
   int* d_nitems_case = nullptr;
+  long long* multi = nullptr;  // pairs with > 1 work item (k_multi_list)
+  long long nmulti = 0;
   FRange* frange = nullptr;
   int* units = nullptr;
   long long* slots = nullptr;
@@ -1341,6 +1356,7 @@ struct AsmWorkspace {
     dev_free(blob);
     for (void* p : rule_mem) dev_free(p);
     dev_free(d_nitems_case);
+    dev_free(multi);
     dev_free(frange);
     dev_free(units);
     dev_free(slots);
@@ -1531,8 +1547,8 @@ int tdb_system_run_impl(TdbSystem* sys) {
   bool multi = false;
   for (int c = 0; c < 4; ++c) multi |= ws->nitems_case[c] > 1;
   if (multi) {
-    k_finalize_items<<<148 * 16, 256, 0, st>>>(ws->E2, ws->units, ws->pcase, ws->slots,
-                                               ws->d_nitems_case, NACC, ws->part);
+    k_finalize_items<<<(unsigned)std::max<long long>(1, std::min<long long>(ws->nmulti, 148 * 16)), 256, 0, st>>>(
+        ws->nmulti, ws->multi, ws->units, ws->pcase, ws->slots, ws->d_nitems_case, NACC, ws->part);
     TDB_CUDA_CHECK(cudaGetLastError());
   }
   TDB_CUDA_CHECK(cudaEventRecord(ws->ev[3], st));
@@ -2103,6 +2119,21 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
   }
   if ((rc = dalloc(&ws->items, ws->total_items))) return rc;
   if ((rc = dalloc(&ws->part, (size_t)ws->total_slots * NACC))) return rc;
+  {  // pairs the singular-group finalize has to visit
+    const long long cap = std::max<long long>(1, (long long)ws->Et * 64);
+    if ((rc = dalloc(&ws->multi, cap))) return rc;
+    unsigned long long* d_cnt = reinterpret_cast<unsigned long long*>(ws->counters) + 63;
+    TDB_CUDA_CHECK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), st));
+    k_multi_list<<<148 * 8, 256, 0, st>>>(E2, ws->units, ws->pcase, ws->d_nitems_case, cap, ws->multi, d_cnt);
+    TDB_CUDA_CHECK(cudaGetLastError());
+    long long nm_ = 0;
+    if ((rc = read_ll(reinterpret_cast<const long long*>(d_cnt), &nm_, st))) return rc;
+    if (nm_ > cap) {
+      set_error("internal: singular pair list overflow");
+      return TDB_E_CUDA;
+    }
+    ws->nmulti = nm_;
+  }
   // pattern sizing: counts -> scan -> nnz
   long long nnz_total = 0;
   for (int f = 0; f < F; ++f) {
