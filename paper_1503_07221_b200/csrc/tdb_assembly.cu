@@ -194,6 +194,32 @@ struct PlanArgs {
 };
 
 __global__ void k_plan_pairs(PlanArgs a) {
+  // the families' support bounds (slo, shi per position) staged in shared memory:
+  // the 2 F binary searches per pair are the kernel's dependent-load chain
+  extern __shared__ double pl_smem[];
+  __shared__ int s_off[kMaxFamilies + 1];
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int f = 0; f < a.F; ++f) {
+      s_off[f] = o;
+      o += a.fams[f].npos;
+    }
+    s_off[a.F] = o;
+  }
+  __syncthreads();
+  const int ntot = s_off[a.F];
+  double* s_lo = pl_smem;
+  double* s_hi = pl_smem + ntot;
+  for (int f = 0; f < a.F; ++f) {
+    const FamDev& fd = a.fams[f];
+    for (int i = threadIdx.x; i < fd.npos; i += blockDim.x) {
+      s_lo[s_off[f] + i] = fd.slo[i];
+      s_hi[s_off[f] + i] = fd.shi[i];
+    }
+  }
+  __syncthreads();
+  // per-thread case counters, reduced per warp before the global atomics
+  unsigned long long c_pairs[4] = {0, 0, 0, 0}, c_units[4] = {0, 0, 0, 0}, c_prim = 0;
   const long long E2 = (long long)a.Et * a.E;  // pairs of this system
   for (long long P = blockIdx.x * (long long)blockDim.x + threadIdx.x; P < E2;
        P += (long long)gridDim.x * blockDim.x) {
@@ -202,9 +228,9 @@ __global__ void k_plan_pairs(PlanArgs a) {
     const int cs = pair_bounds(a.corners, a.tri, ex, ey, dmin, dmax);
     int units = 0;
     for (int f = 0; f < a.F; ++f) {
-      const FamDev& fd = a.fams[f];
-      int s0 = first_geq(fd.shi, fd.npos, dmin);  // shi >= tmin
-      int s1 = last_leq(fd.slo, fd.npos, dmax);   // slo <= tmax
+      const int n = s_off[f + 1] - s_off[f];
+      int s0 = first_geq(s_hi + s_off[f], n, dmin);  // shi >= tmin
+      int s1 = last_leq(s_lo + s_off[f], n, dmax);   // slo <= tmax
       int cnt = s1 >= s0 ? s1 - s0 + 1 : 0;
       FRange fr;
       fr.foff = units;
@@ -218,12 +244,30 @@ __global__ void k_plan_pairs(PlanArgs a) {
     a.slots[P] = (long long)units * ni;
     a.nitems[P] = ni;
     if (units > 0) {
-      atomicAdd(a.case_pairs + cs, 1ULL);
-      atomicAdd(a.case_pairs + 4 + cs, (unsigned long long)units);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c == cs) {
+          c_pairs[c] += 1;
+          c_units[c] += (unsigned long long)units;
+        }
       // each test triangle is "primary" on exactly one row block (owner of its first vertex)
-      if (a.owned[a.tri[3 * ey]]) atomicAdd(a.case_pairs + 8, (unsigned long long)units);
+      if (a.owned[a.tri[3 * ey]]) c_prim += (unsigned long long)units;
     }
   }
+  auto wsum = [](unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
+  const bool lead = (threadIdx.x & 31) == 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const unsigned long long p_ = wsum(c_pairs[c]), u_ = wsum(c_units[c]);
+    if (lead && p_) atomicAdd(a.case_pairs + c, p_);
+    if (lead && u_) atomicAdd(a.case_pairs + 4 + c, u_);
+  }
+  const unsigned long long q_ = wsum(c_prim);
+  if (lead && q_) atomicAdd(a.case_pairs + 8, q_);
 }
 
 __global__ void k_fill_items(long long E2, const long long* __restrict__ item_base,
@@ -1456,7 +1500,12 @@ static int run_plan(TdbSystem* sys, cudaStream_t st) {
   TDB_CUDA_CHECK(cudaMemsetAsync(ws->counters, 0, 64 * sizeof(unsigned long long), st));
   PlanArgs pa = plan_args(sys);
   const long long blocks = std::min<long long>((ws->E2 + 255) / 256, 148LL * 32);
-  k_plan_pairs<<<(int)blocks, 256, 0, st>>>(pa);
+  int ntot = 0;
+  for (int f = 0; f < sys->F; ++f) ntot += sys->fam[f].npos;
+  const size_t psmem = (size_t)2 * ntot * sizeof(double);
+  if (psmem > 48 * 1024)
+    TDB_CUDA_CHECK(cudaFuncSetAttribute(k_plan_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+  k_plan_pairs<<<(int)blocks, 256, psmem, st>>>(pa);
   TDB_CUDA_CHECK(cudaGetLastError());
   int rc;
   if ((rc = scan_inplace(ws, ws->slots, ws->E2, st))) return rc;
