@@ -1136,7 +1136,7 @@ __device__ void gather_entry(const PatternArgs& a, const RowStar& rs, int s0, in
 // (j, l) gathers its values for SC positions at a time and writes the entries
 // that are in each position's pattern.
 #ifndef TDB_FILL_MINB
-#define TDB_FILL_MINB 3
+#define TDB_FILL_MINB 2
 #endif
 template <int NM>
 __global__ void __launch_bounds__(256, TDB_FILL_MINB) k_pattern_fill(PatternArgs a) {
