@@ -419,7 +419,16 @@ __device__ __forceinline__ XPow xpowers(double x) {
 // float2 per FP32-tail row of one subinterval: (D - K + 1) coefficients x NT / 2
 // table pairs, rounded up to odd so rows of consecutive subintervals fall in
 // distinct shared-memory bank pairs
-__host__ __device__ constexpr int tail_row_f2(int D, int K, int NT) { return ((D - K + 1) * NT / 2) | 1; }
+// At NT = 2 (p = 0) the pitch is 2 x odd float2 (16 x odd bytes): rows start
+// 16-byte aligned for the paired LDS.128 tail loads, and up to 8 distinct rows of
+// one warp access still land in distinct bank groups.
+__host__ __device__ constexpr int tail_row_f2(int D, int K, int NT) {
+#ifdef TDB_TAIL128
+  return NT == 2 ? ((((D - K + 1) + 1) / 2) | 1) * 2 : ((D - K + 1) * NT / 2) | 1;
+#else
+  return ((D - K + 1) * NT / 2) | 1;
+#endif
+}
 
 template <int NT, bool GLOBAL, int D, int K>
 __device__ __forceinline__ void eval_pair(const double* __restrict__ cf, int tail_off, int idx, int m,
@@ -469,13 +478,29 @@ __device__ __forceinline__ void eval_pair(const double* __restrict__ cf, int tai
       constexpr int TROW = tail_row_f2(D, K, NT);
       const float2* tp = reinterpret_cast<const float2*>(cf + tail_off) + idx * TROW + m;
       float2 b[D - K + 1];
-#pragma unroll
-      for (int k = 0; k <= D - K; ++k) {
-#ifdef TDB_ABL_NOCOEF
-        b[k] = make_float2(idx * 1e-3f + k, idx * 2e-3f - k);
+#ifdef TDB_TAIL128
+      constexpr bool kPairTail = NT == 2 && (D - K + 1) % 2 == 0;
 #else
-        b[k] = GLOBAL ? __ldg(tp + k * stride) : tp[k * stride];
+      constexpr bool kPairTail = false;
 #endif
+      if constexpr (kPairTail) {
+        // consecutive coefficients are adjacent float2: two per 128-bit load
+        const float4* tp4 = reinterpret_cast<const float4*>(tp);
+#pragma unroll
+        for (int k = 0; k <= D - K; k += 2) {
+          const float4 q = GLOBAL ? __ldg(tp4 + k / 2) : tp4[k / 2];
+          b[k] = make_float2(q.x, q.y);
+          b[k + 1] = make_float2(q.z, q.w);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k <= D - K; ++k) {
+#ifdef TDB_ABL_NOCOEF
+          b[k] = make_float2(idx * 1e-3f + k, idx * 2e-3f - k);
+#else
+          b[k] = GLOBAL ? __ldg(tp + k * stride) : tp[k * stride];
+#endif
+        }
       }
       // (psi, psi~) tails together: one packed fma.rn.f32x2 (FFMA2) per coefficient;
       // each half is an IEEE fp32 FMA, so the result equals two scalar Horner chains
@@ -492,12 +517,9 @@ __device__ __forceinline__ void eval_pair(const double* __restrict__ cf, int tai
 }
 
 struct SortedPts {
-  const double* r;
-  const double* c;
-  const double* x1;
-  const double* x2;
-  const double* y1;
-  const double* y2;
+  const double2* rc;  // (r, weight) of the r-sorted points
+  const double2* px;  // (x1, x2)
+  const double2* py;  // (y1, y2)
   const unsigned* cur;  // bucket ends
   double rmin, rmax, inv_wb;
 };
@@ -551,12 +573,13 @@ __device__ __forceinline__ void eval_rounds(const QFam& fd, const double* __rest
 #ifdef TDB_ABL_NOPT
       r[u] = pt.rmin + j * 1e-4; c[u] = 1.0 + j; x1[u] = 0.5; x2[u] = 0.25 + j * 1e-3; y1[u] = 0.3; y2[u] = 0.1;
 #else
-      r[u] = pt.r[j];
-      c[u] = pt.c[j];
-      x1[u] = pt.x1[j];
-      x2[u] = pt.x2[j];
-      y1[u] = pt.y1[j];
-      y2[u] = pt.y2[j];
+      const double2 rc_ = pt.rc[j], px_ = pt.px[j], py_ = pt.py[j];
+      r[u] = rc_.x;
+      c[u] = rc_.y;
+      x1[u] = px_.x;
+      x2[u] = px_.y;
+      y1[u] = py_.x;
+      y2[u] = py_.y;
 #endif
     }
     double cw[NS], xl[NS];
@@ -621,13 +644,10 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
   double* sdelta = sblob + (SMEM_COEF ? (a.blob_doubles + 1) / 2 * 2 : 0);
   char* swarp = reinterpret_cast<char*>(sdelta + (a.delta_doubles + 1) / 2 * 2);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* sr = reinterpret_cast<double*>(swarp + (size_t)wid * kWarpScratchBytes);
-  double* sc = sr + kChunk;
-  double* sx1 = sc + kChunk;
-  double* sx2 = sx1 + kChunk;
-  double* sy1 = sx2 + kChunk;
-  double* sy2 = sy1 + kChunk;
-  unsigned* cur = reinterpret_cast<unsigned*>(sy2 + kChunk);  // kBuckets + 1
+  double2* s_rc = reinterpret_cast<double2*>(swarp + (size_t)wid * kWarpScratchBytes);
+  double2* s_px = s_rc + kChunk;
+  double2* s_py = s_px + kChunk;
+  unsigned* cur = reinterpret_cast<unsigned*>(s_py + kChunk);  // kBuckets + 1
 
   {  // stage the coefficients and the per-position table offsets
     if (SMEM_COEF)
@@ -752,23 +772,17 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
       const unsigned pos = cur[b] + __popc(grp & lanemask_lt);
       __syncwarp();
       if ((grp & lanemask_lt) == 0) cur[b] += __popc(grp);
-      sr[pos] = rk[k];
-      sc[pos] = ck[k];
-      sx1[pos] = px1[k];
-      sx2[pos] = px2[k];
-      sy1[pos] = py1[k];
-      sy2[pos] = py2[k];
+      s_rc[pos] = make_double2(rk[k], ck[k]);
+      s_px[pos] = make_double2(px1[k], px2[k]);
+      s_py[pos] = make_double2(py1[k], py2[k]);
       __syncwarp();
     }
     // now cur[b] = end of bucket b in the sorted arrays
 
     SortedPts pt;
-    pt.r = sr;
-    pt.c = sc;
-    pt.x1 = sx1;
-    pt.x2 = sx2;
-    pt.y1 = sy1;
-    pt.y2 = sy2;
+    pt.rc = s_rc;
+    pt.px = s_px;
+    pt.py = s_py;
     pt.cur = cur;
     pt.rmin = rmin;
     pt.rmax = rmax;
