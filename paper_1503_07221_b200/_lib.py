@@ -123,6 +123,7 @@ def _load():
         "tdb_matvec_plan_destroy": (i32, [P]),
         "tdb_matvec": (i32, [P, P, P]),
         "tdb_matvec_plan_work": (i32, [P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+        "tdb_matvec_plan_kind": (i32, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
         # device-side GMRES cycle bookkeeping (pointers are device addresses)
         "tdb_krylov_init": (i32, [P, P, C.c_double, P, P]),
         "tdb_krylov_givens": (i32, [P, i32, P, P, i32, P, P, P, P]),
@@ -151,7 +152,7 @@ EXPORTED = (
     "tdb_ctx_create", "tdb_ctx_destroy", "tdb_ctx_set_stream", "tdb_system_assemble",
     "tdb_system_destroy", "tdb_system_stats", "tdb_system_family_nnz", "tdb_system_copy_family",
     "tdb_system_family_device", "tdb_matvec_plan_create", "tdb_matvec_plan_destroy", "tdb_matvec",
-    "tdb_matvec_plan_work", "tdb_tri_distance_bounds", "tdb_system_create", "tdb_system_run",
+    "tdb_matvec_plan_work", "tdb_matvec_plan_kind", "tdb_tri_distance_bounds", "tdb_system_create", "tdb_system_run",
     "tdb_fp64_peak", "tdb_krylov_init", "tdb_krylov_givens", "tdb_krylov_update", "tdb_krylov_flag",
     "tdb_krylov_arnoldi", "tdb_release_cached_memory", "tdb_dlp_eval",
     "tdb_rhs_vertex_gather", "tdb_rhs_time_sum", "tdb_table_node_values",

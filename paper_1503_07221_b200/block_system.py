@@ -143,6 +143,7 @@ class _MatvecPlan:
     def __init__(self, A: "BlockHessenbergMatrix", rows, cols):
         grid = A.grid
         self.rows, self.cols = rows, cols
+        self.tiled_terms = self.csr_terms = 0
         rlo, rhi = rows
         clo, chi = cols
         words = (grid.N + 31) // 32
@@ -186,6 +187,9 @@ class _MatvecPlan:
         b, f = C.c_double(), C.c_double()
         _lib.check(_lib.LIB.tdb_matvec_plan_work(h, C.byref(b), C.byref(f)), "matvec_plan_work")
         self.bytes, self.flops = b.value, f.value
+        nt_, nc_ = C.c_int32(0), C.c_int32(0)
+        _lib.check(_lib.LIB.tdb_matvec_plan_kind(h, C.byref(nt_), C.byref(nc_)), "matvec_plan_kind")
+        self.tiled_terms, self.csr_terms = nt_.value, nc_.value
 
     def __del__(self):
         h = getattr(self, "handle", None)

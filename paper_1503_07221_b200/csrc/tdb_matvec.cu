@@ -407,6 +407,7 @@ struct TdbMatvecPlan {
   double bytes = 0.0, flops = 0.0;
   // p = 0 Toeplitz-ordered tensor-core path for the lag terms (tdb_tbsr.cu)
   bool tbsr = false;
+  int n_tiled = 0, n_csr = 0, n_csr_all = 0;
   TbsrMvArgs targs{};
   int* d_toff = nullptr;
   unsigned* d_tact = nullptr;
@@ -503,6 +504,7 @@ static int plan_create_impl(TdbSystem* sys, const TdbMatvecDesc* d, TdbMatvecPla
   bytes += 8.0 * ((double)nr * NR + (double)nc * M) * NP1;
   p->bytes = bytes;
   p->flops = flops;
+  p->n_csr_all = nt;
   // groups: enough warps to fill the chip on small meshes
   static const int warps_per_sm = [] {
     const char* e = std::getenv("TDB_MV_WARPS_PER_SM");
@@ -836,7 +838,16 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   ta.xs = xs_b;
   ta.ypart = p->d_typart;
   p->tbsr = true;
+  p->n_tiled = nt - (int)cf.size();
+  p->n_csr = (int)cf.size();
   *out = p;
+  return TDB_OK;
+}
+
+extern "C" int tdb_matvec_plan_kind(const TdbMatvecPlan* p, int32_t* tiled_terms, int32_t* csr_terms) {
+  TDB_REQUIRE(p != nullptr, "NULL plan");
+  if (tiled_terms) *tiled_terms = p->tbsr ? p->n_tiled : 0;
+  if (csr_terms) *csr_terms = p->tbsr ? p->n_csr : p->n_csr_all;
   return TDB_OK;
 }
 

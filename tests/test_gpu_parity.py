@@ -316,3 +316,26 @@ def test_row_partition_bitwise_and_emulated_allgather(G, cfg1_mesh):
             y[:, rows[r]] = yl
         # same CSR rows; only the matvec's term grouping (sized per rank) reorders sums
         assert np.linalg.norm(y.ravel() - y_full) <= 1e-14 * np.linalg.norm(y_full)
+
+
+def test_tiled_matvec_ranges_vs_dense(G, cfg1_mesh):
+    # the tensor-core tile path (lag terms, tdb_tbsr.cu) and the CSR path on the
+    # config-1 system, full / half / off-diagonal / quarter ranges vs the dense matrix
+    from paper_1503_07221_b200.temporal_basis import TimeGrid
+
+    grid = TimeGrid(T=3.9, N=40, p=0)
+    A = G[2].assemble_system(cfg1_mesh, grid)
+    dense = G[2].reconstruct_dense(A)
+    M = cfg1_mesh.num_vertices
+    rng = np.random.default_rng(11)
+    kinds = {}
+    for rows, cols in [((1, 40), (1, 40)), ((21, 40), (21, 40)), ((21, 40), (1, 20)), ((1, 10), (1, 10)),
+                       ((3, 37), (2, 29))]:
+        x = rng.standard_normal((cols[1] - cols[0] + 1) * M)
+        y = A.matvec(x, rows=rows, cols=cols)
+        ref = dense[(rows[0] - 1) * M:rows[1] * M, (cols[0] - 1) * M:cols[1] * M] @ x
+        assert np.linalg.norm(y - ref) <= 1e-12 * np.linalg.norm(ref), (rows, cols)
+        pl = A.matvec_plan(rows, cols)
+        kinds[(rows, cols)] = (pl.tiled_terms, pl.csr_terms)
+    assert kinds[((1, 40), (1, 40))][0] > 0, kinds       # lag terms on the tensor cores
+    assert kinds[((1, 10), (1, 10))][0] == 0, kinds      # short diagonal range: CSR only
