@@ -914,24 +914,48 @@ struct PatternArgs {
   int nacc, nm;
 };
 
+// Bitmap pattern of row j for the launch's positions: bit (s, l) is set iff some
+// admissible pair (ex, ey), ey in star(j), ex in star(l), covers position s.  A
+// thread takes one ex, merges the admissible position ranges of its <= kStarBm
+// combos (ex, star(j)) and sets the 3 vertex bits once per position of the union
+// (the same set of bits as one pass per combo, with ~1/valence the shared-memory
+// atomics).
+constexpr int kStarBm = 16;
 __device__ void build_bitmaps(const PatternArgs& a, int j, unsigned* bm) {
   const int nwords = a.s_count * a.words;
   for (int i = threadIdx.x; i < nwords; i += blockDim.x) bm[i] = 0u;
   __syncthreads();
-  const long long E2 = (long long)a.E * a.E;
-  (void)E2;
-  for (int k = a.star_off[j]; k < a.star_off[j + 1]; ++k) {
-    const int ey = a.star_ids[k];
-    const FRange* row = a.frange + (long long)a.ey_map[ey] * a.E;
+  const int kb = a.star_off[j], ke = a.star_off[j + 1];
+  const int s_end = a.s_begin + a.s_count;
+  for (int k0 = kb; k0 < ke; k0 += kStarBm) {
+    const int k1 = min(ke, k0 + kStarBm);
+    const FRange* rowp[kStarBm];
+    for (int k = k0; k < k1; ++k) rowp[k - k0] = a.frange + (long long)a.ey_map[a.star_ids[k]] * a.E;
     for (int ex = threadIdx.x; ex < a.E; ex += blockDim.x) {
-      const FRange fr = row[ex];
-      const int cnt = fr.lo_cnt >> 16;
-      if (cnt == 0) continue;
-      const int s_lo = fr.lo_cnt & 0xffff;
-      const int lo = max(s_lo, a.s_begin), hi = min(s_lo + cnt, a.s_begin + a.s_count);
-      if (lo >= hi) continue;
+      int lo[kStarBm], hi[kStarBm];
+      int umin = s_end, umax = a.s_begin;
+#pragma unroll
+      for (int q = 0; q < kStarBm; ++q) {
+        lo[q] = 0;
+        hi[q] = 0;
+        if (k0 + q < k1) {
+          const FRange fr = rowp[q][ex];
+          const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
+          lo[q] = max(s_lo, a.s_begin);
+          hi[q] = min(s_lo + cnt, s_end);
+          if (lo[q] < hi[q]) {
+            umin = min(umin, lo[q]);
+            umax = max(umax, hi[q]);
+          }
+        }
+      }
+      if (umin >= umax) continue;
       const int l0 = a.tri[3 * ex], l1 = a.tri[3 * ex + 1], l2 = a.tri[3 * ex + 2];
-      for (int s = lo; s < hi; ++s) {
+      for (int s = umin; s < umax; ++s) {
+        bool on = false;
+#pragma unroll
+        for (int q = 0; q < kStarBm; ++q) on |= (s >= lo[q]) & (s < hi[q]);
+        if (!on) continue;
         unsigned* b = bm + (s - a.s_begin) * a.words;
         atomicOr(b + (l0 >> 5), 1u << (l0 & 31));
         atomicOr(b + (l1 >> 5), 1u << (l1 & 31));

@@ -104,6 +104,7 @@ __global__ void k_krylov_flag(const double* st, double* err) {
 // coefficients (deterministic, no atomics) and the step is one launch.
 constexpr int kArnThreads = 256;
 constexpr int kArnMaxK = 64;  // restart lengths up to 64
+constexpr int kArnMaxCluster = 16;  // non-portable cluster size used by the launcher
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -165,8 +166,15 @@ __global__ void __launch_bounds__(kArnThreads) k_krylov_arnoldi(const double* __
     }
     cl.sync();
     for (int j = tid; j < nc; j += kArnThreads) {
+      // every rank's partial loaded first (independent DSMEM loads in flight),
+      // then summed in rank order
+      double pr[kArnMaxCluster];
+#pragma unroll
+      for (int r = 0; r < kArnMaxCluster; ++r) pr[r] = r < csize ? *cl.map_shared_rank(cb + j, r) : 0.0;
       double s_ = 0.0;
-      for (int r = 0; r < csize; ++r) s_ += *cl.map_shared_rank(cb + j, r);
+#pragma unroll
+      for (int r = 0; r < kArnMaxCluster; ++r)
+        if (r < csize) s_ += pr[r];
       h[j] = s_;
       if (pass < 2) hs[j] += s_;
     }

@@ -42,6 +42,7 @@ struct MvArgs {
   int words;
   int G;
   const FamCsr* fam;
+  const FamCsr* term_csr;   // (nterms,) the term's CSR with indptr at its position's first row
   const int* term_f;
   const int* term_s;
   const int* term_d;
@@ -110,8 +111,8 @@ struct MvCursor {
 
 template <int NM>
 __device__ __forceinline__ void mv_row_bounds(const MvArgs& a, int t, int j, int64_t& e0, int64_t& e1) {
-  const FamCsr* fc = a.fam + __ldg(a.term_f + t);
-  const long long row = (long long)__ldg(a.term_s + t) * a.nrows + j;
+  const FamCsr* fc = a.term_csr + t;  // one dependent level less than family -> position
+  const long long row = j;
   const int kt0 = __ldg(a.term_kt + 4 * t);
   if (kt0 == 0) {  // empty mask: nothing to do
     e0 = e1 = 0;
@@ -142,7 +143,7 @@ __device__ __forceinline__ bool mv_next_chunk(const MvArgs& a, int j, MvCursor& 
 
 template <int NM>
 __device__ __forceinline__ void mv_stage(const MvArgs& a, const MvChunk& ch, int* s_idx, double* s_val, int lane) {
-  const FamCsr* fc = a.fam + __ldg(a.term_f + ch.t);
+  const FamCsr* fc = a.term_csr + ch.t;
   const int32_t* gi = fc->indices + ch.b;
   const double* gv = fc->data + ch.b * NM;
   for (int q = lane; q < ch.n; q += 32) cp_async4(s_idx + q, gi + q);
@@ -399,6 +400,7 @@ struct TdbMatvecPlan {
   long long* d_xmap = nullptr;
   long long xstride = 0;
   FamCsr* d_fam = nullptr;
+  FamCsr* d_tcsr = nullptr;
   int* d_ints = nullptr;       // term_f, term_s, term_d, group_begin
   unsigned* d_mask = nullptr;
   double* d_xt = nullptr;
@@ -430,6 +432,7 @@ extern "C" int tdb_matvec_plan_destroy(TdbMatvecPlan* p) {
   dev_free(p->d_tact);
   dev_free(p->d_typart);
   dev_free(p->d_fam);
+  dev_free(p->d_tcsr);
   dev_free(p->d_ints);
   dev_free(p->d_mask);
   dev_free(p->d_xt);
@@ -548,7 +551,13 @@ static int plan_create_impl(TdbSystem* sys, const TdbMatvecDesc* d, TdbMatvecPla
     if ((n) > 0 && (src) != nullptr)                                                               \
       cudaMemcpyAsync((dst), (src), (size_t)(n) * sizeof(T), cudaMemcpyHostToDevice, st);          \
   } while (0)
+  std::vector<FamCsr> tcsr(std::max(1, nt));
+  for (int t = 0; t < nt; ++t) {
+    const FamilyStore& fs_ = sys->fam[d->term_family[t]];
+    tcsr[t] = {fs_.indptr + (size_t)d->term_pos[t] * NR, fs_.indices, fs_.data};
+  }
   ALLOC_COPY(p->d_fam, fam.data(), sys->F, FamCsr);
+  ALLOC_COPY(p->d_tcsr, tcsr.data(), nt, FamCsr);
   ALLOC_COPY(p->d_ints, ints.data(), ints.size(), int);
   ALLOC_COPY(p->d_mask, d->term_mask, (size_t)nt * d->words, unsigned);
   ALLOC_COPY(p->d_xt, (const double*)nullptr, (size_t)M * (nc + 1) * NP1, double);
@@ -572,6 +581,7 @@ static int plan_create_impl(TdbSystem* sys, const TdbMatvecDesc* d, TdbMatvecPla
   a.words = d->words;
   a.G = G;
   a.fam = p->d_fam;
+  a.term_csr = p->d_tcsr;
   a.term_f = p->d_ints;
   a.term_s = p->d_ints + nt;
   a.term_d = p->d_ints + 2 * nt;
