@@ -20,6 +20,7 @@ tensors) and accepts/returns numpy arrays for reference-style callers.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import os
 from dataclasses import dataclass, field
 
@@ -78,6 +79,13 @@ def is_zero_position(grid: TimeGrid, diameter: float, kt: int, it: int) -> bool:
 
 
 def canonical_positions(grid: TimeGrid, diameter: float) -> list:
+    """Sorted canonical block positions (pure function of the grid and the diameter,
+    cached: repeated assemblies of one system skip the O(N^2) predicate loop)."""
+    return list(_canonical_positions(grid, float(diameter)))
+
+
+@functools.lru_cache(maxsize=64)
+def _canonical_positions(grid: TimeGrid, diameter: float) -> tuple:
     pos = set()
     for kt in range(1, grid.N + 1):
         for it in range(max(1, kt - grid.N), min(grid.N, kt + 1) + 1):
@@ -86,7 +94,7 @@ def canonical_positions(grid: TimeGrid, diameter: float) -> list:
             c = canonical_position(grid, kt, it)
             if c is not None:
                 pos.add(c)
-    return sorted(pos)
+    return tuple(sorted(pos))
 
 
 @dataclass(frozen=True)
@@ -108,11 +116,17 @@ class DistributionPlan:
 
 def plan_distribution(grid: TimeGrid, mesh: SurfaceMesh, P: int) -> DistributionPlan:
     """Inner positions diagonal by diagonal in P contiguous near-equal chunks;
-    boundary positions greedily to the least-loaded rank (block_system.py:86-129)."""
+    boundary positions greedily to the least-loaded rank (block_system.py:86-129).
+    The mesh enters only through its diameter, so the plan is cached on (grid, diameter, P)."""
     if P < 1:
         raise ValueError(f"worker count {P} must be >= 1")
+    return _plan_distribution(grid, float(mesh.diameter), int(P))
+
+
+@functools.lru_cache(maxsize=64)
+def _plan_distribution(grid: TimeGrid, diameter: float, P: int) -> DistributionPlan:
     n = grid.N
-    ntz = n_tilde_z(grid, mesh.diameter)
+    ntz = n_tilde_z(grid, diameter)
     inner = [(it + d, it) for d in range(-1, ntz) for it in range(2, n) if 2 <= it + d <= n - 1]
     owners = {}
     base, extra = divmod(len(inner), P)

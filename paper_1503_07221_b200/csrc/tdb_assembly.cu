@@ -33,6 +33,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <vector>
+#include <mutex>
+#include <cstring>
 
 #include "tdb_common.cuh"
 #include "tdb_geometry.cuh"
@@ -1843,6 +1845,43 @@ static void select_split(const TdbPsiPack& pk, int nt, int nsub, int* R_out, int
   family_monomials(pk, nt, nsub, 1, mono_out);
 }
 
+// The split depends only on the family's tables: repeated system creations with
+// the same tables (same grid and p) reuse it.  The key holds the full coefficient
+// bytes (compared on a hit, so a hash collision cannot alias two families).
+static void select_split_cached(const TdbPsiPack& pk, int nt, int nsub, int* R_out, int* D_out, int* K_out,
+                                std::vector<long double>& mono) {
+  struct Entry {
+    std::vector<double> key;
+    int R, D, K;
+    std::vector<long double> mono;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  std::vector<double> key;
+  key.reserve((size_t)nt * nsub * (kDeg + 1) + 3);
+  key.push_back((double)nt);
+  key.push_back((double)nsub);
+  key.push_back(pk.width[0]);
+  for (int t = 0; t < nt; ++t)
+    key.insert(key.end(), pk.coeffs + (size_t)t * pk.max_nsub * (kDeg + 1),
+               pk.coeffs + ((size_t)t * pk.max_nsub + nsub) * (kDeg + 1));
+  {
+    std::lock_guard<std::mutex> g(mu);
+    for (const Entry& e : cache)
+      if (e.key.size() == key.size() && std::memcmp(e.key.data(), key.data(), key.size() * sizeof(double)) == 0) {
+        *R_out = e.R;
+        *D_out = e.D;
+        *K_out = e.K;
+        mono = e.mono;
+        return;
+      }
+  }
+  select_split(pk, nt, nsub, R_out, D_out, K_out, mono);
+  std::lock_guard<std::mutex> g(mu);
+  if (cache.size() >= 64) cache.erase(cache.begin());
+  cache.push_back(Entry{std::move(key), *R_out, *D_out, *K_out, mono});
+}
+
 int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemblyDesc* desc,
                            TdbSystem* sys) {
   cudaStream_t st = ctx->stream;
@@ -1934,7 +1973,7 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
     // (select_split, checked on 65 points per subinterval).
     int R = 1, D = 16, K = 17;
     std::vector<long double> mono_all;
-    select_split(pk, nt, fd.nsub, &R, &D, &K, mono_all);
+    select_split_cached(pk, nt, fd.nsub, &R, &D, &K, mono_all);
     const int nsub_ref = fd.nsub;
     fd.nsub = nsub_ref * R;  // refined subintervals (R a power of two: exact w / R)
     fd.w = pk.width[0] / R;
