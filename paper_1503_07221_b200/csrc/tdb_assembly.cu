@@ -914,6 +914,8 @@ struct PatternArgs {
   const double* normals;
   const double* curls;
   int nacc, nm;
+  const int* row_order;   // CTA -> local row (Morton order: CTAs that run together share
+                          // test triangles, so their partial records are re-read from L2)
 };
 
 // Bitmap pattern of row j for the launch's positions: bit (s, l) is set iff some
@@ -970,7 +972,7 @@ __device__ void build_bitmaps(const PatternArgs& a, int j, unsigned* bm) {
 
 __global__ void k_pattern_count(PatternArgs a) {
   extern __shared__ unsigned bm[];
-  const int rloc = blockIdx.x, j = a.rows[rloc];
+  const int rloc = a.row_order ? a.row_order[blockIdx.x] : (int)blockIdx.x, j = a.rows[rloc];
   build_bitmaps(a, j, bm);
   __shared__ int red[32];
   for (int sl = 0; sl < a.s_count; ++sl) {
@@ -1186,7 +1188,7 @@ __global__ void __launch_bounds__(256, TDB_FILL_MINB) k_pattern_fill(PatternArgs
   int* pref = reinterpret_cast<int*>(smem_u + a.s_count * a.words);       // [s_count][words]
   unsigned* un = reinterpret_cast<unsigned*>(pref + a.s_count * a.words);  // [words] union
   int* upref = reinterpret_cast<int*>(un + a.words);                       // [words + 1]
-  const int rloc = blockIdx.x, j = a.rows[rloc];
+  const int rloc = a.row_order ? a.row_order[blockIdx.x] : (int)blockIdx.x, j = a.rows[rloc];
   __shared__ RowStar rs;
   if (threadIdx.x == 0) {
     const int b = a.star_off[j], e = a.star_off[j + 1];
@@ -1531,6 +1533,7 @@ static PatternArgs pattern_args(TdbSystem* sys, int f) {
   ga.curls = sys->curls;
   ga.nacc = sys->nacc;
   ga.nm = sys->nm;
+  ga.row_order = sys->d_rperm;
   return ga;
 }
 
