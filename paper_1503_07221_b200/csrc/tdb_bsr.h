@@ -50,7 +50,9 @@ struct TbsrMvArgs {
 };
 
 int tbsr_build(TdbSystem* sys, int f);
-int tbsr_mv_launch(const TbsrMvArgs& a, cudaStream_t st);
+int tbsr_mv_launch(const TbsrMvArgs& a, cudaStream_t st);              // tiles + ordered reduce
+int tbsr_mv_tiles(const TbsrMvArgs& a, cudaStream_t st, bool reduce);  // tile kernel (optionally + reduce)
+int tbsr_mv_reduce(const TbsrMvArgs& a, cudaStream_t st);              // ordered reduce into y
 
 int bsr_build(TdbSystem* sys);
 int bsr_mv_launch(const BsrMvArgs& a, cudaStream_t st);

@@ -410,6 +410,9 @@ struct TdbMatvecPlan {
   // p = 0 Toeplitz-ordered tensor-core path for the lag terms (tdb_tbsr.cu)
   bool tbsr = false;
   int n_tiled = 0, n_csr = 0, n_csr_all = 0;
+  // the tile kernel runs on its own stream, concurrently with the CSR kernel
+  cudaStream_t tst = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   TbsrMvArgs targs{};
   int* d_toff = nullptr;
   unsigned* d_tact = nullptr;
@@ -428,6 +431,9 @@ struct TdbMatvecPlan {
 extern "C" int tdb_matvec_plan_destroy(TdbMatvecPlan* p) {
   if (!p) return TDB_OK;
   cudaDeviceSynchronize();  // the system may already be gone: no p->sys access here
+  if (p->tst) cudaStreamDestroy(p->tst);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
   dev_free(p->d_toff);
   dev_free(p->d_tact);
   dev_free(p->d_typart);
@@ -847,6 +853,13 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   ta.xp = p->d_xp;
   ta.xs = xs_b;
   ta.ypart = p->d_typart;
+  if (cudaStreamCreateWithFlags(&p->tst, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    tdb_matvec_plan_destroy(p);
+    set_error("matvec plan: stream/event creation failed");
+    return TDB_E_CUDA;
+  }
   p->tbsr = true;
   p->n_tiled = nt - (int)cf.size();
   p->n_csr = (int)cf.size();
@@ -880,6 +893,31 @@ extern "C" int tdb_matvec(TdbMatvecPlan* p, const double* x, double* y) {
     p->bargs.y = y;
     return bsr_mv_launch(p->bargs, st);
   }
+  // Eager calls fork the tile kernel onto the plan's stream (concurrent with the CSR
+  // kernel); inside a CUDA-graph capture (the recursive preconditioner) the two
+  // stay on the capturing stream, which measured faster for the captured solve.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  TDB_CUDA_CHECK(cudaStreamIsCapturing(st, &cap));
+  const bool fork = p->tbsr && cap == cudaStreamCaptureStatusNone;
+  if (p->tbsr && !fork) {
+    dim3 blk(32, 8), grd((a.M + 31) / 32, (ncols + 31) / 32);
+    k_transpose_in<<<grd, blk, 0, st>>>(x, p->d_xp, a.M, ncols, p->targs.xs, p->d_xmap_p, p->xstride);
+    TDB_CUDA_CHECK(cudaGetLastError());
+    p->targs.y = y;
+    int rc = tbsr_mv_tiles(p->targs, st, false);
+    if (rc) return rc;
+  }
+  if (fork) {  // fork: the lag-term tiles on the plan's stream, concurrent with the CSR kernel
+    TDB_CUDA_CHECK(cudaEventRecord(p->ev_fork, st));
+    TDB_CUDA_CHECK(cudaStreamWaitEvent(p->tst, p->ev_fork, 0));
+    dim3 blk(32, 8), grd((a.M + 31) / 32, (ncols + 31) / 32);
+    k_transpose_in<<<grd, blk, 0, p->tst>>>(x, p->d_xp, a.M, ncols, p->targs.xs, p->d_xmap_p, p->xstride);
+    TDB_CUDA_CHECK(cudaGetLastError());
+    p->targs.y = y;
+    int rc = tbsr_mv_tiles(p->targs, p->tst, false);
+    if (rc) return rc;
+    TDB_CUDA_CHECK(cudaEventRecord(p->ev_join, p->tst));
+  }
   {
     dim3 blk(32, 8), grd((a.M + 31) / 32, (ncols + 31) / 32);
     k_transpose_in<<<grd, blk, 0, st>>>(x, p->d_xt, a.M, ncols, a.xs, p->d_xmap, p->xstride);
@@ -897,12 +935,9 @@ extern "C" int tdb_matvec(TdbMatvecPlan* p, const double* x, double* y) {
     }
   }
   TDB_CUDA_CHECK(cudaGetLastError());
-  if (p->tbsr) {  // lag terms on the tensor cores, added to the CSR kernel's y
-    dim3 blk(32, 8), grd((a.M + 31) / 32, (ncols + 31) / 32);
-    k_transpose_in<<<grd, blk, 0, st>>>(x, p->d_xp, a.M, ncols, p->targs.xs, p->d_xmap_p, p->xstride);
-    TDB_CUDA_CHECK(cudaGetLastError());
-    p->targs.y = y;
-    return tbsr_mv_launch(p->targs, st);
+  if (p->tbsr) {  // (join,) then the tiles' partials are added to the CSR kernel's y in part order
+    if (fork) TDB_CUDA_CHECK(cudaStreamWaitEvent(st, p->ev_join, 0));
+    return tbsr_mv_reduce(p->targs, st);
   }
   return TDB_OK;
 }

@@ -215,7 +215,7 @@ __global__ void k_tbsr_reduce(TbsrMvArgs a) {
 }
 
 template <int TT>
-static int launch_tt(const TbsrMvArgs& a, cudaStream_t st) {
+static int launch_tt(const TbsrMvArgs& a, cudaStream_t st, bool reduce) {
   const size_t smem = (size_t)a.npos * (TT * 8 + 1) * sizeof(int);
   static bool attr = false;
   if (!attr) {
@@ -225,6 +225,7 @@ static int launch_tt(const TbsrMvArgs& a, cudaStream_t st) {
   const long long ctas = (((long long)a.nRB * a.G + kTbsrWarps - 1) / kTbsrWarps) * a.ntg;
   k_tbsr_mv<TT><<<(unsigned)ctas, kTbsrWarps * 32, smem, st>>>(a);
   TDB_CUDA_CHECK(cudaGetLastError());
+  if (!reduce) return TDB_OK;
   const long long total = (long long)a.nRB * a.ntg * TT * 64;
   k_tbsr_reduce<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0, st>>>(a);
   TDB_CUDA_CHECK(cudaGetLastError());
@@ -316,15 +317,24 @@ int tbsr_build(TdbSystem* sys, int f) {
   return TDB_OK;
 }
 
-int tbsr_mv_launch(const TbsrMvArgs& a, cudaStream_t st) {
+int tbsr_mv_tiles(const TbsrMvArgs& a, cudaStream_t st, bool reduce) {
   switch (a.TT) {
-    case 2: return launch_tt<2>(a, st);
-    case 4: return launch_tt<4>(a, st);
-    case 6: return launch_tt<6>(a, st);
-    case 8: return launch_tt<8>(a, st);
-    case 10: return launch_tt<10>(a, st);
-    default: return launch_tt<12>(a, st);
+    case 2: return launch_tt<2>(a, st, reduce);
+    case 4: return launch_tt<4>(a, st, reduce);
+    case 6: return launch_tt<6>(a, st, reduce);
+    case 8: return launch_tt<8>(a, st, reduce);
+    case 10: return launch_tt<10>(a, st, reduce);
+    default: return launch_tt<12>(a, st, reduce);
   }
 }
+
+int tbsr_mv_reduce(const TbsrMvArgs& a, cudaStream_t st) {
+  const long long total = (long long)a.nRB * a.ntg * a.TT * 64;
+  k_tbsr_reduce<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0, st>>>(a);
+  TDB_CUDA_CHECK(cudaGetLastError());
+  return TDB_OK;
+}
+
+int tbsr_mv_launch(const TbsrMvArgs& a, cudaStream_t st) { return tbsr_mv_tiles(a, st, true); }
 
 }  // namespace tdb
