@@ -280,7 +280,10 @@ template <int NP1, int NC>
 #ifndef TDB_MV_MIN_BLOCKS
 #define TDB_MV_MIN_BLOCKS 16
 #endif
-__global__ void __launch_bounds__(32, TDB_MV_MIN_BLOCKS) k_matvec(MvArgs a) {
+#ifndef TDB_MV_MIN_BLOCKS_NC1
+#define TDB_MV_MIN_BLOCKS_NC1 16
+#endif
+__global__ void __launch_bounds__(32, NC <= 1 ? TDB_MV_MIN_BLOCKS_NC1 : TDB_MV_MIN_BLOCKS) k_matvec(MvArgs a) {
   // one warp per CTA: the warp index is blockIdx.x, so every loop bound below is
   // provably warp-uniform (plain SHFL / no divergence handling)
   constexpr int NM = NP1 * NP1;
