@@ -339,3 +339,37 @@ def test_tiled_matvec_ranges_vs_dense(G, cfg1_mesh):
         kinds[(rows, cols)] = (pl.tiled_terms, pl.csr_terms)
     assert kinds[((1, 40), (1, 40))][0] > 0, kinds       # lag terms on the tensor cores
     assert kinds[((1, 10), (1, 10))][0] == 0, kinds      # short diagonal range: CSR only
+
+
+def test_tiled_vs_csr_only_plan_agree(G, cfg1_mesh, tmp_path):
+    # the same matvecs with every term on the CSR kernel (TDB_MV_TBSR=0, separate
+    # process: the switch is read once per process) agree with the default plans
+    import os
+    import subprocess
+    import sys
+
+    from paper_1503_07221_b200.temporal_basis import TimeGrid
+
+    grid = TimeGrid(T=3.9, N=40, p=0)
+    A = G[2].assemble_system(cfg1_mesh, grid)
+    M = cfg1_mesh.num_vertices
+    x = np.random.default_rng(5).standard_normal(grid.L * M)
+    np.save(tmp_path / "x.npy", x)
+    ys = [A.matvec(x), A.matvec(x[: 20 * M], rows=(21, 40), cols=(1, 20))]
+    assert A.matvec_plan((1, 40), (1, 40)).tiled_terms > 0
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "from paper_1503_07221_b200.mesh import icosphere\n"
+        "from paper_1503_07221_b200.block_system import assemble_system\n"
+        "from paper_1503_07221_b200.temporal_basis import TimeGrid\n"
+        "mesh = icosphere(2); g = TimeGrid(T=3.9, N=40, p=0); A = assemble_system(mesh, g)\n"
+        "x = np.load(%r); M = mesh.num_vertices\n"
+        "assert A.matvec_plan((1, 40), (1, 40)).tiled_terms == 0\n"
+        "np.save(%r, np.stack([A.matvec(x), np.pad(A.matvec(x[:20 * M], rows=(21, 40), cols=(1, 20)), (0, 20 * M))]))\n"
+    ) % (root, os.path.join(root, "tests"), str(tmp_path / "x.npy"), str(tmp_path / "y.npy"))
+    env = dict(os.environ, TDB_MV_TBSR="0")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=root)
+    yc = np.load(tmp_path / "y.npy")
+    assert np.linalg.norm(ys[0] - yc[0]) <= 1e-13 * np.linalg.norm(yc[0])
+    assert np.linalg.norm(ys[1] - yc[1][: 20 * M]) <= 1e-13 * np.linalg.norm(yc[1][: 20 * M])
