@@ -232,7 +232,8 @@ int tdb_matvec(TdbMatvecPlan* plan, const double* x_dev, double* y_dev);
 /* canonical stored bytes and logical flops of one application of this plan */
 int tdb_matvec_plan_work(const TdbMatvecPlan* plan, double* algorithmic_bytes, double* flops);
 /* how the plan applies its terms: *tiled_terms lag terms on the FP64 tensor-core
- * tiles (tdb_tbsr.cu), *csr_terms on the CSR kernel (tdb_matvec.cu) */
+ * tiles (tdb_tbsr.cu), *csr_terms on the CSR kernel (tdb_matvec.cu).  Introspection
+ * only (no counterpart in the reference, whose matvec is block_system.py:180-216). */
 int tdb_matvec_plan_kind(const TdbMatvecPlan* plan, int32_t* tiled_terms, int32_t* csr_terms);
 
 /* ---- device-side GMRES cycle bookkeeping (solvers.py:172-223) ------------
