@@ -124,6 +124,34 @@ __device__ __forceinline__ void tbsr_load(const TbsrMvArgs& a, const int* __rest
   }
 }
 
+// Cursor over a warp's tile range: batches of 32 tiles (coalesced column /
+// position loads), live tiles (position in the plan) picked by ballot.  Warp-uniform.
+struct TbsrCursor {
+  long long pb, q1;
+  int my_cb, my_s;
+  unsigned my_act, live;
+};
+
+__device__ __forceinline__ bool tbsr_next(const TbsrMvArgs& a, const unsigned* s_act, int lane, TbsrCursor& c,
+                                          TbsrTile& t) {
+  while (c.live == 0u) {
+    if (c.pb >= c.q1) return false;
+    const int n = (int)min(32LL, c.q1 - c.pb);
+    c.my_cb = lane < n ? __ldg(a.col + c.pb + lane) : 0;
+    c.my_s = lane < n ? __ldg(a.pos + c.pb + lane) : 0;
+    c.my_act = lane < n ? s_act[c.my_s] : 0u;
+    c.live = __ballot_sync(0xffffffffu, c.my_act != 0u);
+    c.pb += 32;
+  }
+  const int i = __ffs(c.live) - 1;
+  c.live &= c.live - 1;
+  t.s = __shfl_sync(0xffffffffu, c.my_s, i);
+  t.cb = __shfl_sync(0xffffffffu, c.my_cb, i);
+  t.act = __shfl_sync(0xffffffffu, c.my_act, i);
+  t.p = c.pb - 32 + i;
+  return true;
+}
+
 template <int TT>
 __global__ void __launch_bounds__(kTbsrWarps * 32) k_tbsr_mv(TbsrMvArgs a) {
   extern __shared__ __align__(16) int tb_smem[];
@@ -148,46 +176,23 @@ __global__ void __launch_bounds__(kTbsrWarps * 32) k_tbsr_mv(TbsrMvArgs a) {
   const long long q0 = r0 + (r1 - r0) * g / a.G, q1 = r0 + (r1 - r0) * (g + 1) / a.G;
   const double* xq = a.xp + (long long)tq * a.xs;
   // Software pipeline over the warp's live tiles (tiles whose position is a lag
-  // term of this plan): the next tile's A and B loads are in flight while the
-  // current tile's DMMAs issue.
-  TbsrTile cur{0, 0, 0u, 0};
-  bool have = false;
-  double av = 0.0, bv[TT];
-  for (long long pb = q0; pb < q1; pb += 32) {
-    const int n = (int)min(32LL, q1 - pb);
-    const int my_cb = lane < n ? __ldg(a.col + pb + lane) : 0;
-    const int my_s = lane < n ? __ldg(a.pos + pb + lane) : 0;
-    const unsigned my_act = lane < n ? s_act[my_s] : 0u;
-    unsigned live = __ballot_sync(0xffffffffu, my_act != 0u);
-    while (live) {
-      const int i = __ffs(live) - 1;
-      live &= live - 1;
-      TbsrTile nx;
-      nx.s = __shfl_sync(0xffffffffu, my_s, i);
-      nx.cb = __shfl_sync(0xffffffffu, my_cb, i);
-      nx.act = __shfl_sync(0xffffffffu, my_act, i);
-      nx.p = pb + i;
-      double avn, bvn[TT];
-      tbsr_load<TT>(a, s_off, xq, nx, gq, lane, avn, bvn);
-      if (have) {
+  // term of this plan), ping-pong buffers A / B: the next tile's A and B loads are
+  // in flight while the current tile's DMMAs issue (no register copies).
+  TbsrCursor cs{q0, q1, 0, 0, 0u, 0u};
+  TbsrTile tA, tB;
+  double avA, avB, bvA[TT], bvB[TT];
+  bool hA = tbsr_next(a, s_act, lane, cs, tA);
+  if (hA) tbsr_load<TT>(a, s_off, xq, tA, gq, lane, avA, bvA);
+  while (hA) {
+    const bool hB = tbsr_next(a, s_act, lane, cs, tB);
+    if (hB) tbsr_load<TT>(a, s_off, xq, tB, gq, lane, avB, bvB);
 #pragma unroll
-        for (int u = 0; u < TT; ++u) {
-#ifdef TDB_TBSR_PRED
-          if ((cur.act >> u) & 1u)
-#endif
-            dmma884(acc[u][0], acc[u][1], av, bv[u]);
-        }
-      }
-      cur = nx;
-      av = avn;
+    for (int u = 0; u < TT; ++u) dmma884(acc[u][0], acc[u][1], avA, bvA[u]);
+    if (!hB) break;
+    hA = tbsr_next(a, s_act, lane, cs, tA);
+    if (hA) tbsr_load<TT>(a, s_off, xq, tA, gq, lane, avA, bvA);
 #pragma unroll
-      for (int u = 0; u < TT; ++u) bv[u] = bvn[u];
-      have = true;
-    }
-  }
-  if (have) {
-#pragma unroll
-    for (int u = 0; u < TT; ++u) dmma884(acc[u][0], acc[u][1], av, bv[u]);
+    for (int u = 0; u < TT; ++u) dmma884(acc[u][0], acc[u][1], avB, bvB[u]);
   }
   // partial tiles of the G parts: summed in part order by k_tbsr_reduce
   const long long key = (long long)J * a.ntg + tg;
