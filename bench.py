@@ -1,24 +1,29 @@
 #!/usr/bin/env python
 """Benchmark: lag-block assembly throughput (triangle-pair x lag quadratures/s) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
 
-Workload (BASELINE.json configs[1], the metric's single-GPU configuration):
-icosphere refined 3x (1280 triangles, 642 P1 dofs), dt = 0.05, N = 80, p = 0,
+Workload: BASELINE.json gives no config for its metric, so the bench runs the
+largest configuration that fits one GPU, configs[3] (config 4): icosphere
+refined 4x (5120 triangles, 2562 P1 dofs), dt = 0.025, N = 160, p = 0,
 reference quadrature rules (q_reg 4, q_sing 5, n_rad auto).  A "step" is one
 complete assembly of every canonical block position (pair plan with exact
 distance bounds, all-lags quadrature, singular reduction, CSR pattern and
 compensated gather) from device-resident mesh/tables.  `value` = units / s,
 units = admissible (triangle pair, block position) quadratures.  `e2e` is the
 same metric through the public API (assemble_system from host arrays, all
-blocks copied back to host as CSR).
+blocks copied back to host as CSR).  --config 2 keeps the round-1 workload.
 
-N > 1 (torchrun, one process per GPU): SURVEY 8e row-block sharding - each rank
+N > 1 (torchrun, one process per GPU; `--gpus N` without torchrun re-launches
+itself under torch.distributed.run): SURVEY 8e row-block sharding - each rank
 assembles its own test-vertex rows of every block with no communication (strong
 scaling over the fixed config); times are the max over ranks; value counts each
-global unit once (halo duplicates reported separately).  --impl reference
-times the reference's own compiled kernel (oracle/_ref) on the host cores on a
-stratified sample of the same workload (rank 0 only).
+global unit once (halo duplicates reported separately).
+
+--impl reference times the REFERENCE package itself (tdbem from oracle/_ref/pkg
+or baseline/_ref, never this repo's package): its assemble_subblocks at every
+canonical position for a seeded sample of test rows per step, on all host cores
+(oracle/reference_arm.py; rank 0 only).
 """
 
 from __future__ import annotations
@@ -125,101 +130,65 @@ def max_over_ranks(world, v: float, device) -> float:
     return float(t.item())
 
 
-def load_traffic():
-    path = os.path.join(ROOT, "profiles", "ncu_quad_summary.json")
+def load_traffic(c: int):
+    """DRAM bytes per k_quad launch of config c from its committed ncu --set full capture, or None."""
+    path = os.path.join(ROOT, "profiles", "r02", f"ncu_quad_cfg{c}.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
-        return d.get("dram_bytes_per_launch"), d
+        return d.get("dram_bytes_per_launch"), path
     except (OSError, ValueError):
         return None, None
 
 
-def cpu_baseline(cfg, mesh, grid, tables, plan, units_case, kind, workers, sample_scale=1.0, seed=0):
-    from oracle import cpu_baseline as CB
-
-    n = {"regular": int(2000 * sample_scale), "coincident": max(2, int(12 * sample_scale)),
-         "edge": max(2, int(12 * sample_scale)), "vertex": max(2, int(24 * sample_scale))}
-    tasks = CB.build_tasks(mesh, grid, tables, plan, n, seed=seed)
-    meas = CB.measure(tasks, kind=kind, workers=workers)
-    seconds, rate = CB.estimate(meas, units_case)
-    sample_units = sum(u for u, _ in meas.values())
-    sample_secs = sum(t for _, t in meas.values())
-    return rate, seconds, {
-        "sample": (f"stratified: {n} pairs per case, all admissible positions "
-                   f"({sample_units} units, {sample_secs:.1f} s wall on {workers} process(es)); "
-                   f"full {cfg.name} extrapolated by exact per-case unit counts; kernel "
-                   f"{'reference _core (oracle/_ref)' if kind == 'reference' else 'C port (oracle)'}"),
-        "strata": {c: {"units": u, "seconds": round(t, 4)} for c, (u, t) in meas.items()},
-        "extrapolated_seconds_full_assembly": seconds,
-    }
+REF_ROWS = {1: 24, 2: 8, 3: 4, 4: 2, 5: 1}  # sampled test vertices per reference step
 
 
 def run_reference(args, world, rank):
+    """The reference package's own assembly on the host cores (oracle/reference_arm.py)."""
     if rank != 0:
         return 0
-    from paper_1503_07221_b200.assembly import build_plan
-    from paper_1503_07221_b200.block_system import canonical_positions
-    from paper_1503_07221_b200.configs import get_config
-    from paper_1503_07221_b200.kernel_weights import tables_for
-    from oracle import assembly as OA
+    from oracle import reference_arm as RA
 
-    cfg = get_config(args.config)
-    mesh, grid = cfg.mesh(), cfg.grid()
-    tables = tables_for(grid)
-    plan = build_plan(mesh, grid, tables, canonical_positions(grid, mesh.diameter))
-    units_case = unit_counts_host(mesh, plan)
-    kind = "reference" if OA.ref_core() is not None else "port"
-    workers = os.cpu_count() or 1
-    rates = []
-    info = None
+    try:
+        rs = RA.RowSampler(args.config, args.ref_rows or REF_ROWS[args.config])
+    except (ImportError, RuntimeError) as e:
+        print(json.dumps({"impl": "reference", "unavailable": str(e)}), flush=True)
+        return 0
+    units_full, npos = RA.full_units(args.config)
+    got_u, got_s = [], []
     for step in range(args.warmup + args.steps):
-        rate, seconds, info = cpu_baseline(cfg, mesh, grid, tables, plan, units_case,
-                                           "reference" if kind == "reference" else "c", workers,
-                                           sample_scale=args.ref_sample, seed=step)
+        prep = rs.prepare(step)  # pre-warmed bounds of this step's rows (untimed)
+        u, secs = rs.step(prep)
         if step >= args.warmup:
-            rates.append(rate)
-    value = float(np.median(rates))
-    total_units = sum(units_case.values())
+            got_u.append(u)
+            got_s.append(secs)
+    value = float(sum(got_u) / sum(got_s))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total_units / value, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * float(np.mean(got_s)), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8d meshes)",
-        "config": {"workload": cfg.name, "units_per_step": total_units, "p": grid.p,
-                   "l2": "n/a (CPU)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": kind,
-                         "sample": info["sample"]},
+        "config": {"workload": rs.name, "units_per_step": units_full, "p": 0, "positions": npos},
+        "sample_units_per_step": float(np.mean(got_u)),
+        "parallelism": f"{rs.workers} host processes (reference per-position pool)",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": rs.workers, "kind": "reference",
+                         "sample": rs.describe(args.steps)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "detail": info,
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def unit_counts_host(mesh, plan):
-    """Exact units per case with the oracle's (reference-order) distance bounds."""
-    from oracle import assembly as OA
-    from oracle import cpu_baseline as CB
-    from paper_1503_07221_b200.mesh import touching_pairs
+def cpu_baseline_line(c: int):
+    """Bounded reference sample for the cpu_baseline key of our own line (rank 0, N = 1)."""
+    from oracle import reference_arm as RA
 
-    slo = np.concatenate([f.slo for f in plan.families])
-    shi = np.concatenate([f.shi for f in plan.families])
-    tmin, tmax = OA.tri_distance_bounds(mesh)
-    total = 0
-    for a, b in zip(slo, shi):
-        total += int(((tmin <= b) & (tmax >= a)).sum())
-    out = {}
-    tp = touching_pairs(mesh)
-    for case in ("coincident", "edge", "vertex"):
-        ex, ey, _, _ = tp[case]
-        if len(ex) == 0:
-            out[case] = 0
-            continue
-        t0, t1 = CB.pair_bounds(mesh, ex, ey)
-        out[case] = int(((t0[:, None] <= shi[None, :]) & (t1[:, None] >= slo[None, :])).sum())
-    out["regular"] = total - sum(out.values())
-    return out
+    rs = RA.RowSampler(c, REF_ROWS[c])
+    rs.step(rs.prepare(0))  # warm the pool / page cache
+    u, secs = rs.step(rs.prepare(1))
+    return {"value": u / secs, "unit": UNIT, "cores": rs.workers, "kind": "reference",
+            "sample": rs.describe(1), "sample_units": u, "sample_seconds": secs}
 
 
 def sum_over_ranks(world, v: float, device) -> float:
@@ -264,15 +233,27 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--ref-sample", type=float, default=1.0)
+    ap.add_argument("--ref-rows", type=int, default=0, help="reference arm: sampled test vertices per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (the driver's own launch sets WORLD_SIZE)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
     world, rank, local = dist_init()
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args, world, rank)
 
@@ -341,11 +322,12 @@ def main():
     q_ms = float(np.mean(quad_ms))
     achieved = fl / (q_ms * 1e-3) / 1e12
     peak_meas = _lib.fp64_peak_tflops(ctx, repeats=5)
-    traffic, _ = load_traffic()
+    traffic, traffic_src = load_traffic(args.config)
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak_meas, "unit": "TFLOP/s",
                 "frac": achieved / peak_meas,
-                "peak_source": "measured in-run DFMA microbenchmark (tdb_fp64_peak); "
-                               "MEASURED_PEAKS.json has no FP64 entry",
+                "peak_source": "measured in-run, best of a DFMA and a DMMA (FP64 tensor core) "
+                               "microbenchmark (tdb_fp64_peak); MEASURED_PEAKS.json has no FP64 entry",
+                "traffic_source": traffic_src,
                 "peak_nominal": 37.2, "frac_of_nominal": achieved / 37.2,
                 "traffic": traffic if world == 1 else None, "kernel": "k_quad", "kernel_ms": q_ms,
                 "kernel_share_of_step": q_ms / float(np.mean(step_ms)),
@@ -369,8 +351,8 @@ def main():
               "achieved_TFLOPs": mv_flops / (mv_ms * 1e-3) / 1e12 / max(1, world),
               "frac_fp64_per_gpu": mv_flops / (mv_ms * 1e-3) / 1e12 / max(1, world) / peak_meas,
               "intensity_flop_per_byte": mv_flops / max(mv_bytes, 1.0),
-              "kernels": "lag terms of the inner family: FP64 DMMA tiles (k_tbsr_mv + k_tbsr_reduce); "
-                         "boundary terms: CSR (k_matvec)",
+              "kernels": "regular lag terms of the inner family: FP64 DMMA lag-band tiles (k_band_mv + "
+                         "k_band_reduce); boundary terms and the light-cone tie lag: CSR (k_matvec)",
               "includes": ("ncclAllGather of the iterate" if world > 1 else "transposes + CSR SpMM + DMMA tiles"
                            " + ordered reduce")}
 
@@ -446,15 +428,10 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import assembly as OA
-
-        kind = "reference" if OA.ref_core() is not None else "port"
-        uc = {"regular": int(stats["units_case"][0]), "coincident": int(stats["units_case"][1]),
-              "edge": int(stats["units_case"][2]), "vertex": int(stats["units_case"][3])}
-        rate, secs, info = cpu_baseline(cfg, mesh, grid, tables, plan, uc,
-                                        "reference" if kind == "reference" else "c", 1)
-        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": kind, "sample": info["sample"],
-               "extrapolated_seconds_full_assembly": secs}
+        try:
+            cpu = cpu_baseline_line(args.config)
+        except (ImportError, RuntimeError) as e:
+            cpu = {"value": None, "unavailable": str(e)}
 
     if rank == 0:
         line = {
@@ -463,11 +440,11 @@ def main():
             "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8d meshes)",
             "config": {"workload": cfg.name, "units_per_step": units, "p": grid.p,
-                       "positions": len(plan.where), "nnz": stats["nnz_total"],
-                       "parallelism": (f"row blocks x{world} (NCCL all-gather per matvec)" if world > 1
-                                       else "1 GPU"),
-                       "units_computed_incl_halo": units_computed,
-                       "l2": "flushed between timed steps (256 MB write)"},
+                       "positions": len(plan.where)},
+            "nnz": stats["nnz_total"],
+            "parallelism": (f"row blocks x{world} (NCCL all-gather per matvec)" if world > 1 else "1 GPU"),
+            "units_computed_incl_halo": units_computed,
+            "l2": "flushed between timed steps (256 MB write)",
             "roofline": roofline,
             "matvec": matvec,
             "solve": solve,

@@ -9,8 +9,8 @@
  * pointers; all others are host pointers owned by the caller.
  *
  * Reference interfaces replaced (paths under /root/reference/pkg/src/tdbem/):
- *   tdb_pair_block_contributions  <- _kernels/__init__.py:7-9,32
- *                                    (_core.pyx:81-193, _fallback.py:239-274)
+ *   tdb_pair_block_contributions  <- _kernels/__init__.py:1-34 dispatch
+ *                                    (_core.pyx:47-159, _fallback.py:46-81)
  *   tdb_system_assemble           <- block_system.py:228-275 assemble_system
  *                                    + assembly.py:240-306 assemble_subblocks
  *   tdb_system_copy_family        <- the CSR lists of BlockHessenbergMatrix
@@ -148,8 +148,9 @@ int tdb_abi_version(void);
 /* Device blocks freed by destroyed systems / plans are cached for reuse (up to
  * 8 GB); this returns them to the driver. */
 int tdb_release_cached_memory(void);
-/* Measured FP64 FMA throughput of the device (TFLOP/s, 2 flops per DFMA):
- * a dependent-chain microbenchmark over all SMs, best of `repeats`. */
+/* Measured FP64 throughput of the device (TFLOP/s): the better of a DFMA
+ * (2 flops per lane) and a DMMA m8n8k4 (512 flops per warp) microbenchmark of
+ * independent chains over all SMs, best of `repeats`. */
 int tdb_fp64_peak(TdbContext* ctx, int repeats, double* tflops);
 const char* tdb_last_error(void);
 int tdb_device_count(int* count);
@@ -183,6 +184,15 @@ int tdb_system_destroy(TdbSystem* sys);
 int tdb_system_stats(const TdbSystem* sys, TdbStats* out);
 /* nnz of family f (stored pattern incl. explicit zeros) */
 int tdb_system_family_nnz(const TdbSystem* sys, int32_t f, int64_t* nnz);
+/* Admissible (pair, position) units of every position of family f (npos,),
+ * i.e. len(block_pattern(mesh, grid, kt, it).element_pairs) of the reference
+ * (assembly.py:167-184) over this system's test triangles; valid after a run. */
+int tdb_system_position_units(TdbSystem* sys, int32_t f, int64_t* units);
+/* Evaluation split family f runs with (introspection; chosen at create so every
+ * table stays within 3e-15 of its max of the reference's Clenshaw value):
+ * subintervals refined R-fold, monomial degree D, monomials k < K in FP64 and
+ * K <= k <= D in FP32 (K = D + 1: all FP64). */
+int tdb_system_family_split(const TdbSystem* sys, int32_t f, int32_t* R, int32_t* D, int32_t* K);
 /* D2H copy of family f: indptr (npos*nrows+1,) int64 with rows (s, local row r);
  * indices (nnz,) int32 columns; data (nnz,(p+1)^2) */
 int tdb_system_copy_family(const TdbSystem* sys, int32_t f, int64_t* indptr,

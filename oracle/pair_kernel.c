@@ -3,7 +3,7 @@
  *
  * Plain-C, single-threaded restatement of the reference hot kernel
  * tdbem._kernels._core.pair_block_contributions
- * (/root/reference/pkg/src/tdbem/_kernels/_core.pyx:81-193, helpers :53-78),
+ * (/root/reference/pkg/src/tdbem/_kernels/_core.pyx:47-159, helpers :19-44),
  * point loop, table evaluation and accumulation order kept as in the Cython
  * source so the result agrees with the compiled reference to rounding.
  * Built by oracle/Makefile into oracle/liboracle.so; called from tests/ and

@@ -118,6 +118,8 @@ def _load():
         "tdb_system_stats": (i32, [P, C.POINTER(TdbStats)]),
         "tdb_system_family_nnz": (i32, [P, i32, C.POINTER(i64)]),
         "tdb_system_copy_family": (i32, [P, i32, i64p, i32p, f64p]),
+        "tdb_system_position_units": (i32, [P, i32, i64p]),
+        "tdb_system_family_split": (i32, [P, i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
         "tdb_system_family_device": (i32, [P, i32, C.POINTER(P), C.POINTER(P), C.POINTER(P)]),
         "tdb_matvec_plan_create": (i32, [P, C.POINTER(TdbMatvecDesc), C.POINTER(P)]),
         "tdb_matvec_plan_destroy": (i32, [P]),
@@ -151,6 +153,7 @@ EXPORTED = (
     "tdb_abi_version", "tdb_last_error", "tdb_device_count", "tdb_pair_block_contributions",
     "tdb_ctx_create", "tdb_ctx_destroy", "tdb_ctx_set_stream", "tdb_system_assemble",
     "tdb_system_destroy", "tdb_system_stats", "tdb_system_family_nnz", "tdb_system_copy_family",
+    "tdb_system_position_units", "tdb_system_family_split",
     "tdb_system_family_device", "tdb_matvec_plan_create", "tdb_matvec_plan_destroy", "tdb_matvec",
     "tdb_matvec_plan_work", "tdb_matvec_plan_kind", "tdb_tri_distance_bounds", "tdb_system_create", "tdb_system_run",
     "tdb_fp64_peak", "tdb_krylov_init", "tdb_krylov_givens", "tdb_krylov_update", "tdb_krylov_flag",

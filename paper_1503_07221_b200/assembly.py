@@ -341,6 +341,31 @@ class DeviceAssembly:
             _lib.ptr(data)), "copy_family")
         return indptr, indices[: nnz.value], data[: nnz.value]
 
+    def position_units(self) -> dict:
+        """(kt, it) -> admissible-pair count of every assembled position (block_pattern size,
+        ref/assembly.py:167-184) over this system's test triangles."""
+        out = {}
+        for f, fam in enumerate(self.plan.families):
+            if self.handle is None:
+                break
+            u = np.zeros(len(fam.positions), dtype=np.int64)
+            _lib.check(_lib.LIB.tdb_system_position_units(self.handle, f, _lib.ptr(u, _lib.C.c_int64)),
+                       "position_units")
+            out.update({pos: int(u[s]) for s, pos in enumerate(fam.positions)})
+        return out
+
+    def family_splits(self) -> dict:
+        """(ansatz kind, test kind) -> (R, D, K) evaluation split of each family (tdb_system_family_split)."""
+        out = {}
+        for f, fam in enumerate(self.plan.families):
+            if self.handle is None:
+                break
+            R, D, K = (_lib.C.c_int32() for _ in range(3))
+            _lib.check(_lib.LIB.tdb_system_family_split(self.handle, f, _lib.C.byref(R), _lib.C.byref(D),
+                                                        _lib.C.byref(K)), "family_split")
+            out[tuple(fam.kinds)] = (R.value, D.value, K.value)
+        return out
+
     def family_device(self, f: int):
         a, b, c = _lib.C.c_void_p(), _lib.C.c_void_p(), _lib.C.c_void_p()
         _lib.check(_lib.LIB.tdb_system_family_device(self.handle, f, _lib.C.byref(a), _lib.C.byref(b),

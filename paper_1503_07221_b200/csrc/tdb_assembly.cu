@@ -1983,6 +1983,9 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
     fd.inv_w = R / pk.width[0];
     fd.deg = D;
     fd.khead = K;
+    sys->fam[f].split_R = R;
+    sys->fam[f].split_D = D;
+    sys->fam[f].split_K = K;
     if (std::getenv("TDB_VERBOSE"))
       std::fprintf(stderr, "tdb: family %d npos %d nsub %d -> refine %d, degree %d, fp64 head %d\n", f,
                    hf.npos, nsub_ref, R, D, K);
@@ -2156,7 +2159,7 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
     if ((rc = dupload(&ws->owned, own.data(), own.size(), st))) return rc;
     sys->nrows = ws->nrows;
     // Morton (Z-order) ranks of the vertices: spatially close dofs get close ids,
-    // so a lag block's 8 x 4 tiles are ~50% full (tensor-core matvec, tdb_bsr.cu)
+    // so the band tiles of neighbouring test rows overlap (tensor-core matvec, tdb_band.cu)
     {
       std::vector<double> xyz(3 * V, 0.0);
       for (long long e = 0; e < E; ++e)
@@ -2295,6 +2298,57 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
   return TDB_OK;
 }
 
+// Admissible units per position of family f, from the pair plan of the last
+// run: len(block_pattern(mesh, grid, kt, it).element_pairs) of every position
+// (assembly.py:167-184), restricted to this system's test triangles.  A block
+// histogram of the range starts/ends in shared memory (difference array), one
+// global atomic per position and block.
+__global__ void k_position_units(const FRange* __restrict__ fr, long long E2, int npos,
+                                 unsigned long long* __restrict__ diff) {
+  extern __shared__ int pu_smem[];
+  for (int i = threadIdx.x; i <= npos; i += blockDim.x) pu_smem[i] = 0;
+  __syncthreads();
+  for (long long P = blockIdx.x * (long long)blockDim.x + threadIdx.x; P < E2;
+       P += (long long)gridDim.x * blockDim.x) {
+    const int lc = fr[P].lo_cnt;
+    const int cnt = lc >> 16, s0 = lc & 0xffff;
+    if (cnt > 0) {
+      atomicAdd(pu_smem + s0, 1);
+      atomicSub(pu_smem + s0 + cnt, 1);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= npos; i += blockDim.x)
+    if (pu_smem[i]) atomicAdd(diff + i, (unsigned long long)(long long)pu_smem[i]);
+}
+
+int tdb_position_units_impl(TdbSystem* sys, int f, int64_t* out) {
+  AsmWorkspace* ws = sys->ws;
+  if (!ws || !ws->frange) {
+    set_error("position units: no pair plan (system not run)");
+    return TDB_E_INVALID;
+  }
+  const int npos = sys->fam[f].npos;
+  cudaStream_t st = sys->ctx->stream;
+  Dev d;
+  int rc = dalloc_dev<unsigned long long>(d, npos + 1);
+  if (rc) return rc;
+  TDB_CUDA_CHECK(cudaMemsetAsync(d.p, 0, (npos + 1) * sizeof(unsigned long long), st));
+  const int blocks = (int)std::min<long long>((ws->E2 + 255) / 256, 148LL * 8);
+  k_position_units<<<blocks, 256, (npos + 1) * sizeof(int), st>>>(ws->frange + (long long)f * ws->E2, ws->E2,
+                                                                    npos, d.as<unsigned long long>());
+  TDB_CUDA_CHECK(cudaGetLastError());
+  std::vector<unsigned long long> h(npos + 1);
+  TDB_CUDA_CHECK(cudaMemcpyAsync(h.data(), d.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  TDB_CUDA_CHECK(cudaStreamSynchronize(st));
+  long long run = 0;
+  for (int s = 0; s < npos; ++s) {
+    run += (long long)h[s];
+    out[s] = run;
+  }
+  return TDB_OK;
+}
+
 // Device computation of SurfaceMesh.tri_distance_bounds rows (mesh.py:146-153):
 // tmin/tmax (nrows, E) for triangle rows `rows` against every triangle.
 int tdb_tri_bounds_impl(TdbContext* ctx, const TdbMesh* mesh, int64_t nrows, const int64_t* rows,
@@ -2344,25 +2398,57 @@ __global__ void k_dfma_peak(double* out, int iters, double a, double b) {
   const double s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
   if (s == 1234.5678) out[0] = s;  // keep the chains alive
 }
+
+__device__ __forceinline__ void dmma_chain(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+__global__ void k_dmma_peak(double* out, int iters) {
+  double acc[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = threadIdx.x * 1e-3;
+  const double a = 1.0 + threadIdx.x * 1e-6, b = 0.999;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma_chain(acc[i][0], acc[i][1], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += acc[i][0] + acc[i][1];
+  if (s == 1234.5678) out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
 }  // namespace tdb
 
+// FP64 peak of the device as the best of two measured instruction streams
+// (independent 8-deep chains, all SMs): DFMA (2 flops per lane) and the FP64
+// tensor-core DMMA mma.sync.m8n8k4 (512 flops per warp instruction).  The
+// roofline denominator is the higher of the two (they share the FP64 pipe on
+// B200: nominal 148 SM x 64 FMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s).
 int tdb_fp64_peak_impl(TdbContext* ctx, int repeats, double* tflops) {
   cudaStream_t st = ctx->stream;
   Dev d;
   int rc;
-  if ((rc = dalloc_dev<double>(d, 1))) return rc;
+  if ((rc = dalloc_dev<double>(d, (size_t)ctx->num_sms * 2 * 512))) return rc;
   const int threads = 256, blocks = ctx->num_sms * 8, iters = 2048;
+  const int mthreads = 512, mblocks = ctx->num_sms * 2, miters = 4096;
   Timer t;
   double best = 0.0;
   k_dfma_peak<<<blocks, threads, 0, st>>>(d.as<double>(), 64, 0.999999, 1e-7);
+  k_dmma_peak<<<mblocks, mthreads, 0, st>>>(d.as<double>(), 64);
   for (int r = 0; r < std::max(1, repeats); ++r) {
     TDB_CUDA_CHECK(cudaEventRecord(t.a, st));
     k_dfma_peak<<<blocks, threads, 0, st>>>(d.as<double>(), iters, 0.999999, 1e-7);
     TDB_CUDA_CHECK(cudaEventRecord(t.b, st));
     TDB_CUDA_CHECK(cudaEventSynchronize(t.b));
-    const double ms = elapsed(t.a, t.b);
-    const double flops = 2.0 * 64.0 * iters * (double)threads * blocks;
-    best = std::max(best, flops / (ms * 1e-3) / 1e12);
+    double ms = elapsed(t.a, t.b);
+    best = std::max(best, 2.0 * 64.0 * iters * (double)threads * blocks / (ms * 1e-3) / 1e12);
+    TDB_CUDA_CHECK(cudaEventRecord(t.a, st));
+    k_dmma_peak<<<mblocks, mthreads, 0, st>>>(d.as<double>(), miters);
+    TDB_CUDA_CHECK(cudaEventRecord(t.b, st));
+    TDB_CUDA_CHECK(cudaEventSynchronize(t.b));
+    ms = elapsed(t.a, t.b);
+    best = std::max(best, 512.0 * 8.0 * miters * (mthreads / 32.0) * mblocks / (ms * 1e-3) / 1e12);
   }
   TDB_CUDA_CHECK(cudaGetLastError());
   *tflops = best;

@@ -102,6 +102,7 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
                            TdbSystem* sys);
 int tdb_system_run_impl(TdbSystem* sys);
 int tdb_fp64_peak_impl(TdbContext* ctx, int repeats, double* tflops);
+int tdb_position_units_impl(TdbSystem* sys, int f, int64_t* out);
 int tdb_tri_bounds_impl(TdbContext* ctx, const TdbMesh* mesh, int64_t nrows, const int64_t* rows,
                         double* tmin, double* tmax);
 
@@ -184,14 +185,9 @@ int tdb_system_destroy(TdbSystem* sys) {
     dev_free(f.slo);
     dev_free(f.shi);
   }
-  for (auto& b : sys->tbsr) {
+  for (auto& b : sys->band) {
     dev_free(b.col);
-    dev_free(b.pos);
-    dev_free(b.val);
-    dev_free(b.rbptr);
-  }
-  for (auto& b : sys->bsr) {
-    dev_free(b.col);
+    dev_free(b.stile);
     dev_free(b.val);
     dev_free(b.rbptr);
   }
@@ -253,6 +249,22 @@ int tdb_system_family_nnz(const TdbSystem* sys, int32_t f, int64_t* nnz) {
   TDB_REQUIRE(sys && nnz, "NULL argument");
   TDB_REQUIRE(f >= 0 && f < sys->F, "family index out of range");
   *nnz = sys->fam[f].nnz;
+  return TDB_OK;
+}
+
+int tdb_system_position_units(TdbSystem* sys, int32_t f, int64_t* units) {
+  TDB_REQUIRE(sys && units, "NULL argument");
+  TDB_REQUIRE(f >= 0 && f < sys->F, "family index out of range");
+  TDB_CUDA_CHECK(cudaSetDevice(sys->ctx->device));
+  return tdb_position_units_impl(sys, f, units);
+}
+
+int tdb_system_family_split(const TdbSystem* sys, int32_t f, int32_t* R, int32_t* D, int32_t* K) {
+  TDB_REQUIRE(sys && R && D && K, "NULL argument");
+  TDB_REQUIRE(f >= 0 && f < sys->F, "family index out of range");
+  *R = sys->fam[f].split_R;
+  *D = sys->fam[f].split_D;
+  *K = sys->fam[f].split_K;
   return TDB_OK;
 }
 

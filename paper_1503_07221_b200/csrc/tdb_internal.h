@@ -50,30 +50,22 @@ struct FRange {
   int lo_cnt;  // s_lo | (cnt << 16)
 };
 
-// One family's stored blocks as 8 x 4 tiles (p = 0 tensor-core matvec): dofs in
-// Morton order (rows: the system's owned rows; columns: all vertices), tiles of a
-// (position, row block) contiguous and ordered by column block; values in the
-// DMMA m8n8k4 A-fragment order (lane = 4 * row + col).
-struct BsrStore {
-  long long ntiles = 0;
-  int32_t* col = nullptr;     // (ntiles,) column block
+// One family's stored blocks as lag-band tiles (tdb_band.cu): 8 test rows
+// (Morton row block J) x 4 consecutive positions (S-tile) of ONE column vertex l,
+// A-fragment order (lane = 4 * row + position % 4), sorted (J, l, S).
+struct BandStore {
+  bool built = false, failed = false;
+  long long ntiles = 0, nnz = 0;
+  int nS = 0;
+  int32_t* col = nullptr;     // (ntiles,) column vertex
+  int32_t* stile = nullptr;   // (ntiles,) S-tile
   double* val = nullptr;      // (ntiles, 32)
-  int64_t* rbptr = nullptr;   // (npos * nRB + 1,)
-};
-
-// One family's stored blocks as 8 x 4 tiles ordered (row block, column block,
-// position): the lag blocks that reuse one x strip are adjacent (tdb_tbsr.cu).
-struct TbsrStore {
-  bool built = false;
-  long long ntiles = 0;
-  int32_t* col = nullptr;     // (ntiles,) column block
-  int32_t* pos = nullptr;     // (ntiles,) position within the family
-  double* val = nullptr;      // (ntiles, 32) A-fragment order
   int64_t* rbptr = nullptr;   // (nRB + 1,)
 };
 
 struct FamilyStore {
   int npos = 0;
+  int split_R = 1, split_D = kDeg, split_K = kDeg + 1;  // evaluation split chosen at create
   long long nnz = 0;
   int64_t* indptr = nullptr;   // npos * M + 1
   int32_t* indices = nullptr;  // nnz
@@ -130,8 +122,6 @@ struct TdbSystem {
   int* d_rperm = nullptr;
   int* d_rinv = nullptr;
   int nRB = 0, nCB = 0;  // ceil(nrows / 8), ceil(V / 4)
-  std::vector<tdb::BsrStore> bsr;
-  bool bsr_built = false;
-  std::vector<tdb::TbsrStore> tbsr;  // per family, built on first use by a matvec plan
+  std::vector<tdb::BandStore> band;  // per family, built on first use by a matvec plan
   TdbStats stats{};
 };

@@ -21,7 +21,7 @@
 #include <cstdlib>
 #include <vector>
 
-#include "tdb_bsr.h"
+#include "tdb_band.h"
 #include "tdb_common.cuh"
 #include "tdb_internal.h"
 
@@ -410,25 +410,17 @@ struct TdbMatvecPlan {
   double* d_ypart = nullptr;
   unsigned* d_done = nullptr;
   double bytes = 0.0, flops = 0.0;
-  // p = 0 Toeplitz-ordered tensor-core path for the lag terms (tdb_tbsr.cu)
-  bool tbsr = false;
+  // p = 0 lag-band tensor-core path for the inner family's regular lag terms (tdb_band.cu)
+  bool band = false;
   int n_tiled = 0, n_csr = 0, n_csr_all = 0;
-  // the tile kernel runs on its own stream, concurrently with the CSR kernel
+  // the band kernel runs on its own stream, concurrently with the CSR kernel
   cudaStream_t tst = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  TbsrMvArgs targs{};
-  int* d_toff = nullptr;
-  unsigned* d_tact = nullptr;
-  double* d_typart = nullptr;
-  // p = 0 tensor-core path (tdb_bsr.cu)
-  bool bsr = false;
-  BsrMvArgs bargs{};
-  BsrFam* d_bfam = nullptr;
-  int* d_bgroups = nullptr;
-  long long* d_xmap_p = nullptr;  // permuted row l' -> offset of vertex vperm[l'] in x
-  double* d_xp = nullptr;
+  BandMvArgs bargs{};
+  int band_cols = 0, band_c0 = 0, band_padl = 0;  // inner columns of x copied into xt, first one, pad
+  unsigned* d_sact = nullptr;
+  double* d_bxt = nullptr;
   double* d_bypart = nullptr;
-  unsigned* d_bdone = nullptr;
 };
 
 extern "C" int tdb_matvec_plan_destroy(TdbMatvecPlan* p) {
@@ -437,9 +429,9 @@ extern "C" int tdb_matvec_plan_destroy(TdbMatvecPlan* p) {
   if (p->tst) cudaStreamDestroy(p->tst);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
-  dev_free(p->d_toff);
-  dev_free(p->d_tact);
-  dev_free(p->d_typart);
+  dev_free(p->d_sact);
+  dev_free(p->d_bxt);
+  dev_free(p->d_bypart);
   dev_free(p->d_fam);
   dev_free(p->d_tcsr);
   dev_free(p->d_ints);
@@ -448,12 +440,6 @@ extern "C" int tdb_matvec_plan_destroy(TdbMatvecPlan* p) {
   dev_free(p->d_ypart);
   dev_free(p->d_done);
   dev_free(p->d_xmap);
-  dev_free(p->d_bfam);
-  dev_free(p->d_bgroups);
-  dev_free(p->d_xmap_p);
-  dev_free(p->d_xp);
-  dev_free(p->d_bypart);
-  dev_free(p->d_bdone);
   delete p;
   return TDB_OK;
 }
@@ -601,113 +587,23 @@ static int plan_create_impl(TdbSystem* sys, const TdbMatvecDesc* d, TdbMatvecPla
   a.xs = (nc + 1) * NP1;
   a.ypart = p->d_ypart;
   a.row_done = p->d_done;
-  // ---- p = 0: optional tensor-core BSR path (TDB_MV_BSR=1; measured slower than the
-  // CSR lanes-over-time kernel on configs 2 and 4) ----
-  static const bool use_bsr = std::getenv("TDB_MV_BSR") != nullptr && std::atoi(std::getenv("TDB_MV_BSR")) != 0;
-  if (NP1 == 1 && use_bsr) {
-    int rc = bsr_build(sys);
-    if (rc) {
-      tdb_matvec_plan_destroy(p);
-      return rc;
-    }
-    const int nRB = sys->nRB, nCB = sys->nCB;
-    // tiles per term (row blocks of its position)
-    std::vector<double> tcost_b(nt, 0.0);
-    std::vector<std::vector<int64_t>> rbp(sys->F);
-    for (int t = 0; t < nt; ++t) {
-      const int f = d->term_family[t], s_ = d->term_pos[t];
-      if (rbp[f].empty()) {
-        rbp[f].resize((size_t)sys->fam[f].npos * nRB + 1);
-        TDB_CUDA_CHECK(cudaMemcpy(rbp[f].data(), sys->bsr[f].rbptr, rbp[f].size() * sizeof(int64_t),
-                                  cudaMemcpyDeviceToHost));
-      }
-      const double tiles = (double)(rbp[f][(size_t)(s_ + 1) * nRB] - rbp[f][(size_t)s_ * nRB]);
-      tcost_b[t] = tiles * (1.0 + (term_kt[4 * (size_t)t] < 0 ? (nr + 7) / 8 : 1));
-    }
-    // time tiles per CTA: the largest T in {8, 4, 2, 1} that still gives >= 2 CTAs per SM
-    const int ntile = (nr + 7) / 8;
-    int T = 8;
-    while (T > 1 && (long long)nRB * ((ntile + T - 1) / T) < 2LL * sys->ctx->num_sms) T /= 2;
-    const int KG = (ntile + T - 1) / T;
-    const int Gb = kBsrWarps;
-    std::vector<int> gbb(Gb + 1, nt);
-    {
-      double total = 0;
-      for (double v : tcost_b) total += v;
-      double acc_ = 0;
-      int g = 0;
-      gbb[0] = 0;
-      for (int t = 0; t < nt && g < Gb - 1; ++t) {
-        acc_ += tcost_b[t];
-        if (acc_ * Gb >= total * (g + 1)) gbb[++g] = t + 1;
-      }
-      for (int k = g + 1; k <= Gb; ++k) gbb[k] = nt;
-    }
-    std::vector<BsrFam> bf(sys->F);
-    for (int f = 0; f < sys->F; ++f) bf[f] = {sys->bsr[f].col, sys->bsr[f].val, sys->bsr[f].rbptr};
-    std::vector<long long> xmp(M);
-    for (int lp = 0; lp < M; ++lp) {
-      const int l = sys->vperm[lp];
-      xmp[lp] = d->x_map ? (long long)d->x_map[l] : (long long)l;
-    }
-    const int xs_b = nc + 8;
-    const size_t xp_n = (size_t)nCB * 4 * xs_b;
-#define ALLOC_COPY2(dst, src, n, T_)                                                               \
-  do {                                                                                             \
-    size_t nn = std::max<size_t>(1, (size_t)(n));                                                  \
-    if (dev_malloc((void**)&(dst), nn * sizeof(T_)) != cudaSuccess) {                             \
-      tdb_matvec_plan_destroy(p);                                                                  \
-      set_error("matvec plan: cudaMalloc failed");                                                 \
-      return TDB_E_NOMEM;                                                                          \
-    }                                                                                              \
-    if ((n) > 0 && (src) != nullptr)                                                               \
-      cudaMemcpyAsync((dst), (src), (size_t)(n) * sizeof(T_), cudaMemcpyHostToDevice, st);         \
-  } while (0)
-    ALLOC_COPY2(p->d_bfam, bf.data(), sys->F, BsrFam);
-    ALLOC_COPY2(p->d_bgroups, gbb.data(), Gb + 1, int);
-    ALLOC_COPY2(p->d_xmap_p, xmp.data(), M, long long);
-    ALLOC_COPY2(p->d_xp, (const double*)nullptr, xp_n, double);
-    cudaMemsetAsync(p->d_xp, 0, xp_n * sizeof(double), st);
-#undef ALLOC_COPY2
-    TDB_CUDA_CHECK(cudaStreamSynchronize(st));
-    BsrMvArgs& b = p->bargs;
-    b.nrows = NR;
-    b.nRB = nRB;
-    b.KG = KG;
-    b.T = T;
-    b.rlo = d->rlo;
-    b.nr = nr;
-    b.clo = d->clo;
-    b.nc = nc;
-    b.words = d->words;
-    b.fam = p->d_bfam;
-    b.term_f = a.term_f;
-    b.term_s = a.term_s;
-    b.term_d = a.term_d;
-    b.term_mask = a.term_mask;
-    b.group_begin = p->d_bgroups;
-    b.rperm = sys->d_rperm;
-    b.xp = p->d_xp;
-    b.xs = xs_b;
-    p->bsr = true;
-    // stored bytes of the tile format (the canonical CSR figure stays in p->bytes)
-  }
   *out = p;
   return TDB_OK;
 }
 
-// Lag terms of the most reused family -> Toeplitz-ordered DMMA tiles (tdb_tbsr.cu);
-// every other term (boundary blocks used at a few block rows, and all terms when
-// p > 0) -> the CSR kernel above, which writes y first; the tile kernel adds.
+// Regular lag terms of the inner (Toeplitz) family -> lag-band DMMA tiles
+// (tdb_band.cu); every other term (boundary blocks, the light-cone tie lag whose
+// logical mask is not the full band, and all terms when p > 0) -> the CSR kernel
+// above, which writes y first; the band partials are added after it.
 extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, TdbMatvecPlan** out) {
   TDB_REQUIRE(sys && d && out, "NULL argument");
-  static const bool tbsr_on = [] {
-    const char* e = std::getenv("TDB_MV_TBSR");
-    const char* b = std::getenv("TDB_MV_BSR");
-    return !(e && std::atoi(e) == 0) && !(b && std::atoi(b) != 0);
+  static const bool band_on = [] {
+    const char* e = std::getenv("TDB_MV_BAND");
+    return !(e && std::atoi(e) == 0);
   }();
   const int nt = d->nterms;
-  if (!tbsr_on || sys->np1 != 1 || nt <= 0 || d->words != (d->N + 31) / 32) return plan_create_impl(sys, d, out);
+  if (!band_on || sys->np1 != 1 || nt <= 0 || d->words != (d->N + 31) / 32) return plan_create_impl(sys, d, out);
+  const int N = d->N;
   std::vector<int> nlog(nt, 0), cnt(sys->F, 0);
   for (int t = 0; t < nt; ++t) {
     const int f = d->term_family[t];
@@ -718,27 +614,54 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   }
   const int tf = (int)(std::max_element(cnt.begin(), cnt.end()) - cnt.begin());
   if (cnt[tf] < 2) return plan_create_impl(sys, d, out);
+  // band rows / columns: the inner block rows and columns of the plan's ranges
+  const int ktlo = std::max(d->rlo, 2), kthi = std::min(d->rhi, N - 1);
+  const int itlo = std::max(d->clo, 2), ithi = std::min(d->chi, N - 1);
+  if (ktlo > kthi || itlo > ithi) return plan_create_impl(sys, d, out);
   const int npos = sys->fam[tf].npos;
+  // lag of each position: must be d0 + s (the family's positions are consecutive lags)
+  int d0 = 0;
+  bool have_d0 = false, consecutive = true;
+  for (int t = 0; t < nt; ++t)
+    if (d->term_family[t] == tf) {
+      const int dd = d->term_d[t] - d->term_pos[t];
+      if (!have_d0) {
+        d0 = dd;
+        have_d0 = true;
+      } else if (dd != d0) {
+        consecutive = false;
+      }
+    }
+  if (!consecutive) return plan_create_impl(sys, d, out);
   std::vector<int> term_of(npos, -1);
   std::vector<char> to_tile(nt, 0);
-  for (int t = 0; t < nt; ++t)
-    if (d->term_family[t] == tf && nlog[t] > kSpmvMaxKt && term_of[d->term_pos[t]] < 0) {
-      term_of[d->term_pos[t]] = t;
-      to_tile[t] = 1;
+  double useful = 0.0;
+  for (int t = 0; t < nt; ++t) {
+    if (d->term_family[t] != tf || term_of[d->term_pos[t]] >= 0) continue;
+    // regular: the logical mask is exactly {kt in band rows : kt - d in band columns}
+    const unsigned* mk = d->term_mask + (long long)t * d->words;
+    bool regular = true;
+    int n = 0;
+    for (int kt = 1; kt <= N && regular; ++kt) {
+      const bool want = kt >= ktlo && kt <= kthi && kt - d->term_d[t] >= itlo && kt - d->term_d[t] <= ithi;
+      const bool have = (mk[(kt - 1) >> 5] >> ((kt - 1) & 31)) & 1u;
+      regular = want == have;
+      n += have;
     }
-  {  // tile-walk efficiency: useful (block row, time tile) slots over all slots walked
-    const int nr_ = d->rhi - d->rlo + 1, ntt_ = (nr_ + 7) / 8, ntg_ = (ntt_ + 11) / 12;
-    const int TT_ = std::min(12, (((ntt_ + ntg_ - 1) / ntg_) + 1) & ~1);
-    double useful = 0.0;
-    for (int s_ = 0; s_ < npos; ++s_)
-      if (term_of[s_] >= 0) useful += nlog[term_of[s_]];
-    static const double min_eff = [] {
-      const char* e = std::getenv("TDB_TBSR_MIN_EFF");
-      return e ? std::atof(e) : 0.3;
-    }();
-    if (useful < min_eff * (double)npos * ntg_ * TT_ * 8) return plan_create_impl(sys, d, out);
+    if (!regular || n == 0) continue;
+    term_of[d->term_pos[t]] = t;
+    to_tile[t] = 1;
+    useful += n;
   }
-  if (tbsr_build(sys, tf) != TDB_OK) {  // e.g. no room for the tile copy: CSR for every term
+  const int nkt = kthi - ktlo + 1, nT = (nkt + 7) / 8;
+  int ntiled = 0;
+  for (int s_ = 0; s_ < npos; ++s_) ntiled += term_of[s_] >= 0;
+  static const double min_eff = [] {
+    const char* e = std::getenv("TDB_BAND_MIN_EFF");
+    return e ? std::atof(e) : 0.25;
+  }();
+  if (ntiled < 2 || useful < min_eff * (double)ntiled * nT * 8) return plan_create_impl(sys, d, out);
+  if (band_build(sys, tf) != TDB_OK) {  // e.g. no room for the tile copy: CSR for every term
     cudaGetLastError();
     return plan_create_impl(sys, d, out);
   }
@@ -772,52 +695,37 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
         p->flops += 2.0 * nnz * nlog[t];
       }
   }
-  const int M = (int)sys->V, nRB = sys->nRB, nCB = sys->nCB;
-  const int nr = d->rhi - d->rlo + 1, nc = d->chi - d->clo + 1;
-  const int ntt = (nr + 7) / 8;
-  const int ntg = (ntt + 11) / 12;
-  int TT = (ntt + ntg - 1) / ntg;
-  TT = std::min(12, (TT + 1) & ~1);
-  const int xs_b = nc + 8;
-  std::vector<int> off((size_t)ntg * npos * TT * 8, nc);
-  std::vector<unsigned> act((size_t)ntg * npos, 0u);
-  for (int s_ = 0; s_ < npos; ++s_) {
-    const int t = term_of[s_];
-    if (t < 0) continue;
-    const unsigned* mk = d->term_mask + (long long)t * d->words;
-    for (int tg = 0; tg < ntg; ++tg)
-      for (int u = 0; u < TT; ++u)
-        for (int gq = 0; gq < 8; ++gq) {
-          const int r = 8 * (tg * TT + u) + gq, kt = d->rlo + r;
-          if (r >= nr || !((mk[(kt - 1) >> 5] >> ((kt - 1) & 31)) & 1u)) continue;
-          const int c = kt - d->term_d[t] - d->clo;
-          if (c < 0 || c >= nc) {
-            tdb_matvec_plan_destroy(p);
-            set_error("matvec: term mask has a block column outside the plan's column range");
-            return TDB_E_INVALID;
-          }
-          off[(((size_t)tg * npos + s_) * 8 + gq) * TT + u] = c;
-          act[(size_t)tg * npos + s_] |= 1u << u;
-        }
+  const BandStore& bs = sys->band[tf];
+  const int nS = bs.nS, V = (int)sys->V, nRB = sys->nRB;
+  std::vector<unsigned> sact(nS, 0u);
+  for (int s_ = 0; s_ < npos; ++s_)
+    if (term_of[s_] >= 0) sact[s_ >> 2] |= 1u << (s_ & 3);
+  // time tiles per warp (<= 6), warps per CTA
+  const int W = std::min(kBandMaxWarps, (nT + 5) / 6);
+  const int TT = (nT + W - 1) / W;
+  if (TT > 6) {  // more than 384 block rows: not instantiated
+    tdb_matvec_plan_destroy(p);
+    return plan_create_impl(sys, d, out);
   }
-  static const int tb_warps = [] {
-    const char* e = std::getenv("TDB_TBSR_WARPS_PER_SM");
-    return e ? std::max(1, std::atoi(e)) : 48;
+  // xt column of (kt, lag d): PADL + (kt - d - itlo); off0 = column of (ktlo + n, d0 + 4 S + k) + 4 S + k - n
+  const int base = ktlo - itlo - d0;
+  const int padl = std::max(0, 4 * (nS - 1) + 3 - base);
+  const int off0 = padl + base;
+  const int ncols = ithi - itlo + 1;
+  int xs = std::max(padl + ncols, off0 + 8 * W * TT + 8);
+  xs = (xs + 1) & ~1;
+  const long long tiles_per_rb = bs.ntiles / std::max(1, nRB);
+  static const int band_warps = [] {
+    const char* e = std::getenv("TDB_BAND_WARPS_PER_SM");
+    return e ? std::max(1, std::atoi(e)) : 32;
   }();
-  // parts per (row block, time group): enough warps to hide the B-gather latency,
-  // but >= 64 tiles per warp so the ordered partial reduction stays small
-  const long long tiles_per_rb = sys->tbsr[tf].ntiles / std::max(1, nRB);
-  const int G = (int)std::max<long long>(
-      1, std::min<long long>({256LL, (long long)sys->ctx->num_sms * tb_warps / std::max(1, nRB * ntg),
-                              tiles_per_rb / 64}));
-  std::vector<long long> xmp(M);
-  for (int lp = 0; lp < M; ++lp) {
-    const int l = sys->vperm[lp];
-    xmp[lp] = d->x_map ? (long long)d->x_map[l] : (long long)l;
-  }
+  const int P = (int)std::max<long long>(
+      1, std::min<long long>({64LL, (long long)sys->ctx->num_sms * band_warps / std::max(1, nRB * W),
+                              tiles_per_rb / 32}));
+  const int ldy = 8 * W * TT;
   cudaStream_t st = sys->ctx->stream;
-  const size_t xp_n = (size_t)nCB * 4 * xs_b;
-  const size_t yp_n = (size_t)nRB * ntg * G * TT * 64;
+  const size_t xt_n = (size_t)V * xs;
+  const size_t yp_n = (size_t)P * nRB * 8 * ldy;
 #define ALLOC_COPY3(dst, src, n, T_)                                                               \
   do {                                                                                             \
     size_t nn = std::max<size_t>(1, (size_t)(n));                                                  \
@@ -829,33 +737,37 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
     if ((n) > 0 && (src) != nullptr)                                                               \
       cudaMemcpyAsync((dst), (src), (size_t)(n) * sizeof(T_), cudaMemcpyHostToDevice, st);         \
   } while (0)
-  ALLOC_COPY3(p->d_toff, off.data(), off.size(), int);
-  ALLOC_COPY3(p->d_tact, act.data(), act.size(), unsigned);
-  ALLOC_COPY3(p->d_typart, (const double*)nullptr, yp_n, double);
-  ALLOC_COPY3(p->d_xmap_p, xmp.data(), M, long long);
-  ALLOC_COPY3(p->d_xp, (const double*)nullptr, xp_n, double);
-  cudaMemsetAsync(p->d_xp, 0, xp_n * sizeof(double), st);
+  ALLOC_COPY3(p->d_sact, sact.data(), nS, unsigned);
+  ALLOC_COPY3(p->d_bypart, (const double*)nullptr, yp_n, double);
+  ALLOC_COPY3(p->d_bxt, (const double*)nullptr, xt_n, double);
+  cudaMemsetAsync(p->d_bxt, 0, xt_n * sizeof(double), st);  // zero pads (never written again)
 #undef ALLOC_COPY3
   TDB_CUDA_CHECK(cudaStreamSynchronize(st));
-  const TbsrStore& tb = sys->tbsr[tf];
-  TbsrMvArgs& ta = p->targs;
-  ta.nRB = nRB;
-  ta.G = G;
-  ta.ntg = ntg;
-  ta.TT = TT;
-  ta.npos = npos;
-  ta.nrows = sys->nrows;
-  ta.nr = nr;
-  ta.col = tb.col;
-  ta.pos = tb.pos;
-  ta.val = tb.val;
-  ta.rbptr = tb.rbptr;
-  ta.off_tab = p->d_toff;
-  ta.act_tab = p->d_tact;
-  ta.rperm = sys->d_rperm;
-  ta.xp = p->d_xp;
-  ta.xs = xs_b;
-  ta.ypart = p->d_typart;
+  BandMvArgs& ba = p->bargs;
+  ba.nRB = nRB;
+  ba.P = P;
+  ba.nT = nT;
+  ba.TT = TT;
+  ba.W = W;
+  ba.nrows = sys->nrows;
+  ba.nS = nS;
+  ba.ktlo = ktlo;
+  ba.nkt = nkt;
+  ba.rlo = d->rlo;
+  ba.off0 = off0;
+  ba.xs = xs;
+  ba.ldy = ldy;
+  ba.col = bs.col;
+  ba.stile = bs.stile;
+  ba.val = bs.val;
+  ba.rbptr = bs.rbptr;
+  ba.s_act = p->d_sact;
+  ba.rperm = sys->d_rperm;
+  ba.xt = p->d_bxt;
+  ba.ypart = p->d_bypart;
+  p->band_cols = ncols;
+  p->band_c0 = itlo - d->clo;
+  p->band_padl = padl;
   if (cudaStreamCreateWithFlags(&p->tst, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -863,7 +775,7 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
     set_error("matvec plan: stream/event creation failed");
     return TDB_E_CUDA;
   }
-  p->tbsr = true;
+  p->band = true;
   p->n_tiled = nt - (int)cf.size();
   p->n_csr = (int)cf.size();
   *out = p;
@@ -872,8 +784,8 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
 
 extern "C" int tdb_matvec_plan_kind(const TdbMatvecPlan* p, int32_t* tiled_terms, int32_t* csr_terms) {
   TDB_REQUIRE(p != nullptr, "NULL plan");
-  if (tiled_terms) *tiled_terms = p->tbsr ? p->n_tiled : 0;
-  if (csr_terms) *csr_terms = p->tbsr ? p->n_csr : p->n_csr_all;
+  if (tiled_terms) *tiled_terms = p->band ? p->n_tiled : 0;
+  if (csr_terms) *csr_terms = p->band ? p->n_csr : p->n_csr_all;
   return TDB_OK;
 }
 
@@ -889,37 +801,28 @@ extern "C" int tdb_matvec(TdbMatvecPlan* p, const double* x, double* y) {
   const MvArgs& a = p->args;
   cudaStream_t st = p->sys->ctx->stream;
   const int ncols = a.nc * a.NP1;
-  if (p->bsr) {
-    dim3 blk(32, 8), grd((a.M + 31) / 32, (ncols + 31) / 32);
-    k_transpose_in<<<grd, blk, 0, st>>>(x, p->d_xp, a.M, ncols, p->bargs.xs, p->d_xmap_p, p->xstride);
-    TDB_CUDA_CHECK(cudaGetLastError());
-    p->bargs.y = y;
-    return bsr_mv_launch(p->bargs, st);
-  }
-  // Eager calls fork the tile kernel onto the plan's stream (concurrent with the CSR
-  // kernel); inside a CUDA-graph capture (the recursive preconditioner) the two
-  // stay on the capturing stream, which measured faster for the captured solve.
+  // Eager calls fork the band kernel onto the plan's stream (concurrent with the CSR
+  // kernel); inside a CUDA-graph capture (the recursive preconditioner) both stay
+  // on the capturing stream.
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   TDB_CUDA_CHECK(cudaStreamIsCapturing(st, &cap));
-  const bool fork = p->tbsr && cap == cudaStreamCaptureStatusNone;
-  if (p->tbsr && !fork) {
-    dim3 blk(32, 8), grd((a.M + 31) / 32, (ncols + 31) / 32);
-    k_transpose_in<<<grd, blk, 0, st>>>(x, p->d_xp, a.M, ncols, p->targs.xs, p->d_xmap_p, p->xstride);
+  const bool fork = p->band && cap == cudaStreamCaptureStatusNone;
+  if (p->band) {
+    cudaStream_t bst = st;
+    if (fork) {
+      TDB_CUDA_CHECK(cudaEventRecord(p->ev_fork, st));
+      TDB_CUDA_CHECK(cudaStreamWaitEvent(p->tst, p->ev_fork, 0));
+      bst = p->tst;
+    }
+    // inner columns of x -> vertex-major rows of xt at column padl (pads stay zero)
+    dim3 blk(32, 8), grd((a.M + 31) / 32, (p->band_cols + 31) / 32);
+    k_transpose_in<<<grd, blk, 0, bst>>>(x + (long long)p->band_c0 * p->xstride, p->d_bxt + p->band_padl, a.M,
+                                         p->band_cols, p->bargs.xs, p->d_xmap, p->xstride);
     TDB_CUDA_CHECK(cudaGetLastError());
-    p->targs.y = y;
-    int rc = tbsr_mv_tiles(p->targs, st, false);
+    p->bargs.y = y;
+    int rc = band_mv_tiles(p->bargs, bst);
     if (rc) return rc;
-  }
-  if (fork) {  // fork: the lag-term tiles on the plan's stream, concurrent with the CSR kernel
-    TDB_CUDA_CHECK(cudaEventRecord(p->ev_fork, st));
-    TDB_CUDA_CHECK(cudaStreamWaitEvent(p->tst, p->ev_fork, 0));
-    dim3 blk(32, 8), grd((a.M + 31) / 32, (ncols + 31) / 32);
-    k_transpose_in<<<grd, blk, 0, p->tst>>>(x, p->d_xp, a.M, ncols, p->targs.xs, p->d_xmap_p, p->xstride);
-    TDB_CUDA_CHECK(cudaGetLastError());
-    p->targs.y = y;
-    int rc = tbsr_mv_tiles(p->targs, p->tst, false);
-    if (rc) return rc;
-    TDB_CUDA_CHECK(cudaEventRecord(p->ev_join, p->tst));
+    if (fork) TDB_CUDA_CHECK(cudaEventRecord(p->ev_join, p->tst));
   }
   {
     dim3 blk(32, 8), grd((a.M + 31) / 32, (ncols + 31) / 32);
@@ -938,9 +841,9 @@ extern "C" int tdb_matvec(TdbMatvecPlan* p, const double* x, double* y) {
     }
   }
   TDB_CUDA_CHECK(cudaGetLastError());
-  if (p->tbsr) {  // (join,) then the tiles' partials are added to the CSR kernel's y in part order
+  if (p->band) {  // (join,) then the band partials are added to the CSR kernel's y in part order
     if (fork) TDB_CUDA_CHECK(cudaStreamWaitEvent(st, p->ev_join, 0));
-    return tbsr_mv_reduce(p->targs, st);
+    return band_mv_reduce(p->bargs, st);
   }
   return TDB_OK;
 }

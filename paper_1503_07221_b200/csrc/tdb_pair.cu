@@ -1,7 +1,7 @@
 // Drop-in pair_block_contributions on the GPU (one block position, host buffers).
 //
 // Contract of tdbem._kernels.pair_block_contributions
-// (/root/reference/pkg/src/tdbem/_kernels/__init__.py:7-13, _core.pyx:81-193):
+// (/root/reference/pkg/src/tdbem/_kernels/__init__.py:1-34, _core.pyx:47-159):
 // per pair P and rule point q, X = cx0 + x1 (cx1-cx0) + x2 (cx2-cx1), same for Y,
 // r = |X - Y|, a = r + delta; points with a outside the union of the active
 // table supports are skipped; common = a2x a2y w / (4 pi r);

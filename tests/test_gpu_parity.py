@@ -319,8 +319,8 @@ def test_row_partition_bitwise_and_emulated_allgather(G, cfg1_mesh):
 
 
 def test_tiled_matvec_ranges_vs_dense(G, cfg1_mesh):
-    # the tensor-core tile path (lag terms, tdb_tbsr.cu) and the CSR path on the
-    # config-1 system, full / half / off-diagonal / quarter ranges vs the dense matrix
+    # the lag-band tensor-core path (regular lag terms, tdb_band.cu) and the CSR path on
+    # the config-1 system, full / half / off-diagonal / quarter / ragged ranges vs dense
     from paper_1503_07221_b200.temporal_basis import TimeGrid
 
     grid = TimeGrid(T=3.9, N=40, p=0)
@@ -330,7 +330,8 @@ def test_tiled_matvec_ranges_vs_dense(G, cfg1_mesh):
     rng = np.random.default_rng(11)
     kinds = {}
     for rows, cols in [((1, 40), (1, 40)), ((21, 40), (21, 40)), ((21, 40), (1, 20)), ((1, 10), (1, 10)),
-                       ((3, 37), (2, 29))]:
+                       ((3, 37), (2, 29)), ((11, 20), (1, 10)), ((2, 39), (2, 39)), ((40, 40), (1, 40)),
+                       ((1, 40), (5, 5))]:
         x = rng.standard_normal((cols[1] - cols[0] + 1) * M)
         y = A.matvec(x, rows=rows, cols=cols)
         ref = dense[(rows[0] - 1) * M:rows[1] * M, (cols[0] - 1) * M:cols[1] * M] @ x
@@ -338,11 +339,11 @@ def test_tiled_matvec_ranges_vs_dense(G, cfg1_mesh):
         pl = A.matvec_plan(rows, cols)
         kinds[(rows, cols)] = (pl.tiled_terms, pl.csr_terms)
     assert kinds[((1, 40), (1, 40))][0] > 0, kinds       # lag terms on the tensor cores
-    assert kinds[((1, 10), (1, 10))][0] == 0, kinds      # short diagonal range: CSR only
+    assert kinds[((1, 40), (1, 40))][1] > 0, kinds       # boundary terms + the tie lag on CSR
 
 
 def test_tiled_vs_csr_only_plan_agree(G, cfg1_mesh, tmp_path):
-    # the same matvecs with every term on the CSR kernel (TDB_MV_TBSR=0, separate
+    # the same matvecs with every term on the CSR kernel (TDB_MV_BAND=0, separate
     # process: the switch is read once per process) agree with the default plans
     import os
     import subprocess
@@ -368,7 +369,7 @@ def test_tiled_vs_csr_only_plan_agree(G, cfg1_mesh, tmp_path):
         "assert A.matvec_plan((1, 40), (1, 40)).tiled_terms == 0\n"
         "np.save(%r, np.stack([A.matvec(x), np.pad(A.matvec(x[:20 * M], rows=(21, 40), cols=(1, 20)), (0, 20 * M))]))\n"
     ) % (root, os.path.join(root, "tests"), str(tmp_path / "x.npy"), str(tmp_path / "y.npy"))
-    env = dict(os.environ, TDB_MV_TBSR="0")
+    env = dict(os.environ, TDB_MV_BAND="0")
     subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=root)
     yc = np.load(tmp_path / "y.npy")
     assert np.linalg.norm(ys[0] - yc[0]) <= 1e-13 * np.linalg.norm(yc[0])
