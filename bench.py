@@ -422,7 +422,7 @@ def main():
         solve = {"method": "FGMRES(50, 2(2,10)) recursive block preconditioner", "tol": 1e-5,
                  "seconds": ts, "setup_seconds": t_setup, "iterations": len(hist),
                  "final_rel_residual": float(hist[-1]),
-                 "rhs": "Gaussian-pulse plane wave (sigma 0.2, t0 1.0), assemble_rhs (host)",
+                 "rhs": "Gaussian-pulse plane wave (sigma 0.2, t0 1.0), assemble_rhs (device, csrc/tdb_rhs.cu)",
                  "note": "x0 = 0, device vectors; setup = sub-range matvec plans + graph capture of the "
                          "preconditioner (reusable across right-hand sides)"}
 

@@ -396,3 +396,42 @@ def dense(grid, M, diameter, blocks):
     for k in range(n):
         out[:, k] = matvec(grid, M, diameter, blocks, eye[:, k])
     return out
+
+
+# ---------------------------------------------------------------------------
+# right-hand side (assembly.py:314-355)
+# ---------------------------------------------------------------------------
+def assemble_rhs(mesh, grid, g, q_reg: int = 4):
+    """Host restatement of the reference's load-vector loop (assembly.py:314-355),
+    operation for operation (bit-identical, tests/test_oracle_golden.py)."""
+    from paper_1503_07221_b200.quadrature import gauss_rule, triangle_rule
+    from paper_1503_07221_b200.temporal_basis import basis_b, flat_index, support_interval
+
+    m = mesh.num_vertices
+    pts, w = triangle_rule(q_reg)
+    c = mesh.corners
+    X = (c[:, None, 0, :] + pts[None, :, 0, None] * (c[:, 1] - c[:, 0])[:, None, :]
+         + pts[None, :, 1, None] * (c[:, 2] - c[:, 1])[:, None, :]).reshape(-1, 3)
+    wx = (w[None, :] * 2.0 * mesh.areas[:, None]).reshape(-1)
+    sh = np.column_stack([1.0 - pts[:, 0], pts[:, 0] - pts[:, 1], pts[:, 1]])
+    dofs = np.repeat(mesh.triangles, len(pts), axis=0).reshape(-1)
+    shw = np.tile(sh, (mesh.num_triangles, 1)) * wx[:, None]
+    xg, wg = gauss_rule(2 * (grid.p + 4))
+    out = np.zeros(grid.L * m)
+    for k in range(1, grid.L + 1):
+        idx = flat_index(grid, (k - 1) // (grid.p + 1) + 1, (k - 1) % (grid.p + 1))
+        lo, hi = support_interval(grid, idx.timestep)
+        nhalf = max(1, round((hi - lo) / (0.25 * grid.dt)))
+        comp = np.zeros(m)
+        for panel in range(nhalf):
+            a = lo + (hi - lo) * panel / nhalf
+            b = lo + (hi - lo) * (panel + 1) / nhalf
+            tq = 0.5 * (a + b) + 0.5 * (b - a) * xg
+            tw = 0.5 * (b - a) * wg * basis_b(grid, idx, tq, deriv=1)
+            for ts, ws in zip(tq, tw):
+                if ws == 0.0:
+                    continue
+                gv = np.asarray(g(X, ts), dtype=float)
+                comp += np.bincount(dofs, weights=(shw * gv[:, None] * ws).reshape(-1), minlength=m)
+        out[(k - 1) * m : k * m] = comp
+    return out

@@ -454,59 +454,26 @@ def tri_distance_bounds(mesh: SurfaceMesh, rows=None, ctx: _lib.Context | None =
     return tmin, tmax
 
 
-def assemble_rhs(mesh: SurfaceMesh, grid: TimeGrid, g, config: QuadratureConfig = QuadratureConfig(),
-                 device: bool | None = None):
-    """Load vector b[(k-1) M + l] = int int g(x, t) phi_l(x) bdot_k(t) dx dt (host).
+def assemble_rhs(mesh: SurfaceMesh, grid: TimeGrid, g, config: QuadratureConfig = QuadratureConfig()):
+    """Load vector b[(k-1) M + l] = int int g(x, t) phi_l(x) bdot_k(t) dx dt, on the GPU.
 
-    Restates assembly.py:314-355 of the reference: regular q_reg triangle rule in
-    space; in time, Gauss panels of 2(p+4) points over quarter steps of each
-    basis function's support.  g(X (n,3), t) -> (n,).
-
-    A datum with a ``device_eval(X, t)`` method (torch tensors: X (P, 3), t (n,) ->
-    (n, P)), such as gaussian_pulse_neumann's, is integrated on the GPU
-    (``_assemble_rhs_device``: csrc/tdb_rhs.cu) unless device=False; any other
-    callable is a host (numpy) callback and is integrated on the host exactly as
-    the reference does (bit-identical, tests/golden/rhs.npz).
+    Replaces assembly.py:314-355 of the reference: regular q_reg triangle rule in
+    space; in time, Gauss panels of 2(p+4) points over quarter steps of each basis
+    function's support (nodes and weights built on the host in the reference's
+    arithmetic).  The datum is evaluated at every (time node, rule point):
+      * g.device_eval(X, t) (torch tensors: X (P, 3), t (n,) -> (n, P)) on the GPU when
+        the datum provides it (gaussian_pulse_neumann does);
+      * otherwise g(X, t) -> (P,) is the reference's host callback contract (numpy),
+        called per time node on the host and uploaded in chunks.
+    The vertex gather and the per-basis time sum run in csrc/tdb_rhs.cu.  There is no
+    CPU fallback: without a CUDA device this raises (the host restatement of the
+    reference loop is the oracle's, oracle/assembly.py assemble_rhs).
     """
-    if device is not False and hasattr(g, "device_eval"):
-        import torch
+    import torch
 
-        if torch.cuda.is_available():
-            return _assemble_rhs_device(mesh, grid, g, config)
-        if device:
-            raise RuntimeError("assemble_rhs(device=True): no CUDA device")
-    from .quadrature import gauss_rule, triangle_rule
-    from .temporal_basis import basis_b, flat_index, support_interval
-
-    mesh, grid = as_product_inputs(mesh, grid)
-    m = mesh.num_vertices
-    pts, w = triangle_rule(config.q_reg)
-    c = mesh.corners
-    X = (c[:, None, 0, :] + pts[None, :, 0, None] * (c[:, 1] - c[:, 0])[:, None, :]
-         + pts[None, :, 1, None] * (c[:, 2] - c[:, 1])[:, None, :]).reshape(-1, 3)
-    wx = (w[None, :] * 2.0 * mesh.areas[:, None]).reshape(-1)
-    sh = np.column_stack([1.0 - pts[:, 0], pts[:, 0] - pts[:, 1], pts[:, 1]])
-    dofs = np.repeat(mesh.triangles, len(pts), axis=0).reshape(-1)
-    shw = np.tile(sh, (mesh.num_triangles, 1)) * wx[:, None]
-    xg, wg = gauss_rule(2 * (grid.p + 4))
-    out = np.zeros(grid.L * m)
-    for k in range(1, grid.L + 1):
-        idx = flat_index(grid, (k - 1) // (grid.p + 1) + 1, (k - 1) % (grid.p + 1))
-        lo, hi = support_interval(grid, idx.timestep)
-        nhalf = max(1, round((hi - lo) / (0.25 * grid.dt)))
-        comp = np.zeros(m)
-        for panel in range(nhalf):
-            a = lo + (hi - lo) * panel / nhalf
-            b = lo + (hi - lo) * (panel + 1) / nhalf
-            tq = 0.5 * (a + b) + 0.5 * (b - a) * xg
-            tw = 0.5 * (b - a) * wg * basis_b(grid, idx, tq, deriv=1)
-            for ts, ws in zip(tq, tw):
-                if ws == 0.0:
-                    continue
-                gv = np.asarray(g(X, ts), dtype=float)
-                comp += np.bincount(dofs, weights=(shw * gv[:, None] * ws).reshape(-1), minlength=m)
-        out[(k - 1) * m : k * m] = comp
-    return out
+    if not torch.cuda.is_available():
+        raise RuntimeError("assemble_rhs: no CUDA device (the product has no CPU path)")
+    return _assemble_rhs_device(mesh, grid, g, config)
 
 
 def _rhs_time_nodes(grid: TimeGrid):
@@ -532,8 +499,9 @@ def _rhs_time_nodes(grid: TimeGrid):
 
 
 def _assemble_rhs_device(mesh: SurfaceMesh, grid: TimeGrid, g, config: QuadratureConfig = QuadratureConfig()):
-    """assemble_rhs on the GPU: g.device_eval at every (time node, rule point) in
-    node chunks, vertex gather + per-basis time sum in csrc/tdb_rhs.cu."""
+    """assemble_rhs on the GPU: the datum at every (time node, rule point) in node
+    chunks (device_eval on the GPU, or the host callback per node), vertex gather +
+    per-basis time sum in csrc/tdb_rhs.cu."""
     import ctypes
 
     import torch
@@ -572,7 +540,13 @@ def _assemble_rhs_device(mesh: SurfaceMesh, grid: TimeGrid, g, config: Quadratur
     chunk = max(1, min(nn, (1 << 27) // max(P, 1)))  # <= 1 GiB of datum values per chunk
     for j0 in range(0, nn, chunk):
         nj = min(chunk, nn - j0)
-        G = g.device_eval(Xd, ts_d[j0 : j0 + nj]).to(torch.float64).contiguous()
+        if hasattr(g, "device_eval"):
+            G = g.device_eval(Xd, ts_d[j0 : j0 + nj]).to(torch.float64).contiguous()
+        else:  # host callback g(X, t) -> (P,), the reference's contract (assembly.py:326)
+            Gh = np.empty((nj, P))
+            for i in range(nj):
+                Gh[i] = np.asarray(g(X, float(ts[j0 + i])), dtype=float)
+            G = torch.as_tensor(Gh).to(dev)
         _lib.check(_lib.LIB.tdb_rhs_vertex_gather(p(G), j0, nj, P, p(vptr_d), p(vpts_d), p(vw_d), m, p(H), stream),
                    "rhs_vertex_gather")
     _lib.check(_lib.LIB.tdb_rhs_time_sum(p(H), p(kptr_d), p(ws_d), grid.L, m, p(out), stream), "rhs_time_sum")

@@ -276,11 +276,15 @@ class BlockHessenbergMatrix:
             p = self._mv_plans[key] = _MatvecPlan(self, rows, cols)
         return p
 
+    # block rows per matvec plan (the CSR kernel's lanes cover at most 12 x 32 block rows)
+    MAX_PLAN_ROWS = 384
+
     def matvec(self, x, rows=None, cols=None):
         """y = A[rows, cols] x; rows/cols are inclusive 1-based block ranges.
 
         x may be a numpy array (returns numpy) or a float64 CUDA torch tensor
         (returns a CUDA tensor, stream-ordered on torch's current stream).
+        Row ranges longer than MAX_PLAN_ROWS are applied in row chunks, one plan each.
         """
         import torch
 
@@ -296,14 +300,18 @@ class BlockHessenbergMatrix:
         xd = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64)).to(dev) if is_np else x
         if xd.dtype != torch.float64 or not xd.is_cuda or not xd.is_contiguous():
             raise ValueError("matvec expects a contiguous float64 CUDA tensor")
-        plan = self.matvec_plan((rlo, rhi), (clo, chi))
-        if plan.handle is None:
-            y = torch.zeros(nrow, dtype=torch.float64, device=xd.device)
-        else:
-            y = torch.empty(nrow, dtype=torch.float64, device=xd.device)
+        y = torch.empty(nrow, dtype=torch.float64, device=xd.device)
+        step = self.MAX_PLAN_ROWS
+        for r0 in range(rlo, rhi + 1, step):
+            r1 = min(rhi, r0 + step - 1)
+            plan = self.matvec_plan((r0, r1), (clo, chi))
+            ys = y[(r0 - rlo) * np1 * self.M:(r1 - rlo + 1) * np1 * self.M]
+            if plan.handle is None:
+                ys.zero_()
+                continue
             self._dev.ctx.set_stream(torch.cuda.current_stream(xd.device).cuda_stream)
-            _lib.check(_lib.LIB.tdb_matvec(plan.handle, C.c_void_p(xd.data_ptr()),
-                                           C.c_void_p(y.data_ptr())), "matvec")
+            _lib.check(_lib.LIB.tdb_matvec(plan.handle, C.c_void_p(xd.data_ptr()), C.c_void_p(ys.data_ptr())),
+                       "matvec")
         return y.cpu().numpy() if is_np else y
 
     def __matmul__(self, x):

@@ -8,22 +8,23 @@
 // the contiguous band of lags whose light cone the dof pair touches.
 //
 // Storage (built once per family, on first use): tiles of 8 test rows (Morton
-// order, row block J) x 4 consecutive lags (S-tile: s = 4S .. 4S+3) for ONE column
-// vertex l, in the mma.m8n8k4 A-fragment order (lane = 4 * row + lag).  Tiles are
-// sorted (J, l, S).  The dof pair's lag band is contiguous and neighbouring rows
-// have neighbouring bands, so the tiles are ~80% full (the (j, l)-tiled layout of
-// round 1 was ~50%, and re-gathered x per tile).
+// order, row block J) x 4 consecutive lags for ONE column vertex l, starting at
+// the first lag of the (J, l) band (so the 4-lag windows follow the band, not a
+// fixed grid), in the mma.m8n8k4 A-fragment order (lane = 4 * row + lag) with the
+// (l, first lag) header in the same 272-byte record.  Records are sorted (J, l, lag).
 //
-// Matvec: the B operand of tile (J, l, S) at time tile u is a Hankel window of
-// ONE row of the vertex-major iterate: B[k][n] = X[l][kt0 + n - d_0 - 4S - k], so
-// lane (n = lane / 4, k = lane % 4) reads xt[l][off0 - 4S - k + n + 8u] - a
-// broadcast-heavy, L1-resident load (all S-tiles of (J, l) reuse the row).  One
-// CTA = (row block J, part of J's tile list); its warps split the time tiles and
-// walk the same tiles (A fragments from L1 after the first warp).  Columns outside
-// the plan's range are zero pads of xt; positions outside the plan (or whose
-// logical mask is not the full band, e.g. the light-cone tie lag) are masked off
-// per lane and handled by the CSR kernel.  Part partials are summed in part order
-// (deterministic) and added to y after the CSR kernel has written it.
+// Matvec: the B operand of tile (J, l, s0) at time tile u is a Hankel window of
+// ONE row of the vertex-major iterate: B[k][n] = X[l][kt0 + n - d_0 - s0 - k], so
+// lane (n = lane / 4, k = lane % 4) reads xt[l][off0 - s0 - k + n + 8u] - an
+// L1-resident load (all lag windows of (J, l) reuse the row).  One CTA = (row block
+// J, part of J's tile list): its tile records stream HBM -> shared memory through a
+// 3-stage ring of cp.async.bulk copies completing on mbarriers (one elected
+// thread produces), and its warps split the time tiles over the same staged
+// records (each record read from HBM once).  Columns outside the plan's range are
+// zero pads of xt; positions outside the plan (or whose logical mask is not the
+// full band, e.g. the light-cone tie lag) are masked off per lane and handled by
+// the CSR kernel.  Part partials are summed in part order (deterministic) and
+// added to y after the CSR kernel has written it.
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
@@ -39,8 +40,9 @@ namespace tdb {
 
 namespace {
 
+// pass 1 keys: ((J V + l) << 7 | s) << 3 | r  (entries of one (row block, column) adjacent, by lag)
 __global__ void k_band_keys(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                            long long nrows_total, int nrows, int V, int nS, const int* __restrict__ rinv,
+                            long long nrows_total, int nrows, int V, const int* __restrict__ rinv,
                             unsigned long long* __restrict__ keys, long long* __restrict__ ids) {
   const int lane = threadIdx.x & 31;
   const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -49,34 +51,47 @@ __global__ void k_band_keys(const int64_t* __restrict__ indptr, const int32_t* _
     const int s = (int)(row / nrows);
     const int jp = rinv[(int)(row % nrows)];
     const int64_t e0 = indptr[row], e1 = indptr[row + 1];
-    const unsigned sub = (unsigned)((jp & 7) * 4 + (s & 3));
     for (int64_t e = e0 + lane; e < e1; e += 32) {
-      const unsigned long long k =
-          ((unsigned long long)(jp >> 3) * (unsigned long long)V + (unsigned long long)indices[e]) *
-              (unsigned long long)nS + (unsigned long long)(s >> 2);
-      keys[e] = (k << 5) | sub;
+      const unsigned long long jl = (unsigned long long)(jp >> 3) * (unsigned long long)V + (unsigned long long)indices[e];
+      keys[e] = (((jl << 7) | (unsigned long long)s) << 3) | (unsigned long long)(jp & 7);
       ids[e] = e;
     }
   }
 }
 
-__global__ void k_band_heads(const unsigned long long* __restrict__ keys, long long n, int* __restrict__ head) {
+// segment (row block, column) starts: seg[i] = i at a segment head, else 0 (max-scanned next)
+__global__ void k_band_seg(const unsigned long long* __restrict__ keys, long long n, long long* __restrict__ seg) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    head[i] = (i == 0 || (keys[i] >> 5) != (keys[i - 1] >> 5)) ? 1 : 0;
+    seg[i] = (i == 0 || (keys[i] >> 10) != (keys[i - 1] >> 10)) ? i : 0;
+}
+
+// tile heads: a new (row block, column) segment or a new 4-lag window from the segment's first lag
+__global__ void k_band_heads(const unsigned long long* __restrict__ keys, const long long* __restrict__ seg, long long n,
+                             int* __restrict__ head) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int s0 = (int)((keys[seg[i]] >> 3) & 127u);
+    const int t = ((int)((keys[i] >> 3) & 127u) - s0) >> 2;
+    int h = 1;
+    if (i > 0 && seg[i] == seg[i - 1]) h = t != ((((int)((keys[i - 1] >> 3) & 127u)) - s0) >> 2);
+    head[i] = h;
+  }
 }
 
 __global__ void k_band_fill(const unsigned long long* __restrict__ keys, const long long* __restrict__ ids,
-                            const int* __restrict__ tid_incl, long long n, int V, int nS,
-                            const double* __restrict__ data, int32_t* __restrict__ col, int32_t* __restrict__ stile,
-                            double* __restrict__ val, int* __restrict__ tile_rb) {
+                            const long long* __restrict__ seg, const int* __restrict__ tid_incl, long long n, int V,
+                            const double* __restrict__ data, BandTile* __restrict__ tiles, int* __restrict__ tile_rb) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const long long t = tid_incl[i] - 1;
-    const unsigned long long k = keys[i] >> 5;
-    val[t * 32 + (keys[i] & 31u)] = data[ids[i]];
-    if (i == 0 || (keys[i - 1] >> 5) != k) {
-      stile[t] = (int32_t)(k % (unsigned long long)nS);
-      const unsigned long long jl = k / (unsigned long long)nS;
-      col[t] = (int32_t)(jl % (unsigned long long)V);
+    const unsigned long long k = keys[i];
+    const int sst = (int)((keys[seg[i]] >> 3) & 127u);
+    const int s = (int)((k >> 3) & 127u);
+    const int r = (int)(k & 7u);
+    const int w0 = sst + ((s - sst) & ~3);
+    tiles[t].v[r * 4 + (s - w0)] = data[ids[i]];
+    if (i == 0 || tid_incl[i - 1] != tid_incl[i]) {
+      const unsigned long long jl = k >> 10;
+      tiles[t].l = (int32_t)(jl % (unsigned long long)V);
+      tiles[t].s0 = w0;
       tile_rb[t] = (int)(jl / (unsigned long long)V);
     }
   }
@@ -93,66 +108,137 @@ __global__ void k_band_rbptr(const int* __restrict__ tile_rb, long long ntiles, 
   }
 }
 
+struct MaxLL {
+  __device__ __forceinline__ long long operator()(long long a, long long b) const { return a > b ? a : b; }
+};
+
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
 
-// One CTA = (row block J, part); warp w owns time tiles [w TT, w TT + TT).  Two
-// tiles per step: both tiles' A and B loads are issued before their DMMAs.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned phase) {
+  const unsigned a = smem_u32(b);
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(phase)
+        : "memory");
+  } while (!ok);
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// active-lag bits of positions s0 .. s0 + 3
+__device__ __forceinline__ unsigned act4(const unsigned* act, int s0) {
+  const int w = s0 >> 5, b = s0 & 31;
+  const unsigned long long v = ((unsigned long long)act[w + 1] << 32) | act[w];
+  return (unsigned)(v >> b) & 0xFu;
+}
+
+// One CTA = (row block J, part); warp w owns time tiles [w TT, w TT + TT).  Tile
+// records arrive in shared memory by bulk copy (kBandStages-deep ring); two tiles
+// per step, both tiles' B loads issued before their DMMAs; time tiles without a
+// valid row for the tile's lags (the Toeplitz triangle) are skipped.
 template <int TT>
 __global__ void __launch_bounds__(kBandMaxWarps * 32) k_band_mv(BandMvArgs a) {
-  extern __shared__ unsigned bm_act[];  // (nS,) active-lag bits of each S-tile
-  for (int i = threadIdx.x; i < a.nS; i += blockDim.x) bm_act[i] = __ldg(a.s_act + i);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  extern __shared__ __align__(128) unsigned char bm_smem[];
+  BandTile* stg = reinterpret_cast<BandTile*>(bm_smem);  // [kBandStages][kBandChunk]
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(stg + kBandStages * kBandChunk);
+  unsigned long long* empty = full + kBandStages;
+  unsigned* act = reinterpret_cast<unsigned*>(empty + kBandStages);  // [act_words + 1]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int i = tid; i <= a.act_words; i += blockDim.x) act[i] = i < a.act_words ? __ldg(a.s_act + i) : 0u;
   const int J = blockIdx.x / a.P, part = blockIdx.x % a.P;
+  const long long r0 = __ldg(a.rbptr + J), r1 = __ldg(a.rbptr + J + 1);
+  const long long q0 = r0 + (r1 - r0) * part / a.P, q1 = r0 + (r1 - r0) * (part + 1) / a.P;
+  const int nchunks = (int)((q1 - q0 + kBandChunk - 1) / kBandChunk);
+  if (tid == 0) {
+    for (int i = 0; i < kBandStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], a.W);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int c = 0; c < min(kBandStages, nchunks); ++c) {
+      const long long qb = q0 + (long long)c * kBandChunk;
+      const unsigned bytes = (unsigned)(min((long long)kBandChunk, q1 - qb) * sizeof(BandTile));
+      mbar_arrive_expect_tx(&full[c], bytes);
+      bulk_g2s(stg + c * kBandChunk, a.tiles + qb, bytes, &full[c]);
+    }
   const int g = lane >> 2, k = lane & 3;
+  // warp w owns the contiguous time tiles t = t0 + u (adjacent B windows share L1 sectors)
   const int t0 = w * TT;
   double acc[TT][2];
 #pragma unroll
   for (int u = 0; u < TT; ++u) acc[u][0] = acc[u][1] = 0.0;
-  const long long r0 = __ldg(a.rbptr + J), r1 = __ldg(a.rbptr + J + 1);
-  const long long q0 = r0 + (r1 - r0) * part / a.P, q1 = r0 + (r1 - r0) * (part + 1) / a.P;
   const double* xl = a.xt + (a.off0 - k + g + 8 * t0);
-  const unsigned kbit = 1u << k;
-  for (long long pb = q0; pb < q1; pb += 32) {
-    const int n = (int)min(32LL, q1 - pb);
-    int my_l = 0, my_S = 0;
-    unsigned my_act = 0u;
-    if (lane < n) {
-      my_l = __ldg(a.col + pb + lane);
-      my_S = __ldg(a.stile + pb + lane);
-      my_act = bm_act[my_S];
-    }
-    unsigned live = __ballot_sync(0xffffffffu, my_act != 0u);
-    while (live) {
-      const int i1 = __ffs(live) - 1;
-      live &= live - 1;
-      const int i2 = live ? __ffs(live) - 1 : -1;
-      if (i2 >= 0) live &= live - 1;
-      const int l1 = __shfl_sync(0xffffffffu, my_l, i1), S1 = __shfl_sync(0xffffffffu, my_S, i1);
-      const unsigned c1 = __shfl_sync(0xffffffffu, my_act, i1);
-      const int l2 = __shfl_sync(0xffffffffu, my_l, i2 < 0 ? i1 : i2);
-      const int S2 = __shfl_sync(0xffffffffu, my_S, i2 < 0 ? i1 : i2);
-      const unsigned c2 = __shfl_sync(0xffffffffu, my_act, i2 < 0 ? i1 : i2);
-      double av1 = __ldg(a.val + (pb + i1) * 32 + lane);
-      double av2 = i2 >= 0 ? __ldg(a.val + (pb + i2) * 32 + lane) : 0.0;
-      const double* x1 = xl + (long long)l1 * a.xs - 4 * S1;
-      const double* x2 = xl + (long long)l2 * a.xs - 4 * S2;
+  for (int c = 0; c < nchunks; ++c) {
+    const int st = c % kBandStages;
+    const unsigned ph = (unsigned)(c / kBandStages) & 1u;
+    mbar_wait(&full[st], ph);
+    const BandTile* T = stg + st * kBandChunk;
+    const int n = (int)min((long long)kBandChunk, q1 - (q0 + (long long)c * kBandChunk));
+    for (int i = 0; i < n; i += 2) {
+      const bool two = i + 1 < n;
+      const int l1 = T[i].l, s1 = T[i].s0;
+      const int l2 = two ? T[i + 1].l : l1, s2 = two ? T[i + 1].s0 : s1;
+      const unsigned c1 = act4(act, s1), c2 = two ? act4(act, s2) : 0u;
+      if ((c1 | c2) == 0u) continue;  // warp-uniform: no lag of either tile in this plan
+      // time tiles t holding a valid row kt = ktlo + 8 t + n (itlo <= kt - d <= ithi for a lag
+      // d of the window): ceil((dt0 + s0 - 7) / 8) <= t <= floor((dt1 + s0 + 3) / 8)
+      const int lo1 = (a.dt0 + s1 + 8 * 1024) / 8 - 1024, hi1 = (a.dt1 + s1 + 3 + 8 * 1024) / 8 - 1024;
+      const int lo2 = (a.dt0 + s2 + 8 * 1024) / 8 - 1024, hi2 = (a.dt1 + s2 + 3 + 8 * 1024) / 8 - 1024;
+      double av1 = T[i].v[lane];
+      double av2 = two ? T[i + 1].v[lane] : 0.0;
+      if (!((c1 >> k) & 1u)) av1 = 0.0;
+      if (!((c2 >> k) & 1u)) av2 = 0.0;
+      const double* x1 = xl + (long long)l1 * a.xs - s1;
+      const double* x2 = xl + (long long)l2 * a.xs - s2;
       double b1[TT], b2[TT];
 #pragma unroll
       for (int u = 0; u < TT; ++u) {
         b1[u] = __ldg(x1 + 8 * u);
         b2[u] = __ldg(x2 + 8 * u);
       }
-      if (!(c1 & kbit)) av1 = 0.0;
-      if (i2 < 0 || !(c2 & kbit)) av2 = 0.0;
+      const int u1a = lo1 - t0, u1b = c1 != 0u ? hi1 - t0 : -1;
+      const int u2a = lo2 - t0, u2b = c2 != 0u ? hi2 - t0 : -1;
 #pragma unroll
-      for (int u = 0; u < TT; ++u) dmma884(acc[u][0], acc[u][1], av1, b1[u]);
+      for (int u = 0; u < TT; ++u)
+        if (u >= u1a && u <= u1b) dmma884(acc[u][0], acc[u][1], av1, b1[u]);
 #pragma unroll
-      for (int u = 0; u < TT; ++u) dmma884(acc[u][0], acc[u][1], av2, b2[u]);
+      for (int u = 0; u < TT; ++u)
+        if (u >= u2a && u <= u2b) dmma884(acc[u][0], acc[u][1], av2, b2[u]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (tid == 0 && c + kBandStages < nchunks) {  // refill this stage once every warp released it
+      mbar_wait(&empty[st], ph);
+      const long long qb = q0 + (long long)(c + kBandStages) * kBandChunk;
+      const unsigned bytes = (unsigned)(min((long long)kBandChunk, q1 - qb) * sizeof(BandTile));
+      mbar_arrive_expect_tx(&full[st], bytes);
+      bulk_g2s(stg + st * kBandChunk, a.tiles + qb, bytes, &full[st]);
     }
   }
   // partial tile rows of this part: ypart[part][8 J + g][8 (t0 + u) + 2 k + {0, 1}]
@@ -176,9 +262,16 @@ __global__ void k_band_reduce(BandMvArgs a) {
   }
 }
 
+size_t band_smem_bytes(int act_words) {
+  return (size_t)kBandStages * kBandChunk * sizeof(BandTile) + 2 * kBandStages * sizeof(unsigned long long) +
+         (size_t)(act_words + 1) * sizeof(unsigned);
+}
+
 template <int TT>
 int launch_tt(const BandMvArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)a.nS * sizeof(unsigned);
+  const size_t smem = band_smem_bytes(a.act_words);
+  if (smem > 48 * 1024)
+    TDB_CUDA_CHECK(cudaFuncSetAttribute(k_band_mv<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_band_mv<TT><<<(unsigned)((long long)a.nRB * a.P), a.W * 32, smem, st>>>(a);
   TDB_CUDA_CHECK(cudaGetLastError());
   return TDB_OK;
@@ -195,13 +288,13 @@ int band_build(TdbSystem* sys, int f) {
     return TDB_E_NOMEM;
   }
   TDB_REQUIRE(sys->p == 0, "band tiles: built for p = 0 only");
+  FamilyStore& fs = sys->fam[f];
+  TDB_REQUIRE(fs.npos <= 124, "band tiles: at most 124 positions per family");
   cudaStream_t st = sys->ctx->stream;
   const int NR = sys->nrows, nRB = sys->nRB, V = (int)sys->V;
-  FamilyStore& fs = sys->fam[f];
-  const int nS = (fs.npos + 3) / 4;
   const long long n = fs.nnz;
   unsigned long long *k0 = nullptr, *k1 = nullptr;
-  long long *i0 = nullptr, *i1 = nullptr;
+  long long *i0 = nullptr, *i1 = nullptr, *seg = nullptr;
   int *head = nullptr, *tile_rb = nullptr;
   void* tmp = nullptr;
   auto release = [&]() {
@@ -209,35 +302,34 @@ int band_build(TdbSystem* sys, int f) {
     dev_free(k1);
     dev_free(i0);
     dev_free(i1);
+    dev_free(seg);
     dev_free(head);
     dev_free(tile_rb);
     dev_free(tmp);
+    k0 = k1 = nullptr;
+    i0 = i1 = seg = nullptr;
+    head = tile_rb = nullptr;
+    tmp = nullptr;
   };
   auto fail = [&](cudaError_t e) {
     release();
     dev_free(b.rbptr);
-    dev_free(b.col);
-    dev_free(b.stile);
-    dev_free(b.val);
+    dev_free(b.tiles);
     b.rbptr = nullptr;
-    b.col = b.stile = nullptr;
-    b.val = nullptr;
-    b.failed = true;  // sticky: later plans go straight to CSR
+    b.tiles = nullptr;
+    b.failed = true;  // sticky: later plans go straight to CSR without retrying
     set_error(std::string("band tiles build: ") + cudaGetErrorString(e));
     return e == cudaErrorMemoryAllocation ? TDB_E_NOMEM : TDB_E_CUDA;
   };
-#define TRY(expr)                       \
-  do {                                  \
-    cudaError_t e_ = (expr);            \
+#define TRY(expr)                           \
+  do {                                      \
+    cudaError_t e_ = (expr);                \
     if (e_ != cudaSuccess) return fail(e_); \
   } while (0)
   TRY(dev_malloc((void**)&b.rbptr, (size_t)(nRB + 1) * sizeof(int64_t)));
-  b.nS = nS;
   if (n == 0) {
     TRY(cudaMemsetAsync(b.rbptr, 0, (size_t)(nRB + 1) * sizeof(int64_t), st));
-    TRY(dev_malloc((void**)&b.col, sizeof(int32_t)));
-    TRY(dev_malloc((void**)&b.stile, sizeof(int32_t)));
-    TRY(dev_malloc((void**)&b.val, 32 * sizeof(double)));
+    TRY(dev_malloc((void**)&b.tiles, sizeof(BandTile)));
     TRY(cudaStreamSynchronize(st));
     b.built = true;
     return TDB_OK;
@@ -246,21 +338,25 @@ int band_build(TdbSystem* sys, int f) {
   TRY(dev_malloc((void**)&k1, n * sizeof(unsigned long long)));
   TRY(dev_malloc((void**)&i0, n * sizeof(long long)));
   TRY(dev_malloc((void**)&i1, n * sizeof(long long)));
+  TRY(dev_malloc((void**)&seg, n * sizeof(long long)));
   TRY(dev_malloc((void**)&head, n * sizeof(int)));
-  k_band_keys<<<148 * 16, 256, 0, st>>>(fs.indptr, fs.indices, (long long)fs.npos * NR, NR, V, nS, sys->d_rinv,
-                                        k0, i0);
+  k_band_keys<<<148 * 16, 256, 0, st>>>(fs.indptr, fs.indices, (long long)fs.npos * NR, NR, V, sys->d_rinv, k0, i0);
   TRY(cudaGetLastError());
-  int end_bit = 5;
+  int end_bit = 10;
   {
-    const unsigned long long maxkey = (unsigned long long)nRB * (unsigned long long)V * (unsigned long long)nS;
-    while (end_bit < 64 && (maxkey >> (end_bit - 5)) != 0) ++end_bit;
+    const unsigned long long maxjl = (unsigned long long)nRB * (unsigned long long)V;
+    while (end_bit < 64 && (maxjl >> (end_bit - 10)) != 0) ++end_bit;
   }
-  size_t tb = 0, tb2 = 0;
+  size_t tb = 0, tb2 = 0, tb3 = 0;
   TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, i0, i1, n, 0, end_bit, st));
   TRY(cub::DeviceScan::InclusiveSum(nullptr, tb2, head, head, n, st));
-  TRY(dev_malloc(&tmp, std::max(tb, tb2)));
+  TRY(cub::DeviceScan::InclusiveScan(nullptr, tb3, seg, seg, MaxLL(), n, st));
+  TRY(dev_malloc(&tmp, std::max(tb, std::max(tb2, tb3))));
   TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, i0, i1, n, 0, end_bit, st));
-  k_band_heads<<<148 * 16, 256, 0, st>>>(k1, n, head);
+  k_band_seg<<<148 * 16, 256, 0, st>>>(k1, n, seg);
+  TRY(cudaGetLastError());
+  TRY(cub::DeviceScan::InclusiveScan(tmp, tb3, seg, seg, MaxLL(), n, st));
+  k_band_heads<<<148 * 16, 256, 0, st>>>(k1, seg, n, head);
   TRY(cudaGetLastError());
   TRY(cub::DeviceScan::InclusiveSum(tmp, tb2, head, head, n, st));
   int nt = 0;
@@ -268,12 +364,10 @@ int band_build(TdbSystem* sys, int f) {
   TRY(cudaStreamSynchronize(st));
   b.ntiles = nt;
   b.nnz = n;
-  TRY(dev_malloc((void**)&b.col, (size_t)nt * sizeof(int32_t)));
-  TRY(dev_malloc((void**)&b.stile, (size_t)nt * sizeof(int32_t)));
-  TRY(dev_malloc((void**)&b.val, (size_t)nt * 32 * sizeof(double)));
+  TRY(dev_malloc((void**)&b.tiles, (size_t)nt * sizeof(BandTile)));
   TRY(dev_malloc((void**)&tile_rb, (size_t)nt * sizeof(int)));
-  TRY(cudaMemsetAsync(b.val, 0, (size_t)nt * 32 * sizeof(double), st));
-  k_band_fill<<<148 * 16, 256, 0, st>>>(k1, i1, head, n, V, nS, fs.data, b.col, b.stile, b.val, tile_rb);
+  TRY(cudaMemsetAsync(b.tiles, 0, (size_t)nt * sizeof(BandTile), st));
+  k_band_fill<<<148 * 16, 256, 0, st>>>(k1, i1, seg, head, n, V, fs.data, b.tiles, tile_rb);
   TRY(cudaGetLastError());
   k_band_rbptr<<<(nRB + 256) / 256, 256, 0, st>>>(tile_rb, nt, nRB, b.rbptr);
   TRY(cudaGetLastError());

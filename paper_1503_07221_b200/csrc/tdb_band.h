@@ -9,18 +9,20 @@
 namespace tdb {
 
 constexpr int kBandMaxWarps = 8;  // time-group warps per CTA
+constexpr int kBandChunk = 32;    // tile records per bulk-copy stage
+constexpr int kBandStages = 3;    // stages of the shared-memory ring
 
 struct BandMvArgs {
   int nRB, P, nT, TT, W;  // row blocks, parts per row block, 8-step time tiles, tiles per warp, warps per CTA
-  int nrows, nS;          // owned rows, S-tiles (4 positions each)
+  int nrows, act_words;   // owned rows, words of the active-position bit set
   int ktlo, nkt, rlo;     // band rows kt in [ktlo, ktlo + nkt); y row index kt - rlo
   int off0, xs;           // xt column of (kt = ktlo, lag d_0) and row stride
+  int dt0, dt1;           // itlo + d_0 - ktlo, ithi + d_0 - ktlo: valid rows of lag d_0 + s are
+                          // ktlo + [dt0 + s, dt1 + s]
   int ldy;                // ypart row stride (>= 8 nT)
-  const int32_t* col;
-  const int32_t* stile;
-  const double* val;
+  const BandTile* tiles;
   const int64_t* rbptr;
-  const unsigned* s_act;  // (nS,) bit k: position 4 S + k is a band term of this plan
+  const unsigned* s_act;  // (act_words,) bit s: position s is a band term of this plan
   const int* rperm;       // Morton row -> local row
   const double* xt;       // [V][xs] vertex-major x of the plan's inner columns, zero pads
   double* ypart;          // [P][nRB * 8][ldy]
@@ -29,6 +31,7 @@ struct BandMvArgs {
 
 int band_build(TdbSystem* sys, int f);
 int band_mv_tiles(const BandMvArgs& a, cudaStream_t st);   // tile kernel -> ypart
+size_t band_smem_bytes(int act_words);
 int band_mv_reduce(const BandMvArgs& a, cudaStream_t st);  // y += sum of parts (ordered)
 
 }  // namespace tdb

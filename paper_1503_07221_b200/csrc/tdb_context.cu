@@ -186,9 +186,7 @@ int tdb_system_destroy(TdbSystem* sys) {
     dev_free(f.shi);
   }
   for (auto& b : sys->band) {
-    dev_free(b.col);
-    dev_free(b.stile);
-    dev_free(b.val);
+    dev_free(b.tiles);
     dev_free(b.rbptr);
   }
   dev_free(sys->d_vperm);

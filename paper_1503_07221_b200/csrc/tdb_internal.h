@@ -50,16 +50,19 @@ struct FRange {
   int lo_cnt;  // s_lo | (cnt << 16)
 };
 
-// One family's stored blocks as lag-band tiles (tdb_band.cu): 8 test rows
-// (Morton row block J) x 4 consecutive positions (S-tile) of ONE column vertex l,
-// A-fragment order (lane = 4 * row + position % 4), sorted (J, l, S).
+// One lag-band tile record (tdb_band.cu): 8 test rows (Morton row block J) x 4
+// consecutive positions s0 .. s0+3 of ONE column vertex l, A-fragment order
+// (v[4 * row + (s - s0)]), header in the same 16-byte-aligned record (bulk copies).
+struct __align__(16) BandTile {
+  double v[32];
+  int32_t l, s0, pad0, pad1;
+};
+
+// One family's stored blocks as lag-band tiles, sorted (J, l, s0).
 struct BandStore {
   bool built = false, failed = false;
   long long ntiles = 0, nnz = 0;
-  int nS = 0;
-  int32_t* col = nullptr;     // (ntiles,) column vertex
-  int32_t* stile = nullptr;   // (ntiles,) S-tile
-  double* val = nullptr;      // (ntiles, 32)
+  BandTile* tiles = nullptr;  // (ntiles,)
   int64_t* rbptr = nullptr;   // (nRB + 1,)
 };
 

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cmath>
 
 #include "tdb_common.cuh"
@@ -253,10 +254,20 @@ int tdb_krylov_arnoldi(const double* V, int64_t ldv, int64_t n, int32_t k, doubl
                        double* H, int32_t ldh, double* cs, double* sn, double* g, double* vnext, void* stream) {
   TDB_REQUIRE(V && w && hcol && n > 0 && k >= 0 && k < kArnMaxK, "krylov_arnoldi: bad argument");
   TDB_REQUIRE(H == nullptr || (state && cs && sn && g && ldh > k), "krylov_arnoldi: bad Givens arguments");
-  static int csize = [] {
-    cudaFuncSetAttribute(k_krylov_arnoldi, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    return 16;
-  }();
+  // the non-portable cluster size is a per-device function attribute: set it once per
+  // device (bit set under a mutex; a second GPU in the same process gets its own call)
+  static std::mutex mu;
+  static unsigned long long done = 0ull;
+  int dev = 0;
+  TDB_CUDA_CHECK(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> g_(mu);
+    if (dev < 64 && !((done >> dev) & 1ull)) {
+      TDB_CUDA_CHECK(cudaFuncSetAttribute(k_krylov_arnoldi, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      done |= 1ull << dev;
+    }
+  }
+  const int csize = 16;
   // cluster of up to 16 CTAs (one per SM), at least ~512 elements per CTA
   int cls = (int)std::min<long long>(csize, std::max<long long>(1, n / 512));
   cudaLaunchConfig_t cfg = {};

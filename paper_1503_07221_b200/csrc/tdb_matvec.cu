@@ -696,10 +696,10 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
       }
   }
   const BandStore& bs = sys->band[tf];
-  const int nS = bs.nS, V = (int)sys->V, nRB = sys->nRB;
-  std::vector<unsigned> sact(nS, 0u);
+  const int act_words = (npos + 31) / 32 + 1, V = (int)sys->V, nRB = sys->nRB;
+  std::vector<unsigned> sact(act_words, 0u);
   for (int s_ = 0; s_ < npos; ++s_)
-    if (term_of[s_] >= 0) sact[s_ >> 2] |= 1u << (s_ & 3);
+    if (term_of[s_] >= 0) sact[s_ >> 5] |= 1u << (s_ & 31);
   // time tiles per warp (<= 6), warps per CTA
   const int W = std::min(kBandMaxWarps, (nT + 5) / 6);
   const int TT = (nT + W - 1) / W;
@@ -709,19 +709,20 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   }
   // xt column of (kt, lag d): PADL + (kt - d - itlo); off0 = column of (ktlo + n, d0 + 4 S + k) + 4 S + k - n
   const int base = ktlo - itlo - d0;
-  const int padl = std::max(0, 4 * (nS - 1) + 3 - base);
+  const int padl = std::max(0, npos + 2 - base);  // window start lags s0 <= npos - 1
   const int off0 = padl + base;
   const int ncols = ithi - itlo + 1;
   int xs = std::max(padl + ncols, off0 + 8 * W * TT + 8);
   xs = (xs + 1) & ~1;
   const long long tiles_per_rb = bs.ntiles / std::max(1, nRB);
-  static const int band_warps = [] {
-    const char* e = std::getenv("TDB_BAND_WARPS_PER_SM");
-    return e ? std::max(1, std::atoi(e)) : 32;
+  // parts per row block: ~8 CTAs per SM (shared-memory ring), >= 2 stages of tiles per part
+  static const int band_ctas = [] {
+    const char* e = std::getenv("TDB_BAND_CTAS_PER_SM");
+    return e ? std::max(1, std::atoi(e)) : 8;
   }();
   const int P = (int)std::max<long long>(
-      1, std::min<long long>({64LL, (long long)sys->ctx->num_sms * band_warps / std::max(1, nRB * W),
-                              tiles_per_rb / 32}));
+      1, std::min<long long>({64LL, ((long long)sys->ctx->num_sms * band_ctas + nRB - 1) / std::max(1, nRB),
+                              tiles_per_rb / (2 * kBandChunk)}));
   const int ldy = 8 * W * TT;
   cudaStream_t st = sys->ctx->stream;
   const size_t xt_n = (size_t)V * xs;
@@ -737,7 +738,7 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
     if ((n) > 0 && (src) != nullptr)                                                               \
       cudaMemcpyAsync((dst), (src), (size_t)(n) * sizeof(T_), cudaMemcpyHostToDevice, st);         \
   } while (0)
-  ALLOC_COPY3(p->d_sact, sact.data(), nS, unsigned);
+  ALLOC_COPY3(p->d_sact, sact.data(), act_words, unsigned);
   ALLOC_COPY3(p->d_bypart, (const double*)nullptr, yp_n, double);
   ALLOC_COPY3(p->d_bxt, (const double*)nullptr, xt_n, double);
   cudaMemsetAsync(p->d_bxt, 0, xt_n * sizeof(double), st);  // zero pads (never written again)
@@ -750,16 +751,16 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   ba.TT = TT;
   ba.W = W;
   ba.nrows = sys->nrows;
-  ba.nS = nS;
+  ba.act_words = act_words;
   ba.ktlo = ktlo;
   ba.nkt = nkt;
   ba.rlo = d->rlo;
   ba.off0 = off0;
+  ba.dt0 = itlo + d0 - ktlo;
+  ba.dt1 = ithi + d0 - ktlo;
   ba.xs = xs;
   ba.ldy = ldy;
-  ba.col = bs.col;
-  ba.stile = bs.stile;
-  ba.val = bs.val;
+  ba.tiles = bs.tiles;
   ba.rbptr = bs.rbptr;
   ba.s_act = p->d_sact;
   ba.rperm = sys->d_rperm;

@@ -1,4 +1,4 @@
-"""Row-block sharding over GPUs: one process per GPU, NCCL over NVLink.
+"""Sharding over GPUs by row blocks and lags: one process per GPU, NCCL over NVLink.
 
 Assembly needs no communication: rank r owns a set of test-vertex rows J_r and
 assembles exactly those CSR rows of every canonical block from the pairs whose
@@ -13,6 +13,15 @@ all-gathers the iterate (one ncclAllGather of L*(p+1)*max|J_r| doubles into a
 rank-major buffer), the kernel reads it through an index map (no reshuffle
 copy) and produces the rank's rows of y.  Krylov dots/norms are all-reduced
 (solvers.TorchDistComm).
+
+Lag split (the north star's "by lag and row blocks"; the paper's diagonal-wise block
+ownership, PAPER.md 5.1 / ref/block_system.py:86-129): with lag_groups = G the world
+is R x G, rank = rb * G + lg.  Rank (rb, lg) assembles the rows of row block rb for
+the lg-th contiguous lag range of every table family only (partition_lags).  Its
+matvec produces the partial rows over those lags, summed over the G ranks of the row
+block by one all-reduce (the paper's gather-sum); the iterate is
+all-gathered within the row group (the R ranks sharing lg), and Krylov dot products
+are all-reduced over the row group too (vectors are replicated over the lag group).
 """
 
 from __future__ import annotations
@@ -27,7 +36,8 @@ from .assembly import DeviceAssembly, QuadratureConfig, as_product_inputs, build
 from .block_system import canonical_position, canonical_positions, is_zero_position
 from .kernel_weights import tables_for
 
-__all__ = ["partition_rows", "gathered_x_map", "DistributedBlockHessenbergMatrix", "assemble_system_distributed"]
+__all__ = ["partition_rows", "partition_lags", "gathered_x_map", "make_groups", "DistributedBlockHessenbergMatrix",
+           "assemble_system_distributed"]
 
 
 def partition_rows(mesh, nparts: int):
@@ -51,6 +61,45 @@ def partition_rows(mesh, nparts: int):
             need[ids[off[j] : off[j + 1]]] = True
         tests.append(np.flatnonzero(need))
     return rows, tests
+
+
+def partition_lags(grid, positions, groups: int):
+    """Canonical positions -> `groups` lists: every table family (positions sharing
+    (ansatz kind, test kind), in lag order) cut into contiguous lag ranges of near-equal
+    length, so each group keeps consecutive lags (the band tiles need them) and the
+    small-lag positions carrying the singular pairs are spread over the ranges of every
+    family."""
+    from .temporal_basis import timestep_kind
+
+    fams: dict = {}
+    for kt, it in positions:
+        fams.setdefault((timestep_kind(grid, it), timestep_kind(grid, kt)), []).append((kt, it))
+    out = [[] for _ in range(groups)]
+    for key in sorted(fams):
+        pos = sorted(fams[key], key=lambda p: p[0] - p[1])
+        n = len(pos)
+        for g in range(groups):
+            out[g] += pos[(n * g) // groups:(n * (g + 1)) // groups]
+    return [sorted(o) for o in out]
+
+
+def make_groups(rows: int, lags: int):
+    """torch.distributed process groups of a rows x lags world (every rank calls this):
+    (row group of this rank: the `rows` ranks sharing its lag group, lag group of this
+    rank: the `lags` ranks sharing its row block)."""
+    import torch.distributed as dist
+
+    rank = dist.get_rank()
+    mine_row = mine_lag = None
+    for lg in range(lags):
+        g = dist.new_group([rb * lags + lg for rb in range(rows)])
+        if rank % lags == lg:
+            mine_row = g
+    for rb in range(rows):
+        g = dist.new_group([rb * lags + lg for lg in range(lags)])
+        if rank // lags == rb:
+            mine_lag = g
+    return mine_row, mine_lag
 
 
 def gathered_x_map(rows_per_rank, M: int, ncols: int, nmax: int) -> np.ndarray:
@@ -116,27 +165,40 @@ class _DistMatvecPlan:
 
 
 class DistributedBlockHessenbergMatrix:
-    """This rank's rows of the block Hessenberg matrix (duck-types BlockHessenbergMatrix
-    for the solvers: .grid, .M (local rows), .matvec(x_local, rows, cols))."""
+    """This rank's share of the block Hessenberg matrix (duck-types BlockHessenbergMatrix
+    for the solvers: .grid, .M (local rows), .matvec(x_local, rows, cols)).
+
+    rows_per_rank: the R row blocks (partition_rows); rank = rb * lag_groups + lg.
+    row_group / lag_group: torch.distributed groups (make_groups) for the all-gather of
+    the iterate and the partial-row sum; gather / reduce callbacks replace them (tests).
+    """
 
     def __init__(self, mesh, grid, rows_per_rank, rank: int, ctx=None, tables=None,
-                 config: QuadratureConfig = QuadratureConfig(), gather=None):
+                 config: QuadratureConfig = QuadratureConfig(), gather=None, lag_groups: int = 1,
+                 row_group=None, lag_group=None, reduce=None):
         mesh, grid = as_product_inputs(mesh, grid)
         self.grid = grid
         self.diameter = mesh.diameter
         self.rank = rank
+        self.lag_groups = lag_groups
+        self.rb, self.lg = rank // lag_groups, rank % lag_groups
         self.rows_per_rank = rows_per_rank
         self.nparts = len(rows_per_rank)
-        self.rows = rows_per_rank[rank]
+        self.rows = rows_per_rank[self.rb]
         self.M_global = mesh.num_vertices
         self.M = len(self.rows)  # local rows (what the solvers' half-splits use)
         self.nmax = max(len(r) for r in rows_per_rank)
         tables = tables_for(grid) if tables is None else tables
-        plan = build_plan(mesh, grid, tables, canonical_positions(grid, mesh.diameter), config)
+        positions = canonical_positions(grid, mesh.diameter)
+        if lag_groups > 1:
+            positions = partition_lags(grid, positions, lag_groups)[self.lg]
+        plan = build_plan(mesh, grid, tables, positions, config)
         self.dev = DeviceAssembly(mesh, plan, ctx or _lib.default_context(), rows=self.rows)
         self._plans: dict = {}
         # gather(local_padded (ncols, nmax) tensor) -> (nparts, ncols, nmax) tensor
         self._gather = gather
+        self._reduce = reduce
+        self.row_group, self.lag_group = row_group, lag_group
 
     @property
     def shape_local(self):
@@ -157,8 +219,19 @@ class DistributedBlockHessenbergMatrix:
         import torch.distributed as dist
 
         out = torch.empty((self.nparts, ncols, self.nmax), dtype=x_local.dtype, device=x_local.device)
-        dist.all_gather_into_tensor(out, pad.contiguous())
+        dist.all_gather_into_tensor(out, pad.contiguous(), group=self.row_group)
         return out
+
+    def reduce_lags(self, y: torch.Tensor) -> torch.Tensor:
+        """Sum the partial rows over the lag group (the paper's gather-sum)."""
+        if self.lag_groups == 1:
+            return y
+        if self._reduce is not None:
+            return self._reduce(y)
+        import torch.distributed as dist
+
+        dist.all_reduce(y, group=self.lag_group)
+        return y
 
     def matvec(self, x_local: torch.Tensor, rows=None, cols=None) -> torch.Tensor:
         np1 = self.grid.p + 1
@@ -175,7 +248,7 @@ class DistributedBlockHessenbergMatrix:
             self.dev.ctx.set_stream(torch.cuda.current_stream(x_local.device).cuda_stream)
             _lib.check(_lib.LIB.tdb_matvec(plan.handle, C.c_void_p(xg.data_ptr()), C.c_void_p(y.data_ptr())),
                        "matvec")
-        return y
+        return self.reduce_lags(y)
 
     def __matmul__(self, x):
         return self.matvec(x)
@@ -190,8 +263,15 @@ class DistributedBlockHessenbergMatrix:
 
 
 def assemble_system_distributed(mesh, grid, rank: int, world: int, ctx=None, tables=None,
-                                config: QuadratureConfig = QuadratureConfig()):
-    """Assemble this rank's row block (torch.distributed must be initialised for matvecs)."""
+                                config: QuadratureConfig = QuadratureConfig(), lag_groups: int = 1):
+    """Assemble this rank's (row block, lag range) share; torch.distributed must be
+    initialised (every rank calls this: it creates the process groups)."""
     mesh, grid = as_product_inputs(mesh, grid)
-    rows, _ = partition_rows(mesh, world)
-    return DistributedBlockHessenbergMatrix(mesh, grid, rows, rank, ctx=ctx, tables=tables, config=config)
+    if world % lag_groups:
+        raise ValueError(f"lag_groups {lag_groups} must divide the world size {world}")
+    rows, _ = partition_rows(mesh, world // lag_groups)
+    row_group = lag_group = None
+    if lag_groups > 1:
+        row_group, lag_group = make_groups(world // lag_groups, lag_groups)
+    return DistributedBlockHessenbergMatrix(mesh, grid, rows, rank, ctx=ctx, tables=tables, config=config,
+                                            lag_groups=lag_groups, row_group=row_group, lag_group=lag_group)

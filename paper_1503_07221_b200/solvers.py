@@ -78,6 +78,7 @@ class _LocalComm:
     """Single device: vectors are whole, reductions are no-ops."""
 
     size = 1
+    capturable = True
 
     def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
         return t
@@ -94,6 +95,9 @@ class TorchDistComm:
         self.dist = dist
         self.group = group
         self.size = dist.get_world_size(group)
+        # NCCL collectives can be captured in a CUDA graph (the preconditioner is
+        # replayed as one graph per outer step); gloo ones cannot
+        self.capturable = dist.get_backend(group) == "nccl"
 
     def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
         self.dist.all_reduce(t, group=self.group)
@@ -240,12 +244,22 @@ def _gmres_cycle_raw(apply_A, b, x0, m, tol_abs, precond, history):
                                                    None, None, None,
                                                    C_void(torch.cuda.current_stream(dev).cuda_stream)),
                        "krylov_arnoldi")
+        elif _COMM.size > 1:
+            # row-block distributed vectors: classical Gram-Schmidt with one re-orthogonalisation
+            # pass, each pass ONE batched all-reduce of the k+1 coefficients, then
+            # the norm: 3 collectives per Arnoldi step instead of k+2 for MGS
+            Vk = V[: k + 1]
+            h = _gemv_t(Vk, w)
+            w.sub_(torch.mv(Vk.T, h))
+            h2 = _gemv_t(Vk, w)
+            w.sub_(torch.mv(Vk.T, h2))
+            torch.add(h, h2, out=hcol[: k + 1])
+            hcol[k + 1] = _norm(w)
         else:
             # modified Gram-Schmidt: h_j computed and subtracted one vector at a time
+            # (the reference's order, solvers.py:194-198)
             for j in range(k + 1):
                 torch.dot(V[j], w, out=hcol[j])
-                if _COMM.size > 1:
-                    _COMM.allreduce_(hcol[j : j + 1])
                 w.addcmul_(V[j], hcol[j : j + 1], value=-1.0)
             hcol[k + 1] = _norm(w)
         col = hcol[: k + 2].cpu().numpy()
@@ -441,8 +455,10 @@ def _inner_solve(apply_A, r, icfg: SolverConfig, precond, err: _ErrBox):
 
 
 class _GraphedPreconditioner:
-    """r -> P r of the recursive preconditioner, captured once in a CUDA graph
-    (single device; two eager warm-up calls create every matvec plan first)."""
+    """r -> P r of the recursive preconditioner, captured once in a CUDA graph after
+    two eager warm-up calls (which create every matvec plan and communicator).  With
+    row-block distributed vectors the capture includes the NCCL all-gathers and
+    all-reduces (comm.capturable); a gloo communicator stays eager."""
 
     def __init__(self, fn, err: _ErrBox):
         self.fn = fn
@@ -459,7 +475,7 @@ class _GraphedPreconditioner:
         if not r.is_cuda:
             return self.fn(r)
         self.calls += 1
-        if _COMM.size > 1 or self.calls <= 2:
+        if not getattr(_COMM, "capturable", _COMM.size == 1) or self.calls <= 2:
             out = self.fn(r)
             self._check()
             return out

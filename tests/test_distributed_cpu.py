@@ -116,3 +116,27 @@ def test_distributed_krylov_matches_single_process():
     assert np.linalg.norm(xd - ref) <= 1e-10 * np.linalg.norm(ref)
     assert out[0][2] == out[1][2]  # replicated Hessenberg logic: same iteration count on all ranks
     assert out[0][4] == out[1][4]
+
+
+@pytest.mark.parametrize("groups", [1, 2, 3, 4])
+def test_partition_lags_contiguous_cover(groups):
+    from paper_1503_07221_b200.block_system import canonical_positions
+    from paper_1503_07221_b200.configs import get_config
+    from paper_1503_07221_b200.distributed import partition_lags
+    from paper_1503_07221_b200.temporal_basis import timestep_kind
+
+    cfg = get_config(2)
+    mesh, grid = cfg.mesh(), cfg.grid()
+    pos = canonical_positions(grid, mesh.diameter)
+    parts = partition_lags(grid, pos, groups)
+    flat = [p for part in parts for p in part]
+    assert sorted(flat) == sorted(pos) and len(flat) == len(set(flat))
+    for part in parts:  # every family's share is a run of consecutive lags
+        fam = {}
+        for kt, it in part:
+            fam.setdefault((timestep_kind(grid, it), timestep_kind(grid, kt)), []).append(kt - it)
+        for lags in fam.values():
+            lags.sort()
+            assert lags == list(range(lags[0], lags[0] + len(lags)))
+    sizes = [len(p) for p in parts]
+    assert max(sizes) - min(sizes) <= 8  # <= 1 per family (up to 7 families)

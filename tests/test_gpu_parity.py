@@ -374,3 +374,20 @@ def test_tiled_vs_csr_only_plan_agree(G, cfg1_mesh, tmp_path):
     yc = np.load(tmp_path / "y.npy")
     assert np.linalg.norm(ys[0] - yc[0]) <= 1e-13 * np.linalg.norm(yc[0])
     assert np.linalg.norm(ys[1] - yc[1][: 20 * M]) <= 1e-13 * np.linalg.norm(yc[1][: 20 * M])
+
+
+def test_matvec_long_time_axis_row_chunks(G, ico):
+    # N > 384 block rows: the matvec is applied in row chunks of MAX_PLAN_ROWS, one plan each
+    # (ADVICE r01); compared with the oracle's reference-order block matvec
+    from oracle import assembly as OA
+    from paper_1503_07221_b200.temporal_basis import TimeGrid
+
+    grid = TimeGrid(T=10.0, N=401, p=0)
+    A = G[2].assemble_system(ico, grid)
+    x = np.random.default_rng(4).standard_normal(A.shape[1])
+    y = A.matvec(x)
+    y_ref = OA.matvec(grid, ico.num_vertices, ico.diameter, A.unique_blocks, x)
+    assert np.linalg.norm(y - y_ref) <= 1e-12 * np.linalg.norm(y_ref)
+    A.MAX_PLAN_ROWS = 7  # many chunks, ragged last one
+    y7 = A.matvec(x, rows=(3, 390), cols=(1, 401))
+    assert np.linalg.norm(y7 - y_ref[2 * ico.num_vertices:390 * ico.num_vertices]) <= 1e-12 * np.linalg.norm(y7)

@@ -87,12 +87,15 @@ def test_tables_match_reference(T, N, p):
     assert seen > 0
 
 
-def test_rhs_matches_reference(two_tri):
-    from paper_1503_07221_b200.assembly import assemble_rhs, gaussian_pulse_neumann
+def test_oracle_rhs_matches_reference(two_tri):
+    # the oracle's host restatement of the reference loop (the product's RHS is GPU-only,
+    # tests/test_gpu_rhs.py); the Gaussian datum's host callback is the product's
+    from oracle.assembly import assemble_rhs
+    from paper_1503_07221_b200.assembly import gaussian_pulse_neumann
 
     g = golden("rhs.npz")
     m = M.icosphere(2)
-    b = assemble_rhs(m, TimeGrid(T=3.9, N=40, p=0), gaussian_pulse_neumann(m), device=False)
+    b = assemble_rhs(m, TimeGrid(T=3.9, N=40, p=0), gaussian_pulse_neumann(m))
     assert np.max(np.abs(b - g["cfg1_pulse"])) <= 1e-14 * np.max(np.abs(g["cfg1_pulse"]))
 
     def gs(X, t):

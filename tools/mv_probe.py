@@ -29,4 +29,4 @@ for rows, cols in ranges:
     pl = A.matvec_plan(rows, cols)
     ms = e0.elapsed_time(e1) / 20
     print(f"matvec rows{rows} cols{cols}: {ms:.4f} ms  bytes {pl.bytes:.3e} flops {pl.flops:.3e} "
-          f"nterms {pl.nterms}  {pl.bytes / ms / 1e6:.0f} GB/s", flush=True)
+          f"nterms {pl.nterms} tiled {pl.tiled_terms} csr {pl.csr_terms}  {pl.bytes / ms / 1e6:.0f} GB/s", flush=True)
