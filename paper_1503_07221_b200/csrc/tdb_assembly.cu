@@ -193,6 +193,7 @@ struct PlanArgs {
   unsigned long long* case_pairs;  // [4] pairs with >= 1 unit, [4..7] units, per case,
                                    // [8] units of pairs whose test triangle's first vertex is owned
   const unsigned char* owned;      // (V,) owned test-vertex rows of this system
+  int wlo[kMaxFamilies], whi[kMaxFamilies];  // position batch: family f's positions [wlo, whi)
 };
 
 __global__ void k_plan_pairs(PlanArgs a) {
@@ -231,8 +232,8 @@ __global__ void k_plan_pairs(PlanArgs a) {
     int units = 0;
     for (int f = 0; f < a.F; ++f) {
       const int n = s_off[f + 1] - s_off[f];
-      int s0 = first_geq(s_hi + s_off[f], n, dmin);  // shi >= tmin
-      int s1 = last_leq(s_lo + s_off[f], n, dmax);   // slo <= tmax
+      int s0 = max(a.wlo[f], first_geq(s_hi + s_off[f], n, dmin));  // shi >= tmin
+      int s1 = min(a.whi[f] - 1, last_leq(s_lo + s_off[f], n, dmax));  // slo <= tmax
       int cnt = s1 >= s0 ? s1 - s0 + 1 : 0;
       FRange fr;
       fr.foff = units;
@@ -1422,6 +1423,10 @@ struct AsmWorkspace {
   std::vector<Launch> launches;
   std::vector<int> s_chunk;
   int words = 0;
+  // position batches (bounded partial buffer): batch b covers family f's positions
+  // [wlo[b][f], whi[b][f]); one batch = every position
+  int nbatch = 1;
+  std::vector<std::vector<int>> wlo, whi;
   cudaEvent_t ev[6];
   bool events = false;
   long long launch_count = 0;
@@ -1487,9 +1492,13 @@ static int read_ll(const long long* dev, long long* host, cudaStream_t st) {
   return TDB_OK;
 }
 
-static PlanArgs plan_args(TdbSystem* sys) {
+static PlanArgs plan_args(TdbSystem* sys, int b) {
   AsmWorkspace* ws = sys->ws;
   PlanArgs pa;
+  for (int f = 0; f < kMaxFamilies; ++f) {
+    pa.wlo[f] = f < sys->F ? ws->wlo[b][f] : 0;
+    pa.whi[f] = f < sys->F ? ws->whi[b][f] : 0;
+  }
   pa.E = (int)sys->E;
   pa.F = sys->F;
   pa.Et = ws->Et;
@@ -1538,10 +1547,10 @@ static PatternArgs pattern_args(TdbSystem* sys, int f) {
 }
 
 // plan kernels (bounds, ranges, scans, items) - no host sync
-static int run_plan(TdbSystem* sys, cudaStream_t st) {
+static int run_plan(TdbSystem* sys, cudaStream_t st, int b = 0) {
   AsmWorkspace* ws = sys->ws;
   TDB_CUDA_CHECK(cudaMemsetAsync(ws->counters, 0, 64 * sizeof(unsigned long long), st));
-  PlanArgs pa = plan_args(sys);
+  PlanArgs pa = plan_args(sys, b);
   const long long blocks = std::min<long long>((ws->E2 + 255) / 256, 148LL * 32);
   int ntot = 0;
   for (int f = 0; f < sys->F; ++f) ntot += sys->fam[f].npos;
@@ -1561,46 +1570,55 @@ static int run_plan(TdbSystem* sys, cudaStream_t st) {
   return TDB_OK;
 }
 
-static int run_pattern_count(TdbSystem* sys, int f, cudaStream_t st, void* tmp = nullptr) {
+// CSR row counts of family f's positions [s_lo, s_hi) (the current pair plan must
+// cover them), then (scan = true) the exclusive scan of every row count of the family
+static int run_pattern_count(TdbSystem* sys, int f, cudaStream_t st, void* tmp = nullptr, int s_lo = 0,
+                             int s_hi = -1, bool scan = true) {
   AsmWorkspace* ws = sys->ws;
   PatternArgs ga = pattern_args(sys, f);
   const int npos = ga.npos;
-  for (int s0 = 0; s0 < npos; s0 += ws->s_chunk[f]) {
+  if (s_hi < 0) s_hi = npos;
+  for (int s0 = s_lo; s0 < s_hi; s0 += ws->s_chunk[f]) {
     ga.s_begin = s0;
-    ga.s_count = std::min(ws->s_chunk[f], npos - s0);
+    ga.s_count = std::min(ws->s_chunk[f], s_hi - s0);
     const size_t smem = (size_t)ga.s_count * ws->words * 4;
     TDB_CUDA_CHECK(cudaFuncSetAttribute(k_pattern_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
     k_pattern_count<<<ws->nrows, 256, smem, st>>>(ga);
     TDB_CUDA_CHECK(cudaGetLastError());
   }
+  if (!scan) return TDB_OK;
   const long long nrows = (long long)npos * ws->nrows;
   TDB_CUDA_CHECK(cudaMemsetAsync(ga.row_count + nrows, 0, sizeof(long long), st));
   return scan_inplace(ws, ga.row_count, nrows + 1, st, tmp);
 }
 
-int tdb_system_run_impl(TdbSystem* sys) {
+static int run_pattern_fill(TdbSystem* sys, int f, cudaStream_t st, int s_lo = 0, int s_hi = -1) {
+  AsmWorkspace* ws = sys->ws;
+  PatternArgs ga = pattern_args(sys, f);
+  if (s_hi < 0) s_hi = ga.npos;
+  int rc;
+  for (int s0 = s_lo; s0 < s_hi; s0 += ws->s_chunk[f]) {
+    ga.s_begin = s0;
+    ga.s_count = std::min(ws->s_chunk[f], s_hi - s0);
+    const size_t smem = (size_t)ga.s_count * ws->words * 8 + (2 * ws->words + 1) * 4;
+    switch (sys->nm) {
+      case 1: rc = launch_fill<1>(ga, smem, st); break;
+      case 4: rc = launch_fill<4>(ga, smem, st); break;
+      case 9: rc = launch_fill<9>(ga, smem, st); break;
+      default: rc = launch_fill<16>(ga, smem, st); break;
+    }
+    if (rc) return rc;
+  }
+  return TDB_OK;
+}
+
+// quadrature launches (one per launch family group) of the current pair plan
+static int run_quad(TdbSystem* sys, cudaStream_t st, long long nitems) {
   AsmWorkspace* ws = sys->ws;
   TdbContext* ctx = sys->ctx;
-  cudaStream_t st = ctx->stream;
-  const int p = sys->p, NACC = sys->nacc, NM = sys->nm;
-  int rc;
-  TDB_CUDA_CHECK(cudaEventRecord(ws->ev[0], st));
-  // kernel launches of this run: plan (k_plan_pairs, 2 cub scans x 2, k_fill_items), quad
-  // groups, finalize, per family (count chunks + cub scan x 2 + fill chunks)
-  long long nl = 6 + (long long)ws->launches.size();
-  {
-    bool multi_ = false;
-    for (int c = 0; c < 4; ++c) multi_ |= ws->nitems_case[c] > 1;
-    nl += multi_ ? 1 : 0;
-    for (int f = 0; f < sys->F; ++f) {
-      const int chunks = (sys->fam[f].npos + ws->s_chunk[f] - 1) / ws->s_chunk[f];
-      nl += 2 * chunks + 2;
-    }
-  }
-  ws->launch_count = nl;
-  if ((rc = run_plan(sys, st))) return rc;
-  TDB_CUDA_CHECK(cudaEventRecord(ws->ev[1], st));
+  const int p = sys->p;
+  int rc = TDB_OK;
   int li = 0;
   for (const auto& L : ws->launches) {
     QuadArgs qa;
@@ -1619,7 +1637,7 @@ int tdb_system_run_impl(TdbSystem* sys) {
     qa.a2 = sys->a2;
     for (int c = 0; c < 4; ++c) qa.rules[c] = ws->rules[c];
     qa.items = ws->items;
-    qa.nitems = ws->total_items;
+    qa.nitems = nitems;
     qa.work = ws->counters + 1 + (li % 32);
     qa.frange = ws->frange;
     qa.pair_base = ws->slots;
@@ -1635,7 +1653,13 @@ int tdb_system_run_impl(TdbSystem* sys) {
     if (rc) return rc;
     ++li;
   }
-  TDB_CUDA_CHECK(cudaEventRecord(ws->ev[2], st));
+  return TDB_OK;
+}
+
+// singular pairs: chunk-group partials summed in group order
+static int run_finalize(TdbSystem* sys, cudaStream_t st) {
+  AsmWorkspace* ws = sys->ws;
+  const int NACC = sys->nacc;
   bool multi = false;
   for (int c = 0; c < 4; ++c) multi |= ws->nitems_case[c] > 1;
   if (multi) {
@@ -1643,50 +1667,126 @@ int tdb_system_run_impl(TdbSystem* sys) {
         ws->nmulti, ws->multi, ws->units, ws->pcase, ws->slots, ws->d_nitems_case, NACC, ws->part);
     TDB_CUDA_CHECK(cudaGetLastError());
   }
-  TDB_CUDA_CHECK(cudaEventRecord(ws->ev[3], st));
-  if (!ws->fstreams) {
-    for (int k = 0; k < AsmWorkspace::kFamStreams; ++k) {
-      TDB_CUDA_CHECK(cudaStreamCreateWithFlags(&ws->fstream[k], cudaStreamNonBlocking));
-      TDB_CUDA_CHECK(cudaEventCreateWithFlags(&ws->fevent[k], cudaEventDisableTiming));
-      if (dev_malloc(&ws->fcub[k], ws->cub_bytes) != cudaSuccess) {
-        set_error("pattern streams: cudaMalloc failed");
-        return TDB_E_NOMEM;
-      }
+  return TDB_OK;
+}
+
+// total slots / work items of the current pair plan (exclusive scans + the last pair)
+static int plan_totals(AsmWorkspace* ws, cudaStream_t st, long long* slots, long long* items) {
+  const long long E2 = ws->E2;
+  long long ex_s = 0, ex_i = 0;
+  int rc;
+  if ((rc = read_ll(ws->slots + E2 - 1, &ex_s, st))) return rc;
+  if ((rc = read_ll(ws->nitems + E2 - 1, &ex_i, st))) return rc;
+  int u_last = 0;
+  unsigned char c_last = 0;
+  TDB_CUDA_CHECK(cudaMemcpy(&u_last, ws->units + E2 - 1, sizeof(int), cudaMemcpyDeviceToHost));
+  TDB_CUDA_CHECK(cudaMemcpy(&c_last, ws->pcase + E2 - 1, 1, cudaMemcpyDeviceToHost));
+  const int ni = u_last > 0 ? ws->nitems_case[c_last] : 0;
+  *slots = ex_s + (long long)u_last * ni;
+  *items = ex_i + ni;
+  return TDB_OK;
+}
+
+int tdb_system_run_impl(TdbSystem* sys) {
+  AsmWorkspace* ws = sys->ws;
+  TdbContext* ctx = sys->ctx;
+  cudaStream_t st = ctx->stream;
+  int rc;
+  TDB_CUDA_CHECK(cudaEventRecord(ws->ev[0], st));
+  // kernel launches of this run: plan (k_plan_pairs, 2 cub scans x 2, k_fill_items), quad
+  // groups, finalize, per family (count chunks + cub scan x 2 + fill chunks); per batch
+  // the plan runs twice (counts, then values)
+  const int NB = ws->nbatch;
+  long long nl = (long long)NB * (6 + (long long)ws->launches.size()) + (NB > 1 ? 6LL * NB : 0);
+  {
+    bool multi_ = false;
+    for (int c = 0; c < 4; ++c) multi_ |= ws->nitems_case[c] > 1;
+    nl += multi_ ? NB : 0;
+    for (int f = 0; f < sys->F; ++f) {
+      const int chunks = (sys->fam[f].npos + ws->s_chunk[f] - 1) / ws->s_chunk[f];
+      nl += 2 * chunks + 2 + (NB > 1 ? 2LL * NB : 0);
     }
-    ws->fstreams = true;
   }
-  // families by decreasing position count, dealt round-robin over the streams
-  std::vector<int> forder(sys->F);
-  for (int f = 0; f < sys->F; ++f) forder[f] = f;
-  std::stable_sort(forder.begin(), forder.end(), [&](int x, int y) { return sys->fam[x].npos > sys->fam[y].npos; });
-  for (int k = 0; k < AsmWorkspace::kFamStreams; ++k) TDB_CUDA_CHECK(cudaStreamWaitEvent(ws->fstream[k], ws->ev[3], 0));
-  for (int fi = 0; fi < sys->F; ++fi) {
-    const int f = forder[fi], sk = fi % AsmWorkspace::kFamStreams;
-    cudaStream_t fst = ws->fstream[sk];
-    if ((rc = run_pattern_count(sys, f, fst, ws->fcub[sk]))) return rc;
-    PatternArgs ga = pattern_args(sys, f);
-    for (int s0 = 0; s0 < ga.npos; s0 += ws->s_chunk[f]) {
-      ga.s_begin = s0;
-      ga.s_count = std::min(ws->s_chunk[f], ga.npos - s0);
-      const size_t smem = (size_t)ga.s_count * ws->words * 8 + (2 * ws->words + 1) * 4;
-      switch (NM) {
-        case 1: rc = launch_fill<1>(ga, smem, fst); break;
-        case 4: rc = launch_fill<4>(ga, smem, fst); break;
-        case 9: rc = launch_fill<9>(ga, smem, fst); break;
-        default: rc = launch_fill<16>(ga, smem, fst); break;
-      }
-      if (rc) return rc;
-    }
-  }
-  for (int k = 0; k < AsmWorkspace::kFamStreams; ++k) {
-    TDB_CUDA_CHECK(cudaEventRecord(ws->fevent[k], ws->fstream[k]));
-    TDB_CUDA_CHECK(cudaStreamWaitEvent(st, ws->fevent[k], 0));
-  }
-  TDB_CUDA_CHECK(cudaEventRecord(ws->ev[4], st));
-  TDB_CUDA_CHECK(cudaEventSynchronize(ws->ev[4]));
+  ws->launch_count = nl;
   unsigned long long cnt[64];
-  TDB_CUDA_CHECK(cudaMemcpy(cnt, ws->counters, sizeof(cnt), cudaMemcpyDeviceToHost));
   long long n_geom = 0;
+  if (NB == 1) {
+    if ((rc = run_plan(sys, st))) return rc;
+    TDB_CUDA_CHECK(cudaEventRecord(ws->ev[1], st));
+    if ((rc = run_quad(sys, st, ws->total_items))) return rc;
+    TDB_CUDA_CHECK(cudaEventRecord(ws->ev[2], st));
+    if ((rc = run_finalize(sys, st))) return rc;
+    TDB_CUDA_CHECK(cudaEventRecord(ws->ev[3], st));
+    if (!ws->fstreams) {
+      for (int k = 0; k < AsmWorkspace::kFamStreams; ++k) {
+        TDB_CUDA_CHECK(cudaStreamCreateWithFlags(&ws->fstream[k], cudaStreamNonBlocking));
+        TDB_CUDA_CHECK(cudaEventCreateWithFlags(&ws->fevent[k], cudaEventDisableTiming));
+        if (dev_malloc(&ws->fcub[k], ws->cub_bytes) != cudaSuccess) {
+          set_error("pattern streams: cudaMalloc failed");
+          return TDB_E_NOMEM;
+        }
+      }
+      ws->fstreams = true;
+    }
+    // families by decreasing position count, dealt round-robin over the streams
+    std::vector<int> forder(sys->F);
+    for (int f = 0; f < sys->F; ++f) forder[f] = f;
+    std::stable_sort(forder.begin(), forder.end(), [&](int x, int y) { return sys->fam[x].npos > sys->fam[y].npos; });
+    for (int k = 0; k < AsmWorkspace::kFamStreams; ++k) TDB_CUDA_CHECK(cudaStreamWaitEvent(ws->fstream[k], ws->ev[3], 0));
+    for (int fi = 0; fi < sys->F; ++fi) {
+      const int f = forder[fi], sk = fi % AsmWorkspace::kFamStreams;
+      cudaStream_t fst = ws->fstream[sk];
+      if ((rc = run_pattern_count(sys, f, fst, ws->fcub[sk]))) return rc;
+      if ((rc = run_pattern_fill(sys, f, fst))) return rc;
+    }
+    for (int k = 0; k < AsmWorkspace::kFamStreams; ++k) {
+      TDB_CUDA_CHECK(cudaEventRecord(ws->fevent[k], ws->fstream[k]));
+      TDB_CUDA_CHECK(cudaStreamWaitEvent(st, ws->fevent[k], 0));
+    }
+    TDB_CUDA_CHECK(cudaEventRecord(ws->ev[4], st));
+    TDB_CUDA_CHECK(cudaEventSynchronize(ws->ev[4]));
+    TDB_CUDA_CHECK(cudaMemcpy(cnt, ws->counters, sizeof(cnt), cudaMemcpyDeviceToHost));
+    sys->stats.ms_plan = elapsed(ws->ev[0], ws->ev[1]);
+    sys->stats.ms_quad = elapsed(ws->ev[1], ws->ev[2]);
+    sys->stats.ms_finalize = elapsed(ws->ev[2], ws->ev[3]);
+    sys->stats.ms_pattern = elapsed(ws->ev[3], ws->ev[4]);
+  } else {
+    // position batches: (1) every batch's plan -> its positions' CSR row counts; one scan
+    // per family; (2) per batch: plan -> quadrature -> finalize -> the positions' fill
+    for (int b = 0; b < NB; ++b) {
+      if ((rc = run_plan(sys, st, b))) return rc;
+      for (int f = 0; f < sys->F; ++f)
+        if ((rc = run_pattern_count(sys, f, st, nullptr, ws->wlo[b][f], ws->whi[b][f], false))) return rc;
+    }
+    for (int f = 0; f < sys->F; ++f)
+      if ((rc = run_pattern_count(sys, f, st, nullptr, 0, 0, true))) return rc;
+    TDB_CUDA_CHECK(cudaEventRecord(ws->ev[1], st));
+    std::memset(cnt, 0, sizeof(cnt));
+    float ms_quad = 0.f;
+    for (int b = 0; b < NB; ++b) {
+      if ((rc = run_plan(sys, st, b))) return rc;
+      long long bs = 0, bi = 0;
+      if ((rc = plan_totals(ws, st, &bs, &bi))) return rc;
+      TDB_CUDA_CHECK(cudaEventRecord(ws->ev[2], st));
+      if ((rc = run_quad(sys, st, bi))) return rc;
+      TDB_CUDA_CHECK(cudaEventRecord(ws->ev[3], st));
+      if ((rc = run_finalize(sys, st))) return rc;
+      for (int f = 0; f < sys->F; ++f)
+        if ((rc = run_pattern_fill(sys, f, st, ws->wlo[b][f], ws->whi[b][f]))) return rc;
+      unsigned long long c[64];
+      TDB_CUDA_CHECK(cudaMemcpyAsync(c, ws->counters, sizeof(c), cudaMemcpyDeviceToHost, st));
+      TDB_CUDA_CHECK(cudaStreamSynchronize(st));
+      ms_quad += elapsed(ws->ev[2], ws->ev[3]);
+      cnt[0] += c[0];
+      for (int k = 40; k < 49; ++k) cnt[k] += c[k];
+    }
+    TDB_CUDA_CHECK(cudaEventRecord(ws->ev[4], st));
+    TDB_CUDA_CHECK(cudaEventSynchronize(ws->ev[4]));
+    sys->stats.ms_plan = elapsed(ws->ev[0], ws->ev[1]);  // batch plans + pattern counts
+    sys->stats.ms_quad = ms_quad;
+    sys->stats.ms_finalize = 0.0;
+    sys->stats.ms_pattern = elapsed(ws->ev[1], ws->ev[4]) - ms_quad;
+  }
   for (int c = 0; c < 4; ++c) {
     n_geom += (long long)cnt[40 + c] * ws->rules[c].nq;
     sys->stats.pairs_case[c] = (int64_t)cnt[40 + c];
@@ -1696,10 +1796,6 @@ int tdb_system_run_impl(TdbSystem* sys) {
   sys->stats.launches = ws->launch_count;
   sys->stats.n_in = (int64_t)cnt[0];
   sys->stats.n_geom = n_geom;
-  sys->stats.ms_plan = elapsed(ws->ev[0], ws->ev[1]);
-  sys->stats.ms_quad = elapsed(ws->ev[1], ws->ev[2]);
-  sys->stats.ms_finalize = elapsed(ws->ev[2], ws->ev[3]);
-  sys->stats.ms_pattern = elapsed(ws->ev[3], ws->ev[4]);
   sys->stats.ms_total = elapsed(ws->ev[0], ws->ev[4]);
   return TDB_OK;
 }
@@ -2262,27 +2358,14 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
     ws->cub_bytes = std::max(b1, b2) + 256;
     if ((rc = dalloc(reinterpret_cast<char**>(&ws->cub_tmp), ws->cub_bytes))) return rc;
   }
-  // sizing pass: run the plan once and read the totals
+  // sizing pass: the plan over every position once; totals, singular pair list, units
+  ws->nbatch = 1;
+  ws->wlo.assign(1, std::vector<int>(F, 0));
+  ws->whi.assign(1, std::vector<int>(F, 0));
+  for (int f = 0; f < F; ++f) ws->whi[0][f] = sys->fam[f].npos;
   if ((rc = run_plan(sys, st))) return rc;
-  {
-    long long last_s = 0, last_i = 0;
-    // slots/nitems are exclusive scans now; totals = last exclusive + last raw (recomputed)
-    long long ex_s = 0, ex_i = 0;
-    if ((rc = read_ll(ws->slots + E2 - 1, &ex_s, st))) return rc;
-    if ((rc = read_ll(ws->nitems + E2 - 1, &ex_i, st))) return rc;
-    int u_last = 0;
-    unsigned char c_last = 0;
-    TDB_CUDA_CHECK(cudaMemcpy(&u_last, ws->units + E2 - 1, sizeof(int), cudaMemcpyDeviceToHost));
-    TDB_CUDA_CHECK(cudaMemcpy(&c_last, ws->pcase + E2 - 1, 1, cudaMemcpyDeviceToHost));
-    const int ni = u_last > 0 ? ws->nitems_case[c_last] : 0;
-    last_s = (long long)u_last * ni;
-    last_i = ni;
-    ws->total_slots = ex_s + last_s;
-    ws->total_items = ex_i + last_i;
-  }
-  if ((rc = dalloc(&ws->items, ws->total_items))) return rc;
-  if ((rc = dalloc(&ws->part, (size_t)ws->total_slots * NACC))) return rc;
-  {  // pairs the singular-group finalize has to visit
+  if ((rc = plan_totals(ws, st, &ws->total_slots, &ws->total_items))) return rc;
+  {  // pairs the singular-group finalize has to visit (a superset for every position batch)
     const long long cap = std::max<long long>(1, (long long)ws->Et * 64);
     if ((rc = dalloc(&ws->multi, cap))) return rc;
     unsigned long long* d_cnt = reinterpret_cast<unsigned long long*>(ws->counters) + 63;
@@ -2297,21 +2380,6 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
     }
     ws->nmulti = nm_;
   }
-  // pattern sizing: counts -> scan -> nnz
-  long long nnz_total = 0;
-  for (int f = 0; f < F; ++f) {
-    FamilyStore& fs = sys->fam[f];
-    const long long nrows = (long long)fs.npos * ws->nrows;
-    if ((rc = dalloc(&fs.indptr, nrows + 1))) return rc;
-    if ((rc = run_pattern_count(sys, f, st))) return rc;
-    long long nnz = 0;
-    if ((rc = read_ll(reinterpret_cast<long long*>(fs.indptr) + nrows, &nnz, st))) return rc;
-    fs.nnz = nnz;
-    nnz_total += nnz;
-    if ((rc = dalloc(&fs.indices, nnz))) return rc;
-    if ((rc = dalloc(&fs.data, (size_t)nnz * sys->nm))) return rc;
-  }
-  // units: one reduction
   long long units = 0;
   {
     size_t tb = 0;
@@ -2321,6 +2389,75 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
     long long* d_sum = reinterpret_cast<long long*>(static_cast<char*>(tmp.p) + ((tb + 7) / 8) * 8);
     TDB_CUDA_CHECK(cub::DeviceReduce::Sum(tmp.p, tb, ws->units, d_sum, (int64_t)E2, st));
     if ((rc = read_ll(d_sum, &units, st))) return rc;
+  }
+  // Position batches bound the partial buffer (10 (p+1)^2 doubles per unit and chunk
+  // group): TDB_PARTIAL_GB (default: half of the free device memory) caps it; each
+  // family's positions are cut into nbatch contiguous lag ranges (a pair's admissible
+  // lags are contiguous, so most pairs fall in one batch and few recompute geometry).
+  {
+    size_t freeb = 0, totb = 0;
+    cudaMemGetInfo(&freeb, &totb);
+    const char* e = std::getenv("TDB_PARTIAL_GB");
+    const double budget = e ? std::atof(e) * 1e9 : 0.5 * (double)freeb;
+    const double need = (double)ws->total_slots * NACC * sizeof(double);
+    int nb = need > budget && budget > 0 ? (int)std::ceil(need / budget) : 1;
+    int maxpos = 1;
+    for (int f = 0; f < F; ++f) maxpos = std::max(maxpos, sys->fam[f].npos);
+    nb = std::max(1, std::min(nb, maxpos));
+    if (nb > 1) {
+      ws->nbatch = nb;
+      ws->wlo.assign(nb, std::vector<int>(F, 0));
+      ws->whi.assign(nb, std::vector<int>(F, 0));
+      for (int b = 0; b < nb; ++b)
+        for (int f = 0; f < F; ++f) {
+          const int n = sys->fam[f].npos;
+          ws->wlo[b][f] = (int)((long long)n * b / nb);
+          ws->whi[b][f] = (int)((long long)n * (b + 1) / nb);
+        }
+      long long ms = 0, mi = 0;
+      for (int b = 0; b < nb; ++b) {
+        long long bs = 0, bi = 0;
+        if ((rc = run_plan(sys, st, b))) return rc;
+        if ((rc = plan_totals(ws, st, &bs, &bi))) return rc;
+        ms = std::max(ms, bs);
+        mi = std::max(mi, bi);
+      }
+      ws->total_slots = ms;
+      ws->total_items = mi;
+      if (verbose)
+        std::fprintf(stderr, "tdb: %d position batches, partials %.2f GB (all positions %.2f GB)\n", nb,
+                     (double)ms * NACC * 8 / 1e9, need / 1e9);
+    }
+  }
+  if ((rc = dalloc(&ws->items, ws->total_items))) return rc;
+  if ((rc = dalloc(&ws->part, (size_t)ws->total_slots * NACC))) return rc;
+  // pattern sizing: counts -> scan -> nnz
+  long long nnz_total = 0;
+  for (int f = 0; f < F; ++f) {
+    FamilyStore& fs = sys->fam[f];
+    const long long nrows = (long long)fs.npos * ws->nrows;
+    if ((rc = dalloc(&fs.indptr, nrows + 1))) return rc;
+  }
+  if (ws->nbatch > 1)
+    for (int b = 0; b < ws->nbatch; ++b) {
+      if ((rc = run_plan(sys, st, b))) return rc;
+      for (int f = 0; f < F; ++f)
+        if ((rc = run_pattern_count(sys, f, st, nullptr, ws->wlo[b][f], ws->whi[b][f], false))) return rc;
+    }
+  for (int f = 0; f < F; ++f) {
+    FamilyStore& fs = sys->fam[f];
+    const long long nrows = (long long)fs.npos * ws->nrows;
+    if (ws->nbatch > 1) {
+      if ((rc = run_pattern_count(sys, f, st, nullptr, 0, 0, true))) return rc;
+    } else if ((rc = run_pattern_count(sys, f, st))) {
+      return rc;
+    }
+    long long nnz = 0;
+    if ((rc = read_ll(reinterpret_cast<long long*>(fs.indptr) + nrows, &nnz, st))) return rc;
+    fs.nnz = nnz;
+    nnz_total += nnz;
+    if ((rc = dalloc(&fs.indices, nnz))) return rc;
+    if ((rc = dalloc(&fs.data, (size_t)nnz * sys->nm))) return rc;
   }
   sys->stats.units = units;
   sys->stats.items = ws->total_items;
@@ -2366,9 +2503,12 @@ int tdb_position_units_impl(TdbSystem* sys, int f, int64_t* out) {
   if (rc) return rc;
   TDB_CUDA_CHECK(cudaMemsetAsync(d.p, 0, (npos + 1) * sizeof(unsigned long long), st));
   const int blocks = (int)std::min<long long>((ws->E2 + 255) / 256, 148LL * 8);
-  k_position_units<<<blocks, 256, (npos + 1) * sizeof(int), st>>>(ws->frange + (long long)f * ws->E2, ws->E2,
-                                                                    npos, d.as<unsigned long long>());
-  TDB_CUDA_CHECK(cudaGetLastError());
+  for (int b = 0; b < ws->nbatch; ++b) {  // position batches: each plan covers its window only
+    if (ws->nbatch > 1 && (rc = run_plan(sys, st, b))) return rc;
+    k_position_units<<<blocks, 256, (npos + 1) * sizeof(int), st>>>(ws->frange + (long long)f * ws->E2, ws->E2,
+                                                                      npos, d.as<unsigned long long>());
+    TDB_CUDA_CHECK(cudaGetLastError());
+  }
   std::vector<unsigned long long> h(npos + 1);
   TDB_CUDA_CHECK(cudaMemcpyAsync(h.data(), d.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   TDB_CUDA_CHECK(cudaStreamSynchronize(st));

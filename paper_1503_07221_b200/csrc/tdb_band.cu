@@ -108,6 +108,32 @@ __global__ void k_band_rbptr(const int* __restrict__ tile_rb, long long ntiles, 
   }
 }
 
+// per-plan view: the records whose 4-lag window meets the plan's active positions
+__global__ void k_band_flag(const BandTile* __restrict__ tiles, long long n, const unsigned* __restrict__ act,
+                            int* __restrict__ flag) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    const int s0 = tiles[t].s0, w = s0 >> 5, b = s0 & 31;
+    const unsigned long long v = ((unsigned long long)act[w + 1] << 32) | act[w];
+    flag[t] = ((v >> b) & 0xFull) != 0ull;
+  }
+}
+
+__global__ void k_band_scatter(const BandTile* __restrict__ tiles, long long n, const int* __restrict__ flag,
+                               const long long* __restrict__ pos, BandTile* __restrict__ out) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+    if (flag[t]) out[pos[t]] = tiles[t];
+}
+
+__global__ void k_band_rbview(const int64_t* __restrict__ rbptr, int nRB, const long long* __restrict__ pos,
+                              int64_t* __restrict__ out) {
+  for (int J = blockIdx.x * blockDim.x + threadIdx.x; J <= nRB; J += gridDim.x * blockDim.x) out[J] = pos[rbptr[J]];
+}
+
+__global__ void k_flag_to_ll(const int* __restrict__ f, long long n, long long* __restrict__ o) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t <= n; t += (long long)gridDim.x * blockDim.x)
+    o[t] = t < n ? f[t] : 0;
+}
+
 struct MaxLL {
   __device__ __forceinline__ long long operator()(long long a, long long b) const { return a > b ? a : b; }
 };
@@ -166,8 +192,10 @@ __global__ void __launch_bounds__(kBandMaxWarps * 32) k_band_mv(BandMvArgs a) {
   unsigned long long* full = reinterpret_cast<unsigned long long*>(stg + kBandStages * kBandChunk);
   unsigned long long* empty = full + kBandStages;
   unsigned* act = reinterpret_cast<unsigned*>(empty + kBandStages);  // [act_words + 1]
+  unsigned* irr = act + a.act_words + 1;                              // [kIrrWords]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   for (int i = tid; i <= a.act_words; i += blockDim.x) act[i] = i < a.act_words ? __ldg(a.s_act + i) : 0u;
+  for (int i = tid; i < kIrrWords; i += blockDim.x) irr[i] = a.irr_mask[i];
   const int J = blockIdx.x / a.P, part = blockIdx.x % a.P;
   const long long r0 = __ldg(a.rbptr + J), r1 = __ldg(a.rbptr + J + 1);
   const long long q0 = r0 + (r1 - r0) * part / a.P, q1 = r0 + (r1 - r0) * (part + 1) / a.P;
@@ -194,42 +222,73 @@ __global__ void __launch_bounds__(kBandMaxWarps * 32) k_band_mv(BandMvArgs a) {
 #pragma unroll
   for (int u = 0; u < TT; ++u) acc[u][0] = acc[u][1] = 0.0;
   const double* xl = a.xt + (a.off0 - k + g + 8 * t0);
+  // one pair of tile records: header, A fragments (masked by the plan's lags), B windows
+  struct PairRegs {
+    unsigned c1, c2;
+    int lo1, hi1, lo2, hi2;
+    double av1, av2;
+    double b1[TT], b2[TT];
+  };
+  auto load_pair = [&](const BandTile* T, int i, int n, PairRegs& R) {
+    const bool two = i + 1 < n;
+    const int l1 = T[i].l, s1 = T[i].s0;
+    const int l2 = two ? T[i + 1].l : l1, s2 = two ? T[i + 1].s0 : s1;
+    R.c1 = act4(act, s1);
+    R.c2 = two ? act4(act, s2) : 0u;
+    // time tiles t holding a valid row kt = ktlo + 8 t + n (itlo <= kt - d <= ithi for a lag
+    // d of the window): ceil((dt0 + s0 - 7) / 8) <= t <= floor((dt1 + s0 + 3) / 8)
+    R.lo1 = (a.dt0 + s1 + 8 * 1024) / 8 - 1024 - t0;
+    R.hi1 = R.c1 ? min(a.nT - 1, (a.dt1 + s1 + 3 + 8 * 1024) / 8 - 1024) - t0 : -1;
+    R.lo2 = (a.dt0 + s2 + 8 * 1024) / 8 - 1024 - t0;
+    R.hi2 = R.c2 ? min(a.nT - 1, (a.dt1 + s2 + 3 + 8 * 1024) / 8 - 1024) - t0 : -1;
+    R.av1 = ((R.c1 >> k) & 1u) ? T[i].v[lane] : 0.0;
+    R.av2 = ((R.c2 >> k) & 1u) ? T[i + (two ? 1 : 0)].v[lane] : 0.0;
+    const double* x1 = xl + (long long)l1 * a.xs - s1;
+    const double* x2 = xl + (long long)l2 * a.xs - s2;
+#pragma unroll
+    for (int u = 0; u < TT; ++u) {
+      R.b1[u] = __ldg(x1 + 8 * u);
+      R.b2[u] = __ldg(x2 + 8 * u);
+    }
+    // the light-cone tie lag: only the block rows of its logical mask (per lane / row)
+    if (a.s_irr >= s1 && a.s_irr < s1 + 4 && k == a.s_irr - s1) {
+#pragma unroll
+      for (int u = 0; u < TT; ++u) {
+        const int r = 8 * (t0 + u) + g;
+        if (!((irr[r >> 5] >> (r & 31)) & 1u)) R.b1[u] = 0.0;
+      }
+    }
+    if (a.s_irr >= s2 && a.s_irr < s2 + 4 && k == a.s_irr - s2) {
+#pragma unroll
+      for (int u = 0; u < TT; ++u) {
+        const int r = 8 * (t0 + u) + g;
+        if (!((irr[r >> 5] >> (r & 31)) & 1u)) R.b2[u] = 0.0;
+      }
+    }
+  };
+  auto mma_pair = [&](const PairRegs& R) {
+#pragma unroll
+    for (int u = 0; u < TT; ++u)
+      if (u >= R.lo1 && u <= R.hi1) dmma884(acc[u][0], acc[u][1], R.av1, R.b1[u]);
+#pragma unroll
+    for (int u = 0; u < TT; ++u)
+      if (u >= R.lo2 && u <= R.hi2) dmma884(acc[u][0], acc[u][1], R.av2, R.b2[u]);
+  };
   for (int c = 0; c < nchunks; ++c) {
     const int st = c % kBandStages;
     const unsigned ph = (unsigned)(c / kBandStages) & 1u;
     mbar_wait(&full[st], ph);
     const BandTile* T = stg + st * kBandChunk;
     const int n = (int)min((long long)kBandChunk, q1 - (q0 + (long long)c * kBandChunk));
-    for (int i = 0; i < n; i += 2) {
-      const bool two = i + 1 < n;
-      const int l1 = T[i].l, s1 = T[i].s0;
-      const int l2 = two ? T[i + 1].l : l1, s2 = two ? T[i + 1].s0 : s1;
-      const unsigned c1 = act4(act, s1), c2 = two ? act4(act, s2) : 0u;
-      if ((c1 | c2) == 0u) continue;  // warp-uniform: no lag of either tile in this plan
-      // time tiles t holding a valid row kt = ktlo + 8 t + n (itlo <= kt - d <= ithi for a lag
-      // d of the window): ceil((dt0 + s0 - 7) / 8) <= t <= floor((dt1 + s0 + 3) / 8)
-      const int lo1 = (a.dt0 + s1 + 8 * 1024) / 8 - 1024, hi1 = (a.dt1 + s1 + 3 + 8 * 1024) / 8 - 1024;
-      const int lo2 = (a.dt0 + s2 + 8 * 1024) / 8 - 1024, hi2 = (a.dt1 + s2 + 3 + 8 * 1024) / 8 - 1024;
-      double av1 = T[i].v[lane];
-      double av2 = two ? T[i + 1].v[lane] : 0.0;
-      if (!((c1 >> k) & 1u)) av1 = 0.0;
-      if (!((c2 >> k) & 1u)) av2 = 0.0;
-      const double* x1 = xl + (long long)l1 * a.xs - s1;
-      const double* x2 = xl + (long long)l2 * a.xs - s2;
-      double b1[TT], b2[TT];
-#pragma unroll
-      for (int u = 0; u < TT; ++u) {
-        b1[u] = __ldg(x1 + 8 * u);
-        b2[u] = __ldg(x2 + 8 * u);
-      }
-      const int u1a = lo1 - t0, u1b = c1 != 0u ? hi1 - t0 : -1;
-      const int u2a = lo2 - t0, u2b = c2 != 0u ? hi2 - t0 : -1;
-#pragma unroll
-      for (int u = 0; u < TT; ++u)
-        if (u >= u1a && u <= u1b) dmma884(acc[u][0], acc[u][1], av1, b1[u]);
-#pragma unroll
-      for (int u = 0; u < TT; ++u)
-        if (u >= u2a && u <= u2b) dmma884(acc[u][0], acc[u][1], av2, b2[u]);
+    // software pipeline: the next pair's loads are in flight during this pair's DMMAs
+    PairRegs RA, RB;
+    load_pair(T, 0, n, RA);
+    for (int i = 0; i < n; i += 4) {
+      if (i + 2 < n) load_pair(T, i + 2, n, RB);
+      mma_pair(RA);
+      if (i + 2 >= n) break;
+      if (i + 4 < n) load_pair(T, i + 4, n, RA);
+      mma_pair(RB);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
@@ -264,7 +323,7 @@ __global__ void k_band_reduce(BandMvArgs a) {
 
 size_t band_smem_bytes(int act_words) {
   return (size_t)kBandStages * kBandChunk * sizeof(BandTile) + 2 * kBandStages * sizeof(unsigned long long) +
-         (size_t)(act_words + 1) * sizeof(unsigned);
+         (size_t)(act_words + 1 + kIrrWords) * sizeof(unsigned);
 }
 
 template <int TT>
@@ -375,6 +434,79 @@ int band_build(TdbSystem* sys, int f) {
   release();
 #undef TRY
   b.built = true;
+  return TDB_OK;
+}
+
+// Records of family f restricted to the active positions `act` (bit s set: position s is
+// a band term), order kept; cached per active set (the recursive preconditioner reuses a
+// handful of ranges).  A quarter-range plan then streams only its lags' records.
+int band_view(TdbSystem* sys, int f, const std::vector<unsigned>& act, const BandTile** tiles,
+              const int64_t** rbptr) {
+  BandStore& b = sys->band[f];
+  for (const BandView& v : b.views)
+    if (v.act == act) {
+      *tiles = v.tiles;
+      *rbptr = v.rbptr;
+      return TDB_OK;
+    }
+  cudaStream_t st = sys->ctx->stream;
+  const long long n = b.ntiles;
+  const int nRB = sys->nRB;
+  BandView v;
+  v.act = act;
+  int* flag = nullptr;
+  long long* pos = nullptr;
+  unsigned* dact = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  auto release = [&]() {
+    dev_free(flag);
+    dev_free(pos);
+    dev_free(dact);
+    dev_free(tmp);
+  };
+#define TRY(expr)                                                            \
+  do {                                                                       \
+    cudaError_t e_ = (expr);                                                 \
+    if (e_ != cudaSuccess) {                                                 \
+      release();                                                             \
+      dev_free(v.tiles);                                                     \
+      dev_free(v.rbptr);                                                     \
+      set_error(std::string("band view: ") + cudaGetErrorString(e_));        \
+      return e_ == cudaErrorMemoryAllocation ? TDB_E_NOMEM : TDB_E_CUDA;     \
+    }                                                                        \
+  } while (0)
+  TRY(dev_malloc((void**)&flag, (size_t)std::max(1LL, n) * sizeof(int)));
+  TRY(dev_malloc((void**)&pos, (size_t)(n + 1) * sizeof(long long)));
+  TRY(dev_malloc((void**)&dact, act.size() * sizeof(unsigned)));
+  TRY(cudaMemcpyAsync(dact, act.data(), act.size() * sizeof(unsigned), cudaMemcpyHostToDevice, st));
+  if (n > 0) {
+    k_band_flag<<<148 * 8, 256, 0, st>>>(b.tiles, n, dact, flag);
+    TRY(cudaGetLastError());
+  }
+  k_flag_to_ll<<<148 * 8, 256, 0, st>>>(flag, n, pos);
+  TRY(cudaGetLastError());
+  TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, pos, pos, n + 1, st));
+  TRY(dev_malloc(&tmp, tb));
+  TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, pos, pos, n + 1, st));
+  long long nsel = 0;
+  TRY(cudaMemcpyAsync(&nsel, pos + n, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  TRY(cudaStreamSynchronize(st));
+  TRY(dev_malloc((void**)&v.tiles, (size_t)std::max(1LL, nsel) * sizeof(BandTile)));
+  TRY(dev_malloc((void**)&v.rbptr, (size_t)(nRB + 1) * sizeof(int64_t)));
+  if (n > 0) {
+    k_band_scatter<<<148 * 8, 256, 0, st>>>(b.tiles, n, flag, pos, v.tiles);
+    TRY(cudaGetLastError());
+  }
+  k_band_rbview<<<(nRB + 256) / 256, 256, 0, st>>>(b.rbptr, nRB, pos, v.rbptr);
+  TRY(cudaGetLastError());
+  TRY(cudaStreamSynchronize(st));
+  release();
+#undef TRY
+  v.ntiles = nsel;
+  b.views.push_back(v);
+  *tiles = v.tiles;
+  *rbptr = v.rbptr;
   return TDB_OK;
 }
 

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "tdb_internal.h"
 
 namespace tdb {
@@ -11,6 +13,7 @@ namespace tdb {
 constexpr int kBandMaxWarps = 8;  // time-group warps per CTA
 constexpr int kBandChunk = 32;    // tile records per bulk-copy stage
 constexpr int kBandStages = 3;    // stages of the shared-memory ring
+constexpr int kIrrWords = 13;     // block-row bits of the irregular (tie) lag: 8 x 6 x 8 tiles max
 
 struct BandMvArgs {
   int nRB, P, nT, TT, W;  // row blocks, parts per row block, 8-step time tiles, tiles per warp, warps per CTA
@@ -23,6 +26,9 @@ struct BandMvArgs {
   const BandTile* tiles;
   const int64_t* rbptr;
   const unsigned* s_act;  // (act_words,) bit s: position s is a band term of this plan
+  int s_irr;              // position whose logical mask is a strict subset of the band rows
+                          // (the light-cone tie lag), -1 if none
+  unsigned irr_mask[kIrrWords];  // its valid block rows: bit r <-> kt = ktlo + r
   const int* rperm;       // Morton row -> local row
   const double* xt;       // [V][xs] vertex-major x of the plan's inner columns, zero pads
   double* ypart;          // [P][nRB * 8][ldy]
@@ -30,6 +36,8 @@ struct BandMvArgs {
 };
 
 int band_build(TdbSystem* sys, int f);
+int band_view(TdbSystem* sys, int f, const std::vector<unsigned>& act, const BandTile** tiles,
+              const int64_t** rbptr);
 int band_mv_tiles(const BandMvArgs& a, cudaStream_t st);   // tile kernel -> ypart
 size_t band_smem_bytes(int act_words);
 int band_mv_reduce(const BandMvArgs& a, cudaStream_t st);  // y += sum of parts (ordered)

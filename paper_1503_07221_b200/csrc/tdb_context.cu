@@ -188,6 +188,10 @@ int tdb_system_destroy(TdbSystem* sys) {
   for (auto& b : sys->band) {
     dev_free(b.tiles);
     dev_free(b.rbptr);
+    for (auto& v : b.views) {
+      dev_free(v.tiles);
+      dev_free(v.rbptr);
+    }
   }
   dev_free(sys->d_vperm);
   dev_free(sys->d_vinv);

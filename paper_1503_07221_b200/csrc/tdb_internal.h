@@ -58,12 +58,21 @@ struct __align__(16) BandTile {
   int32_t l, s0, pad0, pad1;
 };
 
+// The records of a BandStore whose lag window meets a set of active positions.
+struct BandView {
+  std::vector<unsigned> act;  // active-position bit set (key)
+  long long ntiles = 0;
+  BandTile* tiles = nullptr;
+  int64_t* rbptr = nullptr;
+};
+
 // One family's stored blocks as lag-band tiles, sorted (J, l, s0).
 struct BandStore {
   bool built = false, failed = false;
   long long ntiles = 0, nnz = 0;
   BandTile* tiles = nullptr;  // (ntiles,)
   int64_t* rbptr = nullptr;   // (nRB + 1,)
+  std::vector<BandView> views;  // per-plan restrictions (tdb_band.cu band_view)
 };
 
 struct FamilyStore {

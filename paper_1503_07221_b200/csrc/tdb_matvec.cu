@@ -393,6 +393,68 @@ static void launch_mv_nc(const MvArgs& a, int nchunks, int blocks, cudaStream_t 
   k_matvec<NP1, NC><<<blocks, 32, smem, st>>>(a);
 }
 
+// ---- single-term SpMV (p = 0): the boundary blocks of a band plan --------------
+// Plans whose lag terms all go to the band tiles keep only "single" CSR terms:
+// boundary-family blocks each applied at <= kSpmvMaxKt block rows (first block
+// column, last block row, singletons).  One warp per output row (kt, j): it walks
+// that row's single items in plan order, lanes over the CSR entries (4 entries
+// per lane in flight, coalesced 4/8-byte streams), x read from the time-major
+// iterate (one block column = M doubles, L1/L2 resident), a fixed xor-butterfly
+// reduction, and ONE plain store y[kt][j] = sum (rows without items get 0; the
+// band partials are added afterwards by k_band_reduce).  Deterministic.
+struct SpmvItem {
+  int64_t rowptr;  // offset of the item's (position, row 0) in its family's indptr
+  int fam, col;    // family, block column of x relative to the plan's clo
+};
+
+struct SpmvArgs {
+  int nrows, nkt;                     // owned rows, output block rows of the plan
+  const int* kt_ptr;                  // (nkt + 1,) items of output row kt
+  const SpmvItem* items;
+  const FamCsr* fam;
+  const double* x;
+  const long long* xmap;              // NULL: x[c * M + l]
+  long long xstride;
+  int M;
+  double* y;                          // y[kt_local * nrows + j]
+};
+
+__global__ void __launch_bounds__(256) k_spmv_single(SpmvArgs a) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (warp >= (long long)a.nkt * a.nrows) return;
+  const int kt = (int)(warp / a.nrows), j = (int)(warp % a.nrows);
+  double sum = 0.0;
+  for (int it = a.kt_ptr[kt]; it < a.kt_ptr[kt + 1]; ++it) {
+    const SpmvItem m = a.items[it];
+    const FamCsr F = a.fam[m.fam];
+    const int64_t e0 = __ldg(F.indptr + m.rowptr + j), e1 = __ldg(F.indptr + m.rowptr + j + 1);
+    const double* xc = a.x + (long long)m.col * a.xstride;
+    double acc = 0.0;
+    int64_t e = e0 + lane;
+    for (; e + 96 < e1; e += 128) {
+      const int l0 = __ldg(F.indices + e), l1 = __ldg(F.indices + e + 32), l2 = __ldg(F.indices + e + 64),
+                l3 = __ldg(F.indices + e + 96);
+      const double v0 = __ldg(F.data + e), v1 = __ldg(F.data + e + 32), v2 = __ldg(F.data + e + 64),
+                   v3 = __ldg(F.data + e + 96);
+      const double x0 = __ldg(xc + (a.xmap ? a.xmap[l0] : l0)), x1 = __ldg(xc + (a.xmap ? a.xmap[l1] : l1));
+      const double x2 = __ldg(xc + (a.xmap ? a.xmap[l2] : l2)), x3 = __ldg(xc + (a.xmap ? a.xmap[l3] : l3));
+      acc = fma(v0, x0, acc);
+      acc = fma(v1, x1, acc);
+      acc = fma(v2, x2, acc);
+      acc = fma(v3, x3, acc);
+    }
+    for (; e < e1; e += 32) {
+      const int l0 = __ldg(F.indices + e);
+      acc = fma(__ldg(F.data + e), __ldg(xc + (a.xmap ? a.xmap[l0] : l0)), acc);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    sum += acc;
+  }
+  if (lane == 0) a.y[(long long)kt * a.nrows + j] = sum;
+}
+
 }  // namespace tdb
 
 using namespace tdb;
@@ -421,6 +483,12 @@ struct TdbMatvecPlan {
   unsigned* d_sact = nullptr;
   double* d_bxt = nullptr;
   double* d_bypart = nullptr;
+  // single-term SpMV replacing the CSR kernel when every non-band term is a single term
+  bool spmv = false;
+  SpmvArgs sargs{};
+  int* d_ktptr = nullptr;
+  SpmvItem* d_items = nullptr;
+  FamCsr* d_sfam = nullptr;
 };
 
 extern "C" int tdb_matvec_plan_destroy(TdbMatvecPlan* p) {
@@ -432,6 +500,9 @@ extern "C" int tdb_matvec_plan_destroy(TdbMatvecPlan* p) {
   dev_free(p->d_sact);
   dev_free(p->d_bxt);
   dev_free(p->d_bypart);
+  dev_free(p->d_ktptr);
+  dev_free(p->d_items);
+  dev_free(p->d_sfam);
   dev_free(p->d_fam);
   dev_free(p->d_tcsr);
   dev_free(p->d_ints);
@@ -636,19 +707,30 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   std::vector<int> term_of(npos, -1);
   std::vector<char> to_tile(nt, 0);
   double useful = 0.0;
+  int s_irr = -1;
+  std::vector<unsigned> irr_bits(kIrrWords, 0u);
   for (int t = 0; t < nt; ++t) {
     if (d->term_family[t] != tf || term_of[d->term_pos[t]] >= 0) continue;
-    // regular: the logical mask is exactly {kt in band rows : kt - d in band columns}
+    // regular: the logical mask is exactly {kt in band rows : kt - d in band columns};
+    // one term whose mask is a strict subset of that (the light-cone tie lag, whose
+    // zero test is decided per logical position) rides along with a row mask
     const unsigned* mk = d->term_mask + (long long)t * d->words;
-    bool regular = true;
+    bool regular = true, subset = true;
     int n = 0;
-    for (int kt = 1; kt <= N && regular; ++kt) {
+    for (int kt = 1; kt <= N; ++kt) {
       const bool want = kt >= ktlo && kt <= kthi && kt - d->term_d[t] >= itlo && kt - d->term_d[t] <= ithi;
       const bool have = (mk[(kt - 1) >> 5] >> ((kt - 1) & 31)) & 1u;
-      regular = want == have;
+      regular &= want == have;
+      subset &= want || !have;
       n += have;
     }
-    if (!regular || n == 0) continue;
+    if (n == 0 || !subset) continue;
+    if (!regular) {
+      if (s_irr >= 0 || kthi - ktlo + 1 > 32 * kIrrWords) continue;
+      s_irr = d->term_pos[t];
+      for (int kt = ktlo; kt <= kthi; ++kt)
+        if ((mk[(kt - 1) >> 5] >> ((kt - 1) & 31)) & 1u) irr_bits[(kt - ktlo) >> 5] |= 1u << ((kt - ktlo) & 31);
+    }
     term_of[d->term_pos[t]] = t;
     to_tile[t] = 1;
     useful += n;
@@ -684,6 +766,51 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   TdbMatvecPlan* p = nullptr;
   int rc = plan_create_impl(sys, &dc, &p);
   if (rc != TDB_OK) return rc;
+  {  // every remaining term a single term: one warp per output row instead of the CSR kernel
+    static const bool spmv_on = [] {
+      const char* e = std::getenv("TDB_MV_SPMV");
+      return !(e && std::atoi(e) == 0);
+    }();
+    bool all_single = spmv_on && sys->np1 == 1;
+    for (int t = 0; t < nt && all_single; ++t)
+      if (!to_tile[t] && nlog[t] > kSpmvMaxKt) all_single = false;
+    if (all_single) {
+      const int nr = d->rhi - d->rlo + 1;
+      std::vector<int> ktptr(nr + 1, 0);
+      std::vector<SpmvItem> items;
+      for (int r = 0; r < nr; ++r) {
+        const int kt = d->rlo + r;
+        for (size_t q = 0; q < cf.size(); ++q) {
+          const unsigned* mk = cm.data() + q * d->words;
+          if (!((mk[(kt - 1) >> 5] >> ((kt - 1) & 31)) & 1u)) continue;
+          items.push_back(SpmvItem{(int64_t)cs[q] * sys->nrows, cf[q], kt - cd[q] - d->clo});
+        }
+        ktptr[r + 1] = (int)items.size();
+      }
+      cudaStream_t st0 = sys->ctx->stream;
+      if (dev_malloc((void**)&p->d_ktptr, ktptr.size() * sizeof(int)) != cudaSuccess ||
+          dev_malloc((void**)&p->d_items, std::max<size_t>(1, items.size()) * sizeof(SpmvItem)) != cudaSuccess) {
+        tdb_matvec_plan_destroy(p);
+        set_error("matvec plan: cudaMalloc failed");
+        return TDB_E_NOMEM;
+      }
+      TDB_CUDA_CHECK(cudaMemcpyAsync(p->d_ktptr, ktptr.data(), ktptr.size() * sizeof(int), cudaMemcpyHostToDevice, st0));
+      if (!items.empty())
+        TDB_CUDA_CHECK(cudaMemcpyAsync(p->d_items, items.data(), items.size() * sizeof(SpmvItem),
+                                       cudaMemcpyHostToDevice, st0));
+      TDB_CUDA_CHECK(cudaStreamSynchronize(st0));
+      SpmvArgs& sa = p->sargs;
+      sa.nrows = sys->nrows;
+      sa.nkt = nr;
+      sa.kt_ptr = p->d_ktptr;
+      sa.items = p->d_items;
+      sa.fam = p->args.fam;
+      sa.xmap = p->d_xmap;
+      sa.xstride = p->xstride;
+      sa.M = (int)sys->V;
+      p->spmv = true;
+    }
+  }
   // algorithmic bytes / flops of the tiled terms (canonical CSR figures, as for the rest)
   {
     std::vector<int64_t> fp((size_t)npos * sys->nrows + 1);
@@ -700,8 +827,21 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   std::vector<unsigned> sact(act_words, 0u);
   for (int s_ = 0; s_ < npos; ++s_)
     if (term_of[s_] >= 0) sact[s_ >> 5] |= 1u << (s_ & 31);
-  // time tiles per warp (<= 6), warps per CTA
-  const int W = std::min(kBandMaxWarps, (nT + 5) / 6);
+  // the records of this plan's active lags only (cached per active set)
+  const BandTile* view_tiles = nullptr;
+  const int64_t* view_rbptr = nullptr;
+  if (band_view(sys, tf, sact, &view_tiles, &view_rbptr) != TDB_OK) {
+    tdb_matvec_plan_destroy(p);
+    return TDB_E_NOMEM;
+  }
+  // time tiles per warp ~3 (more warps per CTA: B-load parallelism), at most 8 warps
+  // (measured on config 4: 3 for the 40-row ranges of the preconditioner, 5 for longer ones)
+  static const int tt_env = [] {
+    const char* e = std::getenv("TDB_BAND_TT");
+    return e ? std::max(1, std::min(6, std::atoi(e))) : 0;
+  }();
+  const int tt_target = tt_env ? tt_env : (nT <= 6 ? 3 : 5);
+  const int W = std::max(1, std::min(kBandMaxWarps, (nT + tt_target - 1) / tt_target));
   const int TT = (nT + W - 1) / W;
   if (TT > 6) {  // more than 384 block rows: not instantiated
     tdb_matvec_plan_destroy(p);
@@ -714,14 +854,17 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   const int ncols = ithi - itlo + 1;
   int xs = std::max(padl + ncols, off0 + 8 * W * TT + 8);
   xs = (xs + 1) & ~1;
-  const long long tiles_per_rb = bs.ntiles / std::max(1, nRB);
+  long long tiles_per_rb = bs.ntiles / std::max(1, nRB);
+  for (const BandView& v : bs.views)
+    if (v.act == sact) tiles_per_rb = v.ntiles / std::max(1, nRB);
   // parts per row block: ~8 CTAs per SM (shared-memory ring), >= 2 stages of tiles per part
   static const int band_ctas = [] {
     const char* e = std::getenv("TDB_BAND_CTAS_PER_SM");
     return e ? std::max(1, std::atoi(e)) : 8;
   }();
+  // one wave: nRB * P <= SMs x resident CTAs (a partial second wave is a pure tail)
   const int P = (int)std::max<long long>(
-      1, std::min<long long>({64LL, ((long long)sys->ctx->num_sms * band_ctas + nRB - 1) / std::max(1, nRB),
+      1, std::min<long long>({64LL, ((long long)sys->ctx->num_sms * band_ctas) / std::max(1, nRB),
                               tiles_per_rb / (2 * kBandChunk)}));
   const int ldy = 8 * W * TT;
   cudaStream_t st = sys->ctx->stream;
@@ -760,8 +903,10 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   ba.dt1 = ithi + d0 - ktlo;
   ba.xs = xs;
   ba.ldy = ldy;
-  ba.tiles = bs.tiles;
-  ba.rbptr = bs.rbptr;
+  ba.tiles = view_tiles;
+  ba.rbptr = view_rbptr;
+  ba.s_irr = s_irr;
+  for (int w_ = 0; w_ < kIrrWords; ++w_) ba.irr_mask[w_] = irr_bits[w_];
   ba.s_act = p->d_sact;
   ba.rperm = sys->d_rperm;
   ba.xt = p->d_bxt;
@@ -825,12 +970,18 @@ extern "C" int tdb_matvec(TdbMatvecPlan* p, const double* x, double* y) {
     if (rc) return rc;
     if (fork) TDB_CUDA_CHECK(cudaEventRecord(p->ev_join, p->tst));
   }
-  {
+  if (p->spmv) {
+    p->sargs.x = x;
+    p->sargs.y = y;
+    const long long warps = (long long)p->sargs.nkt * p->sargs.nrows;
+    k_spmv_single<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(p->sargs);
+    TDB_CUDA_CHECK(cudaGetLastError());
+  } else {
     dim3 blk(32, 8), grd((a.M + 31) / 32, (ncols + 31) / 32);
     k_transpose_in<<<grd, blk, 0, st>>>(x, p->d_xt, a.M, ncols, a.xs, p->d_xmap, p->xstride);
   }
   p->args.y = y;
-  {
+  if (!p->spmv) {
     const long long warps = (long long)a.nrows * a.G;
     const int blocks = (int)warps;
     const int nchunks = (a.nr + 31) >> 5;
