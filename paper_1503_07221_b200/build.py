@@ -39,11 +39,14 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra_flags=(), out: str | None = None) -> str:
+    """Compile every CUDA source for sm_100a and link libtdb.so (or `out`, a tuning variant
+    built with `extra_flags`, e.g. -DTDB_QW=12; load it with TDB_LIBRARY=<path>)."""
+    lib = out or LIB
+    if not force and out is None and not _stale():
         return LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build") if out is None else os.path.join("/tmp", "tdb_objs_" + os.path.basename(out))
     os.makedirs(objdir, exist_ok=True)
     # one nvcc per translation unit, in parallel, then a host link
     procs = []
@@ -51,7 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in srcs:
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
-        cmd = [_nvcc(), *NVCC_FLAGS, "-c", "-o", obj, src]
+        cmd = [_nvcc(), *NVCC_FLAGS, *extra_flags, "-c", "-o", obj, src]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
@@ -61,13 +64,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed ({pr.returncode}): {' '.join(cmd)}\n{out}\n{err}")
         if verbose:
             print(err)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc link failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

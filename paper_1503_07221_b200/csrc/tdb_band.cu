@@ -188,8 +188,9 @@ __device__ __forceinline__ unsigned act4(const unsigned* act, int s0) {
 template <int TT>
 __global__ void __launch_bounds__(kBandMaxWarps * 32) k_band_mv(BandMvArgs a) {
   extern __shared__ __align__(128) unsigned char bm_smem[];
-  BandTile* stg = reinterpret_cast<BandTile*>(bm_smem);  // [kBandStages][kBandChunk]
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(stg + kBandStages * kBandChunk);
+  const int CH = a.chunk;  // tile records per stage
+  BandTile* stg = reinterpret_cast<BandTile*>(bm_smem);  // [kBandStages][CH]
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(stg + kBandStages * CH);
   unsigned long long* empty = full + kBandStages;
   unsigned* act = reinterpret_cast<unsigned*>(empty + kBandStages);  // [act_words + 1]
   unsigned* irr = act + a.act_words + 1;                              // [kIrrWords]
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(kBandMaxWarps * 32) k_band_mv(BandMvArgs a) {
   const int J = blockIdx.x / a.P, part = blockIdx.x % a.P;
   const long long r0 = __ldg(a.rbptr + J), r1 = __ldg(a.rbptr + J + 1);
   const long long q0 = r0 + (r1 - r0) * part / a.P, q1 = r0 + (r1 - r0) * (part + 1) / a.P;
-  const int nchunks = (int)((q1 - q0 + kBandChunk - 1) / kBandChunk);
+  const int nchunks = (int)((q1 - q0 + CH - 1) / CH);
   if (tid == 0) {
     for (int i = 0; i < kBandStages; ++i) {
       mbar_init(&full[i], 1);
@@ -210,10 +211,10 @@ __global__ void __launch_bounds__(kBandMaxWarps * 32) k_band_mv(BandMvArgs a) {
   __syncthreads();
   if (tid == 0)
     for (int c = 0; c < min(kBandStages, nchunks); ++c) {
-      const long long qb = q0 + (long long)c * kBandChunk;
-      const unsigned bytes = (unsigned)(min((long long)kBandChunk, q1 - qb) * sizeof(BandTile));
+      const long long qb = q0 + (long long)c * CH;
+      const unsigned bytes = (unsigned)(min((long long)CH, q1 - qb) * sizeof(BandTile));
       mbar_arrive_expect_tx(&full[c], bytes);
-      bulk_g2s(stg + c * kBandChunk, a.tiles + qb, bytes, &full[c]);
+      bulk_g2s(stg + c * CH, a.tiles + qb, bytes, &full[c]);
     }
   const int g = lane >> 2, k = lane & 3;
   // warp w owns the contiguous time tiles t = t0 + u (adjacent B windows share L1 sectors)
@@ -278,8 +279,8 @@ __global__ void __launch_bounds__(kBandMaxWarps * 32) k_band_mv(BandMvArgs a) {
     const int st = c % kBandStages;
     const unsigned ph = (unsigned)(c / kBandStages) & 1u;
     mbar_wait(&full[st], ph);
-    const BandTile* T = stg + st * kBandChunk;
-    const int n = (int)min((long long)kBandChunk, q1 - (q0 + (long long)c * kBandChunk));
+    const BandTile* T = stg + st * CH;
+    const int n = (int)min((long long)CH, q1 - (q0 + (long long)c * CH));
     // software pipeline: the next pair's loads are in flight during this pair's DMMAs
     PairRegs RA, RB;
     load_pair(T, 0, n, RA);
@@ -294,10 +295,10 @@ __global__ void __launch_bounds__(kBandMaxWarps * 32) k_band_mv(BandMvArgs a) {
     if (lane == 0) mbar_arrive(&empty[st]);
     if (tid == 0 && c + kBandStages < nchunks) {  // refill this stage once every warp released it
       mbar_wait(&empty[st], ph);
-      const long long qb = q0 + (long long)(c + kBandStages) * kBandChunk;
-      const unsigned bytes = (unsigned)(min((long long)kBandChunk, q1 - qb) * sizeof(BandTile));
+      const long long qb = q0 + (long long)(c + kBandStages) * CH;
+      const unsigned bytes = (unsigned)(min((long long)CH, q1 - qb) * sizeof(BandTile));
       mbar_arrive_expect_tx(&full[st], bytes);
-      bulk_g2s(stg + st * kBandChunk, a.tiles + qb, bytes, &full[st]);
+      bulk_g2s(stg + st * CH, a.tiles + qb, bytes, &full[st]);
     }
   }
   // partial tile rows of this part: ypart[part][8 J + g][8 (t0 + u) + 2 k + {0, 1}]
@@ -321,14 +322,10 @@ __global__ void k_band_reduce(BandMvArgs a) {
   }
 }
 
-size_t band_smem_bytes(int act_words) {
-  return (size_t)kBandStages * kBandChunk * sizeof(BandTile) + 2 * kBandStages * sizeof(unsigned long long) +
-         (size_t)(act_words + 1 + kIrrWords) * sizeof(unsigned);
-}
 
 template <int TT>
 int launch_tt(const BandMvArgs& a, cudaStream_t st) {
-  const size_t smem = band_smem_bytes(a.act_words);
+  const size_t smem = band_smem_bytes(a.act_words, a.chunk);
   if (smem > 48 * 1024)
     TDB_CUDA_CHECK(cudaFuncSetAttribute(k_band_mv<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_band_mv<TT><<<(unsigned)((long long)a.nRB * a.P), a.W * 32, smem, st>>>(a);
@@ -337,6 +334,11 @@ int launch_tt(const BandMvArgs& a, cudaStream_t st) {
 }
 
 }  // namespace
+
+size_t band_smem_bytes(int act_words, int chunk) {
+  return (size_t)kBandStages * chunk * sizeof(BandTile) + 2 * kBandStages * sizeof(unsigned long long) +
+         (size_t)(act_words + 1 + kIrrWords) * sizeof(unsigned);
+}
 
 int band_build(TdbSystem* sys, int f) {
   if ((int)sys->band.size() != sys->F) sys->band.assign(sys->F, BandStore{});

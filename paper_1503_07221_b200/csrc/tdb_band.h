@@ -11,13 +11,14 @@
 namespace tdb {
 
 constexpr int kBandMaxWarps = 8;  // time-group warps per CTA
-constexpr int kBandChunk = 32;    // tile records per bulk-copy stage
+constexpr int kBandChunk = 32;    // tile records per bulk-copy stage (wide plans; 16 for 1-2 warps)
 constexpr int kBandStages = 3;    // stages of the shared-memory ring
 constexpr int kIrrWords = 13;     // block-row bits of the irregular (tie) lag: 8 x 6 x 8 tiles max
 
 struct BandMvArgs {
   int nRB, P, nT, TT, W;  // row blocks, parts per row block, 8-step time tiles, tiles per warp, warps per CTA
   int nrows, act_words;   // owned rows, words of the active-position bit set
+  int chunk;              // tile records per pipeline stage
   int ktlo, nkt, rlo;     // band rows kt in [ktlo, ktlo + nkt); y row index kt - rlo
   int off0, xs;           // xt column of (kt = ktlo, lag d_0) and row stride
   int dt0, dt1;           // itlo + d_0 - ktlo, ithi + d_0 - ktlo: valid rows of lag d_0 + s are
@@ -39,7 +40,7 @@ int band_build(TdbSystem* sys, int f);
 int band_view(TdbSystem* sys, int f, const std::vector<unsigned>& act, const BandTile** tiles,
               const int64_t** rbptr);
 int band_mv_tiles(const BandMvArgs& a, cudaStream_t st);   // tile kernel -> ypart
-size_t band_smem_bytes(int act_words);
+size_t band_smem_bytes(int act_words, int chunk);
 int band_mv_reduce(const BandMvArgs& a, cudaStream_t st);  // y += sum of parts (ordered)
 
 }  // namespace tdb

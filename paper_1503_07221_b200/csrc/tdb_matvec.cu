@@ -857,15 +857,19 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   long long tiles_per_rb = bs.ntiles / std::max(1, nRB);
   for (const BandView& v : bs.views)
     if (v.act == sact) tiles_per_rb = v.ntiles / std::max(1, nRB);
-  // parts per row block: ~8 CTAs per SM (shared-memory ring), >= 2 stages of tiles per part
-  static const int band_ctas = [] {
+  // stage size: 16 records for 1-2 warps per CTA (twice the resident CTAs), else 32;
+  // parts per row block: as many CTAs as fit on the SMs at once (shared-memory ring)
+  const int chunk = W <= 2 ? 16 : kBandChunk;
+  static const int band_ctas_env = [] {
     const char* e = std::getenv("TDB_BAND_CTAS_PER_SM");
-    return e ? std::max(1, std::atoi(e)) : 8;
+    return e ? std::max(1, std::atoi(e)) : 0;
   }();
+  const int band_ctas = band_ctas_env ? band_ctas_env
+                                      : std::max(1, std::min(16, (int)((200 * 1024) / band_smem_bytes((npos + 31) / 32 + 1, chunk))));
   // one wave: nRB * P <= SMs x resident CTAs (a partial second wave is a pure tail)
   const int P = (int)std::max<long long>(
       1, std::min<long long>({64LL, ((long long)sys->ctx->num_sms * band_ctas) / std::max(1, nRB),
-                              tiles_per_rb / (2 * kBandChunk)}));
+                              tiles_per_rb / (2 * chunk)}));
   const int ldy = 8 * W * TT;
   cudaStream_t st = sys->ctx->stream;
   const size_t xt_n = (size_t)V * xs;
@@ -895,6 +899,7 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   ba.W = W;
   ba.nrows = sys->nrows;
   ba.act_words = act_words;
+  ba.chunk = chunk;
   ba.ktlo = ktlo;
   ba.nkt = nkt;
   ba.rlo = d->rlo;

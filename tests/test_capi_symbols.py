@@ -33,3 +33,11 @@ def test_no_device_errors_are_loud():
 
     with pytest.raises(RuntimeError):
         _lib.Context(0)
+
+
+def test_library_resolves_every_symbol_at_load():
+    # RTLD_NOW: an internal symbol declared in a header but left undefined (e.g. defined
+    # inside an anonymous namespace) fails here instead of on the GPU box
+    from paper_1503_07221_b200 import _lib
+
+    ctypes.CDLL(_lib.LIB_PATH, mode=os.RTLD_NOW)
