@@ -29,6 +29,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -422,15 +423,8 @@ __device__ __forceinline__ XPow xpowers(double x) {
 // float2 per FP32-tail row of one subinterval: (D - K + 1) coefficients x NT / 2
 // table pairs, rounded up to odd so rows of consecutive subintervals fall in
 // distinct shared-memory bank pairs
-// At NT = 2 (p = 0) the pitch is 2 x odd float2 (16 x odd bytes): rows start
-// 16-byte aligned for the paired LDS.128 tail loads, and up to 8 distinct rows of
-// one warp access still land in distinct bank groups.
 __host__ __device__ constexpr int tail_row_f2(int D, int K, int NT) {
-#ifdef TDB_TAIL128
-  return NT == 2 ? ((((D - K + 1) + 1) / 2) | 1) * 2 : ((D - K + 1) * NT / 2) | 1;
-#else
   return ((D - K + 1) * NT / 2) | 1;
-#endif
 }
 
 template <int NT, bool GLOBAL, int D, int K>
@@ -443,11 +437,7 @@ __device__ __forceinline__ void eval_pair(const double* __restrict__ cf, int tai
   double2 a[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-#ifdef TDB_ABL_NOCOEF
-    a[k] = make_double2(idx * 1e-3 + k, idx * 2e-3 - k);
-#else
     a[k] = GLOBAL ? __ldg(p + k * stride) : p[k * stride];
-#endif
   }
   if constexpr (K == 17) {
     double qa[8], qb[8];
@@ -481,30 +471,8 @@ __device__ __forceinline__ void eval_pair(const double* __restrict__ cf, int tai
       constexpr int TROW = tail_row_f2(D, K, NT);
       const float2* tp = reinterpret_cast<const float2*>(cf + tail_off) + idx * TROW + m;
       float2 b[D - K + 1];
-#ifdef TDB_TAIL128
-      constexpr bool kPairTail = NT == 2 && (D - K + 1) % 2 == 0;
-#else
-      constexpr bool kPairTail = false;
-#endif
-      if constexpr (kPairTail) {
-        // consecutive coefficients are adjacent float2: two per 128-bit load
-        const float4* tp4 = reinterpret_cast<const float4*>(tp);
 #pragma unroll
-        for (int k = 0; k <= D - K; k += 2) {
-          const float4 q = GLOBAL ? __ldg(tp4 + k / 2) : tp4[k / 2];
-          b[k] = make_float2(q.x, q.y);
-          b[k + 1] = make_float2(q.z, q.w);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k <= D - K; ++k) {
-#ifdef TDB_ABL_NOCOEF
-          b[k] = make_float2(idx * 1e-3f + k, idx * 2e-3f - k);
-#else
-          b[k] = GLOBAL ? __ldg(tp + k * stride) : tp[k * stride];
-#endif
-        }
-      }
+      for (int k = 0; k <= D - K; ++k) b[k] = GLOBAL ? __ldg(tp + k * stride) : tp[k * stride];
       // (psi, psi~) tails together: one packed fma.rn.f32x2 (FFMA2) per coefficient;
       // each half is an IEEE fp32 FMA, so the result equals two scalar Horner chains
       const float xf = (float)X.x;
@@ -553,10 +521,7 @@ __device__ __forceinline__ void eval_rounds(const QFam& fd, const double* __rest
                                             double (&acc)[10 * (P + 1) * (P + 1)], unsigned& n_act) {
   constexpr int NM = (P + 1) * (P + 1);
   constexpr int NT = 2 * NM;
-#ifndef TDB_NS
-#define TDB_NS 1
-#endif
-  constexpr int NS = TDB_NS;  // independent round streams per iteration (ILP)
+  constexpr int NS = 1;  // independent round streams per iteration (2 measured slower: spills)
   const int nround = (i1 - i0 + 31) >> 5;
   const int h = (nround + NS - 1) / NS;  // stream u walks rounds [u h, (u + 1) h)
   const int ilast = i1 - 1;
@@ -573,9 +538,6 @@ __device__ __forceinline__ void eval_rounds(const QFam& fd, const double* __rest
       const int i = i0 + lane + 32 * (rr + u * h);
       in[u] = i < i1;
       const int j = min(i, ilast);
-#ifdef TDB_ABL_NOPT
-      r[u] = pt.rmin + j * 1e-4; c[u] = 1.0 + j; x1[u] = 0.5; x2[u] = 0.25 + j * 1e-3; y1[u] = 0.3; y2[u] = 0.1;
-#else
       const double2 rc_ = pt.rc[j], px_ = pt.px[j], py_ = pt.py[j];
       r[u] = rc_.x;
       c[u] = rc_.y;
@@ -583,7 +545,6 @@ __device__ __forceinline__ void eval_rounds(const QFam& fd, const double* __rest
       x2[u] = px_.y;
       y1[u] = py_.x;
       y2[u] = py_.y;
-#endif
     }
     double cw[NS], xl[NS];
     int idx[NS];
@@ -822,6 +783,10 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
 #define TDB_DK(GL)                                         \
   if (fd.khead == 17) {                                    \
     TDB_F(GL, 16, 17);                                     \
+  } else if (fd.deg == 8) {                                \
+    TDB_F(GL, 8, 7);                                       \
+  } else if (fd.deg == 10) {                               \
+    TDB_F(GL, 10, 7);                                      \
   } else if (fd.deg == 12) {                               \
     TDB_F(GL, 12, 7);                                      \
   } else if (fd.deg == 14) {                               \
@@ -839,11 +804,7 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
         my_in += n_act;
         double outv[RS<NACC>::H5];
         int base, valid;
-#ifdef TDB_ABL_NORED
-        outv[0] = acc[lane % NACC]; base = lane; valid = lane < NACC ? 1 : 0;
-#else
         warp_reduce_scatter<NACC>(acc, lane, outv, base, valid);
-#endif
 #pragma unroll
         for (int k = 0; k < RS<NACC>::H5; ++k)
           if (k < valid) dst[base + k] = first ? outv[k] : prev[k] + outv[k];
@@ -1899,8 +1860,27 @@ static void family_monomials(const TdbPsiPack& pk, int nt, int nsub, int R, std:
 // scales coefficient k by R^-k), then the full FP64 degree-16 head.
 static void select_split(const TdbPsiPack& pk, int nt, int nsub, int* R_out, int* D_out, int* K_out,
                          std::vector<long double>& mono_out) {
-  static const int cands[][3] = {{1, 12, 7}, {1, 14, 7}, {1, 16, 7}, {2, 12, 7}, {4, 12, 7},
-                                 {2, 14, 7}, {4, 14, 7}, {2, 16, 7}, {4, 16, 7}, {1, 16, 17}};
+  // candidates in preference order (cheapest evaluation first); TDB_SPLITS="R,D,K;R,D,K;..."
+  // overrides the order for tuning (every candidate is still accuracy-checked below)
+  static const std::vector<std::array<int, 3>> cands = [] {
+    std::vector<std::array<int, 3>> c = {{1, 12, 7}, {1, 14, 7}, {1, 16, 7}, {2, 12, 7}, {4, 12, 7},
+                                         {2, 14, 7}, {4, 14, 7}, {2, 16, 7}, {4, 16, 7}, {1, 16, 17}};
+    if (const char* e = std::getenv("TDB_SPLITS")) {
+      std::vector<std::array<int, 3>> u;
+      int R, D, K, n = 0;
+      const char* q = e;
+      while (std::sscanf(q, "%d,%d,%d%n", &R, &D, &K, &n) == 3) {
+        if ((R == 1 || R == 2 || R == 4 || R == 8) && ((K == 7 && (D == 8 || D == 10 || D == 12 || D == 14 || D == 16)) ||
+                                                       (K == 17 && D == 16)))
+          u.push_back({R, D, K});
+        q += n;
+        while (*q == ';' || *q == ' ') ++q;
+      }
+      u.push_back({1, 16, 17});
+      c = u;
+    }
+    return c;
+  }();
   std::vector<long double> mono;
   int cached_R = 0;
   for (const auto& cd : cands) {

@@ -109,19 +109,46 @@ __global__ void k_band_rbptr(const int* __restrict__ tile_rb, long long ntiles, 
 }
 
 // per-plan view: the records whose 4-lag window meets the plan's active positions
-__global__ void k_band_flag(const BandTile* __restrict__ tiles, long long n, const unsigned* __restrict__ act,
-                            int* __restrict__ flag) {
+__device__ __forceinline__ unsigned act4_g(const unsigned* act, int s0) {
+  const int w = s0 >> 5, b = s0 & 31;
+  const unsigned long long v = ((unsigned long long)act[w + 1] << 32) | act[w];
+  return (unsigned)(v >> b) & 0xFu;
+}
+
+// time tiles t of the plan holding a valid block row for the window's lags:
+// ceil((dt0 + s0 - 7) / 8) <= t <= floor((dt1 + s0 + 3) / 8), clipped to [0, nT)
+__device__ __forceinline__ void band_trange(int dt0, int dt1, int nT, int s0, int& lo, int& hi) {
+  lo = max(0, (dt0 + s0 + 8 * 1024) / 8 - 1024);
+  hi = min(nT - 1, (dt1 + s0 + 3 + 8 * 1024) / 8 - 1024);
+}
+
+__global__ void k_band_flag(const BandTile* __restrict__ tiles, long long n, const unsigned* __restrict__ act, int dt0,
+                            int dt1, int nT, int* __restrict__ flag) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
-    const int s0 = tiles[t].s0, w = s0 >> 5, b = s0 & 31;
-    const unsigned long long v = ((unsigned long long)act[w + 1] << 32) | act[w];
-    flag[t] = ((v >> b) & 0xFull) != 0ull;
+    const int s0 = tiles[t].s0;
+    int lo, hi;
+    band_trange(dt0, dt1, nT, s0, lo, hi);
+    flag[t] = act4_g(act, s0) != 0u && lo <= hi;
   }
 }
 
+// the view's record: A values of lags outside the plan zeroed, the plan's valid time-tile
+// range in the header (pad0 = lo | hi << 8), so the kernel does no per-tile mask work
 __global__ void k_band_scatter(const BandTile* __restrict__ tiles, long long n, const int* __restrict__ flag,
-                               const long long* __restrict__ pos, BandTile* __restrict__ out) {
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
-    if (flag[t]) out[pos[t]] = tiles[t];
+                               const long long* __restrict__ pos, const unsigned* __restrict__ act, int dt0, int dt1,
+                               int nT, BandTile* __restrict__ out) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    if (!flag[t]) continue;
+    BandTile r = tiles[t];
+    const unsigned c = act4_g(act, r.s0);
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (!((c >> (i & 3)) & 1u)) r.v[i] = 0.0;
+    int lo, hi;
+    band_trange(dt0, dt1, nT, r.s0, lo, hi);
+    r.pad0 = lo | (hi << 8);
+    out[pos[t]] = r;
+  }
 }
 
 __global__ void k_band_rbview(const int64_t* __restrict__ rbptr, int nRB, const long long* __restrict__ pos,
@@ -225,25 +252,22 @@ __global__ void __launch_bounds__(kBandMaxWarps * 32) k_band_mv(BandMvArgs a) {
   const double* xl = a.xt + (a.off0 - k + g + 8 * t0);
   // one pair of tile records: header, A fragments (masked by the plan's lags), B windows
   struct PairRegs {
-    unsigned c1, c2;
     int lo1, hi1, lo2, hi2;
     double av1, av2;
     double b1[TT], b2[TT];
   };
   auto load_pair = [&](const BandTile* T, int i, int n, PairRegs& R) {
     const bool two = i + 1 < n;
-    const int l1 = T[i].l, s1 = T[i].s0;
-    const int l2 = two ? T[i + 1].l : l1, s2 = two ? T[i + 1].s0 : s1;
-    R.c1 = act4(act, s1);
-    R.c2 = two ? act4(act, s2) : 0u;
-    // time tiles t holding a valid row kt = ktlo + 8 t + n (itlo <= kt - d <= ithi for a lag
-    // d of the window): ceil((dt0 + s0 - 7) / 8) <= t <= floor((dt1 + s0 + 3) / 8)
-    R.lo1 = (a.dt0 + s1 + 8 * 1024) / 8 - 1024 - t0;
-    R.hi1 = R.c1 ? min(a.nT - 1, (a.dt1 + s1 + 3 + 8 * 1024) / 8 - 1024) - t0 : -1;
-    R.lo2 = (a.dt0 + s2 + 8 * 1024) / 8 - 1024 - t0;
-    R.hi2 = R.c2 ? min(a.nT - 1, (a.dt1 + s2 + 3 + 8 * 1024) / 8 - 1024) - t0 : -1;
-    R.av1 = ((R.c1 >> k) & 1u) ? T[i].v[lane] : 0.0;
-    R.av2 = ((R.c2 >> k) & 1u) ? T[i + (two ? 1 : 0)].v[lane] : 0.0;
+    const int4 h1 = *reinterpret_cast<const int4*>(&T[i].l);
+    const int4 h2 = two ? *reinterpret_cast<const int4*>(&T[i + 1].l) : h1;
+    const int l1 = h1.x, s1 = h1.y, l2 = h2.x, s2 = h2.y;
+    // valid time tiles of the record for this plan (baked into the view's header)
+    R.lo1 = (h1.z & 0xff) - t0;
+    R.hi1 = (h1.z >> 8) - t0;
+    R.lo2 = (h2.z & 0xff) - t0;
+    R.hi2 = two ? (h2.z >> 8) - t0 : -1;
+    R.av1 = T[i].v[lane];
+    R.av2 = two ? T[i + 1].v[lane] : 0.0;
     const double* x1 = xl + (long long)l1 * a.xs - s1;
     const double* x2 = xl + (long long)l2 * a.xs - s2;
 #pragma unroll
@@ -442,11 +466,12 @@ int band_build(TdbSystem* sys, int f) {
 // Records of family f restricted to the active positions `act` (bit s set: position s is
 // a band term), order kept; cached per active set (the recursive preconditioner reuses a
 // handful of ranges).  A quarter-range plan then streams only its lags' records.
-int band_view(TdbSystem* sys, int f, const std::vector<unsigned>& act, const BandTile** tiles,
-              const int64_t** rbptr) {
+int band_view(TdbSystem* sys, int f, const std::vector<unsigned>& act, int dt0, int dt1, int nT,
+              const BandTile** tiles, const int64_t** rbptr, long long* ntiles) {
   BandStore& b = sys->band[f];
   for (const BandView& v : b.views)
-    if (v.act == act) {
+    if (v.act == act && v.dt0 == dt0 && v.dt1 == dt1 && v.nT == nT) {
+      *ntiles = v.ntiles;
       *tiles = v.tiles;
       *rbptr = v.rbptr;
       return TDB_OK;
@@ -456,6 +481,9 @@ int band_view(TdbSystem* sys, int f, const std::vector<unsigned>& act, const Ban
   const int nRB = sys->nRB;
   BandView v;
   v.act = act;
+  v.dt0 = dt0;
+  v.dt1 = dt1;
+  v.nT = nT;
   int* flag = nullptr;
   long long* pos = nullptr;
   unsigned* dact = nullptr;
@@ -483,7 +511,7 @@ int band_view(TdbSystem* sys, int f, const std::vector<unsigned>& act, const Ban
   TRY(dev_malloc((void**)&dact, act.size() * sizeof(unsigned)));
   TRY(cudaMemcpyAsync(dact, act.data(), act.size() * sizeof(unsigned), cudaMemcpyHostToDevice, st));
   if (n > 0) {
-    k_band_flag<<<148 * 8, 256, 0, st>>>(b.tiles, n, dact, flag);
+    k_band_flag<<<148 * 8, 256, 0, st>>>(b.tiles, n, dact, dt0, dt1, nT, flag);
     TRY(cudaGetLastError());
   }
   k_flag_to_ll<<<148 * 8, 256, 0, st>>>(flag, n, pos);
@@ -497,7 +525,7 @@ int band_view(TdbSystem* sys, int f, const std::vector<unsigned>& act, const Ban
   TRY(dev_malloc((void**)&v.tiles, (size_t)std::max(1LL, nsel) * sizeof(BandTile)));
   TRY(dev_malloc((void**)&v.rbptr, (size_t)(nRB + 1) * sizeof(int64_t)));
   if (n > 0) {
-    k_band_scatter<<<148 * 8, 256, 0, st>>>(b.tiles, n, flag, pos, v.tiles);
+    k_band_scatter<<<148 * 8, 256, 0, st>>>(b.tiles, n, flag, pos, dact, dt0, dt1, nT, v.tiles);
     TRY(cudaGetLastError());
   }
   k_band_rbview<<<(nRB + 256) / 256, 256, 0, st>>>(b.rbptr, nRB, pos, v.rbptr);
@@ -509,6 +537,7 @@ int band_view(TdbSystem* sys, int f, const std::vector<unsigned>& act, const Ban
   b.views.push_back(v);
   *tiles = v.tiles;
   *rbptr = v.rbptr;
+  *ntiles = nsel;
   return TDB_OK;
 }
 

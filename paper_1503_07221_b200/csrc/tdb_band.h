@@ -37,8 +37,11 @@ struct BandMvArgs {
 };
 
 int band_build(TdbSystem* sys, int f);
-int band_view(TdbSystem* sys, int f, const std::vector<unsigned>& act, const BandTile** tiles,
-              const int64_t** rbptr);
+// the records of family f for one plan signature (active positions, valid-row offsets
+// dt0 / dt1, time tiles nT): lags outside the plan zeroed, records without a valid time
+// tile dropped, the valid time-tile range in each header; cached per signature
+int band_view(TdbSystem* sys, int f, const std::vector<unsigned>& act, int dt0, int dt1, int nT,
+              const BandTile** tiles, const int64_t** rbptr, long long* ntiles);
 int band_mv_tiles(const BandMvArgs& a, cudaStream_t st);   // tile kernel -> ypart
 size_t band_smem_bytes(int act_words, int chunk);
 int band_mv_reduce(const BandMvArgs& a, cudaStream_t st);  // y += sum of parts (ordered)

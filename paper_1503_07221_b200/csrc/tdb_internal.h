@@ -60,7 +60,8 @@ struct __align__(16) BandTile {
 
 // The records of a BandStore whose lag window meets a set of active positions.
 struct BandView {
-  std::vector<unsigned> act;  // active-position bit set (key)
+  std::vector<unsigned> act;  // active-position bit set (key, with dt0 / dt1 / nT)
+  int dt0 = 0, dt1 = 0, nT = 0;
   long long ntiles = 0;
   BandTile* tiles = nullptr;
   int64_t* rbptr = nullptr;

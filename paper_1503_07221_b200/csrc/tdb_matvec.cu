@@ -398,7 +398,7 @@ static void launch_mv_nc(const MvArgs& a, int nchunks, int blocks, cudaStream_t 
 // boundary-family blocks each applied at <= kSpmvMaxKt block rows (first block
 // column, last block row, singletons).  One warp per output row (kt, j): it walks
 // that row's single items in plan order, lanes over the CSR entries (4 entries
-// per lane in flight, coalesced 4/8-byte streams), x read from the time-major
+// per lane in flight (8 measured slower), coalesced 4/8-byte streams), x read from the time-major
 // iterate (one block column = M doubles, L1/L2 resident), a fixed xor-butterfly
 // reduction, and ONE plain store y[kt][j] = sum (rows without items get 0; the
 // band partials are added afterwards by k_band_reduce).  Deterministic.
@@ -827,10 +827,13 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   std::vector<unsigned> sact(act_words, 0u);
   for (int s_ = 0; s_ < npos; ++s_)
     if (term_of[s_] >= 0) sact[s_ >> 5] |= 1u << (s_ & 31);
-  // the records of this plan's active lags only (cached per active set)
+  // the records of this plan's active lags only, masks and valid time tiles baked in
+  // (cached per plan signature)
   const BandTile* view_tiles = nullptr;
   const int64_t* view_rbptr = nullptr;
-  if (band_view(sys, tf, sact, &view_tiles, &view_rbptr) != TDB_OK) {
+  long long view_ntiles = 0;
+  if (band_view(sys, tf, sact, itlo + d0 - ktlo, ithi + d0 - ktlo, nT, &view_tiles, &view_rbptr, &view_ntiles) !=
+      TDB_OK) {
     tdb_matvec_plan_destroy(p);
     return TDB_E_NOMEM;
   }
@@ -854,9 +857,7 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   const int ncols = ithi - itlo + 1;
   int xs = std::max(padl + ncols, off0 + 8 * W * TT + 8);
   xs = (xs + 1) & ~1;
-  long long tiles_per_rb = bs.ntiles / std::max(1, nRB);
-  for (const BandView& v : bs.views)
-    if (v.act == sact) tiles_per_rb = v.ntiles / std::max(1, nRB);
+  const long long tiles_per_rb = view_ntiles / std::max(1, nRB);
   // stage size: 16 records for 1-2 warps per CTA (twice the resident CTAs), else 32;
   // parts per row block: as many CTAs as fit on the SMs at once (shared-memory ring)
   const int chunk = W <= 2 ? 16 : kBandChunk;
