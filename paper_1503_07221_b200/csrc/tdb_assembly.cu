@@ -783,10 +783,6 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
 #define TDB_DK(GL)                                         \
   if (fd.khead == 17) {                                    \
     TDB_F(GL, 16, 17);                                     \
-  } else if (fd.deg == 8) {                                \
-    TDB_F(GL, 8, 7);                                       \
-  } else if (fd.deg == 10) {                               \
-    TDB_F(GL, 10, 7);                                      \
   } else if (fd.deg == 12) {                               \
     TDB_F(GL, 12, 7);                                      \
   } else if (fd.deg == 14) {                               \
@@ -1870,7 +1866,7 @@ static void select_split(const TdbPsiPack& pk, int nt, int nsub, int* R_out, int
       int R, D, K, n = 0;
       const char* q = e;
       while (std::sscanf(q, "%d,%d,%d%n", &R, &D, &K, &n) == 3) {
-        if ((R == 1 || R == 2 || R == 4 || R == 8) && ((K == 7 && (D == 8 || D == 10 || D == 12 || D == 14 || D == 16)) ||
+        if ((R == 1 || R == 2 || R == 4 || R == 8) && ((K == 7 && (D == 12 || D == 14 || D == 16)) ||
                                                        (K == 17 && D == 16)))
           u.push_back({R, D, K});
         q += n;
