@@ -277,11 +277,15 @@ def main():
     from paper_1503_07221_b200.assembly import DeviceAssembly, build_plan
     from paper_1503_07221_b200.block_system import assemble_system, canonical_positions
     from paper_1503_07221_b200.configs import get_config
-    from paper_1503_07221_b200.distributed import DistributedBlockHessenbergMatrix, partition_rows
+    from paper_1503_07221_b200.distributed import DistributedBlockHessenbergMatrix, assemble_system_distributed
     from paper_1503_07221_b200.kernel_weights import tables_for
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one GPU per rank; TDB_BENCH_BACKEND=gloo (plumbing check on a host with fewer GPUs
+    # than ranks - not a measurement) maps ranks onto the visible devices
+    local_dev = local % max(1, torch.cuda.device_count()) if os.environ.get("TDB_BENCH_BACKEND") == "gloo" else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
+    lag_groups = int(os.environ.get("TDB_LAG_GROUPS", "1"))
     cfg = get_config(args.config)
     mesh, grid = cfg.mesh(), cfg.grid()
     tables = tables_for(grid)
@@ -297,8 +301,10 @@ def main():
     rows_per_rank = None
     A_mv = None
     if world > 1:
-        rows_per_rank, _ = partition_rows(mesh, world)
-        A_mv = DistributedBlockHessenbergMatrix(mesh, grid, rows_per_rank, rank, ctx=ctx, tables=tables)
+        # world = row blocks x lag groups (TDB_LAG_GROUPS, default 1)
+        A_mv = assemble_system_distributed(mesh, grid, rank, world, ctx=ctx, tables=tables, lag_groups=lag_groups,
+                                           create_only=True)
+        rows_per_rank = A_mv.rows_per_rank
         sys_ = A_mv.dev
     else:
         sys_ = DeviceAssembly(mesh, plan, ctx)
@@ -380,7 +386,9 @@ def main():
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
             if world > 1:
-                B = DistributedBlockHessenbergMatrix(mesh, grid, rows_per_rank, rank, ctx=ctx, tables=tables)
+                B = DistributedBlockHessenbergMatrix(mesh, grid, rows_per_rank, rank, ctx=ctx, tables=tables,
+                                                     lag_groups=lag_groups, row_group=A_mv.row_group,
+                                                     lag_group=A_mv.lag_group)
                 host = [B.dev.family_arrays(f) for f in range(B.dev.num_families)]
             else:
                 B = assemble_system(mesh, grid, tables=tables, device=local)
@@ -410,7 +418,7 @@ def main():
 
         b = assemble_rhs(mesh, grid, gaussian_pulse_neumann(mesh))
         if world > 1:
-            S.set_comm(S.TorchDistComm())
+            S.set_comm(S.TorchDistComm(group=A_mv.row_group))
             bl = torch.as_tensor(A_mv.local_of(b)).to(dev)
         else:
             bl = torch.as_tensor(b).to(dev)
@@ -457,7 +465,8 @@ def main():
             "config": {"workload": cfg.name, "units_per_step": units, "p": grid.p,
                        "positions": len(plan.where)},
             "nnz": stats["nnz_total"],
-            "parallelism": (f"row blocks x{world} (NCCL all-gather per matvec)" if world > 1 else "1 GPU"),
+            "parallelism": (f"{world // lag_groups} row blocks x {lag_groups} lag groups (NCCL all-gather per "
+                            f"matvec{', partial-row all-reduce' if lag_groups > 1 else ''})" if world > 1 else "1 GPU"),
             "units_computed_incl_halo": units_computed,
             "l2": "flushed between timed steps (256 MB write)",
             "roofline": roofline,

@@ -175,7 +175,7 @@ class DistributedBlockHessenbergMatrix:
 
     def __init__(self, mesh, grid, rows_per_rank, rank: int, ctx=None, tables=None,
                  config: QuadratureConfig = QuadratureConfig(), gather=None, lag_groups: int = 1,
-                 row_group=None, lag_group=None, reduce=None):
+                 row_group=None, lag_group=None, reduce=None, create_only: bool = False):
         mesh, grid = as_product_inputs(mesh, grid)
         self.grid = grid
         self.diameter = mesh.diameter
@@ -193,7 +193,7 @@ class DistributedBlockHessenbergMatrix:
         if lag_groups > 1:
             positions = partition_lags(grid, positions, lag_groups)[self.lg]
         plan = build_plan(mesh, grid, tables, positions, config)
-        self.dev = DeviceAssembly(mesh, plan, ctx or _lib.default_context(), rows=self.rows)
+        self.dev = DeviceAssembly(mesh, plan, ctx or _lib.default_context(), rows=self.rows, create_only=create_only)
         self._plans: dict = {}
         # gather(local_padded (ncols, nmax) tensor) -> (nparts, ncols, nmax) tensor
         self._gather = gather
@@ -218,6 +218,10 @@ class DistributedBlockHessenbergMatrix:
             return self._gather(pad)
         import torch.distributed as dist
 
+        if dist.get_backend(self.row_group) != "nccl":  # gloo: host-staged (tests / plumbing checks)
+            parts = [torch.empty_like(pad, device="cpu") for _ in range(self.nparts)]
+            dist.all_gather(parts, pad.cpu(), group=self.row_group)
+            return torch.stack(parts).to(x_local.device)
         out = torch.empty((self.nparts, ncols, self.nmax), dtype=x_local.dtype, device=x_local.device)
         dist.all_gather_into_tensor(out, pad.contiguous(), group=self.row_group)
         return out
@@ -230,6 +234,11 @@ class DistributedBlockHessenbergMatrix:
             return self._reduce(y)
         import torch.distributed as dist
 
+        if dist.get_backend(self.lag_group) != "nccl":  # gloo: host-staged
+            c = y.cpu()
+            dist.all_reduce(c, group=self.lag_group)
+            y.copy_(c)
+            return y
         dist.all_reduce(y, group=self.lag_group)
         return y
 
@@ -263,7 +272,8 @@ class DistributedBlockHessenbergMatrix:
 
 
 def assemble_system_distributed(mesh, grid, rank: int, world: int, ctx=None, tables=None,
-                                config: QuadratureConfig = QuadratureConfig(), lag_groups: int = 1):
+                                config: QuadratureConfig = QuadratureConfig(), lag_groups: int = 1,
+                                create_only: bool = False):
     """Assemble this rank's (row block, lag range) share; torch.distributed must be
     initialised (every rank calls this: it creates the process groups)."""
     mesh, grid = as_product_inputs(mesh, grid)
@@ -274,4 +284,5 @@ def assemble_system_distributed(mesh, grid, rank: int, world: int, ctx=None, tab
     if lag_groups > 1:
         row_group, lag_group = make_groups(world // lag_groups, lag_groups)
     return DistributedBlockHessenbergMatrix(mesh, grid, rows, rank, ctx=ctx, tables=tables, config=config,
-                                            lag_groups=lag_groups, row_group=row_group, lag_group=lag_group)
+                                            lag_groups=lag_groups, row_group=row_group, lag_group=lag_group,
+                                            create_only=create_only)

@@ -100,6 +100,11 @@ class TorchDistComm:
         self.capturable = dist.get_backend(group) == "nccl"
 
     def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        if t.is_cuda and not self.capturable:  # gloo: host-staged
+            c = t.cpu()
+            self.dist.all_reduce(c, group=self.group)
+            t.copy_(c)
+            return t
         self.dist.all_reduce(t, group=self.group)
         return t
 
