@@ -284,6 +284,7 @@ def main():
     # than ranks - not a measurement) maps ranks onto the visible devices
     local_dev = local % max(1, torch.cuda.device_count()) if os.environ.get("TDB_BENCH_BACKEND") == "gloo" else local
     torch.cuda.set_device(local_dev)
+    os.environ["TDB_DEVICE"] = str(local_dev)  # libtdb's default context follows the rank's GPU
     dev = torch.device("cuda", local_dev)
     lag_groups = int(os.environ.get("TDB_LAG_GROUPS", "1"))
     cfg = get_config(args.config)
@@ -291,7 +292,7 @@ def main():
     tables = tables_for(grid)
     positions = canonical_positions(grid, mesh.diameter)
     plan = build_plan(mesh, grid, tables, positions)
-    ctx = _lib.default_context(local)
+    ctx = _lib.default_context(local_dev)
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
 

@@ -13,7 +13,10 @@ namespace tdb {
 constexpr int kMaxTables = 32;   // nt = 2 (p+1)^2, p <= 3
 constexpr int kMaxFamilies = 16;
 constexpr int kDeg = 16;         // Chebyshev degree of the fast path (PrototypeTables default)
-constexpr int kChunk = 256;      // rule points per warp work item
+#ifndef TDB_CHUNK
+#define TDB_CHUNK 256
+#endif
+constexpr int kChunk = TDB_CHUNK;  // rule points per warp work item (tuning variants: -DTDB_CHUNK)
 
 // One table family on the device (all tables share domain/nsub/fold).
 struct FamDev {
