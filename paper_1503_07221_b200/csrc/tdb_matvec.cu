@@ -953,12 +953,15 @@ extern "C" int tdb_matvec(TdbMatvecPlan* p, const double* x, double* y) {
   const MvArgs& a = p->args;
   cudaStream_t st = p->sys->ctx->stream;
   const int ncols = a.nc * a.NP1;
-  // Eager calls fork the band kernel onto the plan's stream (concurrent with the CSR
-  // kernel); inside a CUDA-graph capture (the recursive preconditioner) both stay
-  // on the capturing stream.
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  TDB_CUDA_CHECK(cudaStreamIsCapturing(st, &cap));
-  const bool fork = p->band && cap == cudaStreamCaptureStatusNone;
+  // The band kernel runs on the plan's own stream, concurrently with the boundary-term
+  // kernel (event fork / join; inside a CUDA-graph capture, e.g. the recursive
+  // preconditioner, the fork becomes two parallel graph branches).  TDB_MV_FORK=0 keeps
+  // both on the caller's stream.
+  static const bool fork_on = [] {
+    const char* e = std::getenv("TDB_MV_FORK");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const bool fork = p->band && fork_on;
   if (p->band) {
     cudaStream_t bst = st;
     if (fork) {

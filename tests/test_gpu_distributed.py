@@ -159,3 +159,52 @@ def test_two_process_sharding_matches_single(single, mode):
     sol = gather("x", 40)
     assert np.linalg.norm(sol - single["sol"]) <= 1e-9 * np.linalg.norm(single["sol"])
     print(f"{mode}: iterations {[int(r['iters'][0]) for r in res]} vs single {single['iters']}")
+
+
+def _nccl_capture_worker(rank, port, outdir):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    from paper_1503_07221_b200 import solvers as S
+    from paper_1503_07221_b200.assembly import assemble_rhs, gaussian_pulse_neumann
+    from paper_1503_07221_b200.configs import get_config
+    from paper_1503_07221_b200.distributed import DistributedBlockHessenbergMatrix, partition_rows
+
+    cfg = get_config(1)
+    mesh, grid = cfg.mesh(), cfg.grid()
+    rows, _ = partition_rows(mesh, 1)
+    A = DistributedBlockHessenbergMatrix(mesh, grid, rows, 0)  # NCCL all-gather in every matvec
+    comm = S.TorchDistComm()
+    assert comm.capturable
+    S.set_comm(comm)
+    b = torch.as_tensor(A.local_of(assemble_rhs(mesh, grid, gaussian_pulse_neumann(mesh)))).cuda()
+    scfg = S.SolverConfig(restart=50, tol=1e-10, max_iter=2000, recursion_depth=2, inner_iterations=(2, 10))
+    prec = S.recursive_preconditioner(A, scfg)
+    x, hist = S.fgmres(lambda v: A.matvec(v), b, scfg, precond=prec)
+    S.set_comm(None)
+    np.savez(os.path.join(outdir, "nccl.npz"), x=x.cpu().numpy(), graphed=np.array([prec.graph is not None]),
+             rows=A.rows)
+    dist.destroy_process_group()
+
+
+def test_nccl_collectives_captured_in_preconditioner_graph(single):
+    # the preconditioner of a distributed matrix is captured in one CUDA graph when the
+    # communicator is NCCL (its all-gathers inside): world size 1 here (one GPU), same code path
+    import torch.multiprocessing as mp
+
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_nccl_capture_worker, args=(_free_port(), d), nprocs=1, join=True)
+        r = dict(np.load(os.path.join(d, "nccl.npz")))
+    assert bool(r["graphed"][0])
+    M = single["M"]
+    sol = np.zeros((40, M))
+    sol[:, r["rows"]] = r["x"].reshape(40, -1)
+    assert np.linalg.norm(sol.ravel() - single["sol"]) <= 1e-9 * np.linalg.norm(single["sol"])
