@@ -271,11 +271,13 @@ int tdb_krylov_update(double* x, const double* x0, const double* Z, int64_t ldz,
                       const double* H, int32_t ldh, const double* g, int32_t m, void* stream);
 /* *err = 1 if the cycle broke down without converging (BreakdownError) */
 int tdb_krylov_flag(const double* state, double* err, void* stream);
-/* One fused Arnoldi step after the matvec w = A z (one launch, thread-block
- * cluster): w is orthogonalised against the rows V[0..k] (row stride ldv) by
+/* One fused Arnoldi step after the matvec w = A z: w is orthogonalised against the rows V[0..k] (row stride ldv) by
  * two classical Gram-Schmidt passes, hcol[0..k+1] = (coefficients, ||w||).  If
  * H != NULL the Givens step of tdb_krylov_givens follows; if vnext != NULL it
- * receives w / ||w||.  Replaces the MGS loop of solvers.py:189-194. k < 64. */
+ * receives w / ||w||.  Replaces the MGS loop of solvers.py:189-194. k < 64.
+ * n < 32768 (TDB_ARNOLDI_GRID_MIN_N): one launch of a <= 16-CTA thread-block
+ * cluster; longer vectors: four full-grid launches (per-CTA partials summed in
+ * CTA order by the last CTA, so the result is deterministic). */
 int tdb_krylov_arnoldi(const double* V, int64_t ldv, int64_t n, int32_t k, double* w, double* hcol, double* state,
                        double* H, int32_t ldh, double* cs, double* sn, double* g, double* vnext, void* stream);
 

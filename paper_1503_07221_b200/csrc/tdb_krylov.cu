@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <mutex>
 #include <cmath>
+#include <cstdlib>
 
 #include "tdb_common.cuh"
 #include "tdb_internal.h"
@@ -246,6 +247,170 @@ __global__ void __launch_bounds__(kArnThreads) k_krylov_arnoldi(const double* __
   cl.sync();  // peers may still read this CTA's partials
 }
 
+// ---- grid-wide Arnoldi step (long vectors) -----------------------------------
+// The cluster kernel above keeps a step in one launch but uses at most 16 SMs; for
+// long vectors (the quarter-range inner solves of the preconditioner: 1e5 entries,
+// the outer cycle: 4e5) the step runs as four full-grid launches instead, each CTA
+// streaming its slice of V and w: dots -> (update, dots) -> (update, norm) ->
+// (Givens, normalise).  Per-CTA partials are summed by the last CTA to finish
+// (threadfence + ticket), in CTA order: deterministic, no host round trip, capturable.
+constexpr int kArnGridThreads = 256;
+constexpr int kArnK1 = kArnMaxK + 1;
+
+struct ArnWs {
+  double* part;       // [G][kArnK1] per-CTA partial sums
+  double* h;          // [3][kArnK1]: pass-1 and pass-2 coefficients, ||w||^2
+  unsigned* counter;  // CTAs done with the current reduction
+  int G;
+};
+
+__device__ __forceinline__ void arn_slice(long long n, int G, long long& lo, long long& hi) {
+  const long long per = (n + G - 1) / G;
+  lo = (long long)blockIdx.x * per;
+  hi = min(n, lo + per);
+}
+
+// this CTA's partial sums of V[j] . w (j < nc) or w . w (norm) -> part[blockIdx.x][*]
+__device__ void arn_partials(const double* __restrict__ V, long long ldv, int nc, bool norm,
+                             const double* __restrict__ w, long long lo, long long hi, double* part) {
+  constexpr int NW = kArnGridThreads / 32;
+  __shared__ double red[kArnK1][NW];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int jb = 0; jb < nc; jb += 8) {
+    double loc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) loc[u] = 0.0;
+    if (!norm) {
+      const double* vb = V + (long long)jb * ldv;
+      const int nu = min(8, nc - jb);
+      for (long long i = lo + tid; i < hi; i += kArnGridThreads) {
+        const double wi = w[i];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (u < nu) loc[u] = fma(vb[(long long)u * ldv + i], wi, loc[u]);
+      }
+    } else {
+      for (long long i = lo + tid; i < hi; i += kArnGridThreads) loc[0] = fma(w[i], w[i], loc[0]);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double r_ = warp_sum(loc[u]);
+      if (lane == 0 && jb + u < nc) red[jb + u][wid] = r_;
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < nc; j += kArnGridThreads) {
+    double s_ = 0.0;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) s_ += red[j][q];
+    part[(long long)blockIdx.x * kArnK1 + j] = s_;
+  }
+}
+
+// the last CTA to arrive sums the partials in CTA order into hout
+__device__ void arn_last_reduce(const ArnWs& ws, int nc, double* hout) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(ws.counter, 1u) == (unsigned)(gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int j = threadIdx.x; j < nc; j += kArnGridThreads) {
+    double s_ = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) s_ += __ldcg(ws.part + (long long)b * kArnK1 + j);
+    hout[j] = s_;
+  }
+  if (threadIdx.x == 0) *ws.counter = 0u;
+}
+
+__global__ void __launch_bounds__(kArnGridThreads) k_arn_dots(const double* __restrict__ V, long long ldv, long long n,
+                                                             int nj, const double* __restrict__ w, ArnWs ws) {
+  long long lo, hi;
+  arn_slice(n, gridDim.x, lo, hi);
+  arn_partials(V, ldv, nj, false, w, lo, hi, ws.part);
+  arn_last_reduce(ws, nj, ws.h);
+}
+
+// w -= V^T h[src]; then the next pass's partials (dots into h[1], or the norm into h[2])
+__global__ void __launch_bounds__(kArnGridThreads) k_arn_update(const double* __restrict__ V, long long ldv,
+                                                               long long n, int nj, double* __restrict__ w, ArnWs ws,
+                                                               int src, int norm) {
+  __shared__ double h[kArnK1];
+  for (int j = threadIdx.x; j < nj; j += kArnGridThreads) h[j] = __ldcg(ws.h + src * kArnK1 + j);
+  __syncthreads();
+  long long lo, hi;
+  arn_slice(n, gridDim.x, lo, hi);
+  for (long long i = lo + threadIdx.x; i < hi; i += kArnGridThreads) {
+    double acc = 0.0;
+    for (int j = 0; j < nj; ++j) acc = fma(V[(long long)j * ldv + i], h[j], acc);
+    w[i] -= acc;
+  }
+  __syncthreads();  // this CTA's w slice is final before its own partials read it
+  arn_partials(V, ldv, norm ? 1 : nj, norm != 0, w, lo, hi, ws.part);
+  arn_last_reduce(ws, norm ? 1 : nj, ws.h + (norm ? 2 : 1) * kArnK1);
+}
+
+// hcol = (h1 + h2, ||w||), the Givens step of k_krylov_givens (CTA 0), V[k+1] = w / ||w||
+__global__ void __launch_bounds__(kArnGridThreads) k_arn_finish(ArnWs ws, long long n, int k, const double* __restrict__ w,
+                                                               double* hcol, double* st, double* H, int ldh, double* cs,
+                                                               double* sn, double* g, double* vnext) {
+  const int nj = k + 1;
+  const double hk = sqrt(__ldcg(ws.h + 2 * kArnK1));
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double hs[kArnK1];
+    for (int j = 0; j < nj; ++j) {
+      hs[j] = __ldcg(ws.h + j) + __ldcg(ws.h + kArnK1 + j);
+      hcol[j] = hs[j];
+    }
+    hcol[nj] = hk;
+    if (H != nullptr && st[TDB_KS_DONE] == 0.0) {
+      double* col = H + k;
+      double a = hs[0];
+      for (int j = 0; j < k; ++j) {
+        const double b = hs[j + 1];
+        const double t = cs[j] * a + sn[j] * b;
+        a = -sn[j] * a + cs[j] * b;
+        col[j * ldh] = t;
+      }
+      const double denom = hypot(a, hk);
+      const double c = denom > 0.0 ? a / denom : 1.0;
+      const double sg = denom > 0.0 ? hk / denom : 0.0;
+      cs[k] = c;
+      sn[k] = sg;
+      col[k * ldh] = denom;
+      const double gk = g[k];
+      g[k + 1] = -sg * gk;
+      g[k] = c * gk;
+      col[(k + 1) * ldh] = 0.0;
+      st[TDB_KS_KDONE] = (double)(k + 1);
+      if (fabs(-sg * gk) <= st[TDB_KS_TOL_ABS]) {
+        st[TDB_KS_DONE] = 1.0;
+        st[TDB_KS_CONVERGED] = 1.0;
+      } else if (hk <= 1e-14 * st[TDB_KS_BETA]) {
+        st[TDB_KS_DONE] = 1.0;
+        st[TDB_KS_BREAKDOWN] = 1.0;
+      }
+    }
+  }
+  if (vnext != nullptr) {
+    const double inv = 1.0 / hk;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+      vnext[i] = w[i] * inv;
+  }
+}
+
+// per-device workspace of the grid-wide step (allocated on the first eager call; a
+// call inside a stream capture before that uses the cluster kernel)
+struct ArnWsCache {
+  std::mutex mu;
+  ArnWs ws[64] = {};
+};
+ArnWsCache& arn_cache() {
+  static ArnWsCache* c = new ArnWsCache();
+  return *c;
+}
+
 }  // namespace
 
 extern "C" {
@@ -265,6 +430,50 @@ int tdb_krylov_arnoldi(const double* V, int64_t ldv, int64_t n, int32_t k, doubl
     if (dev < 64 && !((done >> dev) & 1ull)) {
       TDB_CUDA_CHECK(cudaFuncSetAttribute(k_krylov_arnoldi, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       done |= 1ull << dev;
+    }
+  }
+  cudaStream_t cs_ = (cudaStream_t)stream;
+  static const long long grid_min_n = [] {
+    const char* e = std::getenv("TDB_ARNOLDI_GRID_MIN_N");
+    return e ? std::atoll(e) : 32768LL;
+  }();
+  if (n >= grid_min_n && dev < 64) {
+    ArnWsCache& C = arn_cache();
+    ArnWs ws{};
+    {
+      std::lock_guard<std::mutex> g_(C.mu);
+      ws = C.ws[dev];
+      if (ws.part == nullptr) {
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        TDB_CUDA_CHECK(cudaStreamIsCapturing(cs_, &cap));
+        if (cap == cudaStreamCaptureStatusNone) {
+          int sms = 148;
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+          ws.G = 2 * sms;
+          void *pp = nullptr, *ph = nullptr, *pc = nullptr;
+          if (dev_malloc(&pp, (size_t)ws.G * kArnK1 * sizeof(double)) != cudaSuccess ||
+              dev_malloc(&ph, 3 * kArnK1 * sizeof(double)) != cudaSuccess ||
+              dev_malloc(&pc, sizeof(unsigned)) != cudaSuccess) {
+            set_error("krylov_arnoldi: workspace allocation failed");
+            return TDB_E_NOMEM;
+          }
+          TDB_CUDA_CHECK(cudaMemset(pc, 0, sizeof(unsigned)));
+          ws.part = static_cast<double*>(pp);
+          ws.h = static_cast<double*>(ph);
+          ws.counter = static_cast<unsigned*>(pc);
+          C.ws[dev] = ws;
+        }
+      }
+    }
+    if (ws.part != nullptr) {
+      const int G = (int)std::min<long long>(ws.G, std::max<long long>(1, n / 1024));
+      k_arn_dots<<<G, kArnGridThreads, 0, cs_>>>(V, (long long)ldv, (long long)n, k + 1, w, ws);
+      k_arn_update<<<G, kArnGridThreads, 0, cs_>>>(V, (long long)ldv, (long long)n, k + 1, w, ws, 0, 0);
+      k_arn_update<<<G, kArnGridThreads, 0, cs_>>>(V, (long long)ldv, (long long)n, k + 1, w, ws, 1, 1);
+      k_arn_finish<<<G, kArnGridThreads, 0, cs_>>>(ws, (long long)n, (int)k, w, hcol, state, H, (int)ldh, cs, sn, g,
+                                                   vnext);
+      TDB_CUDA_CHECK(cudaGetLastError());
+      return TDB_OK;
     }
   }
   const int csize = 16;

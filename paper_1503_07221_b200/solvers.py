@@ -242,7 +242,7 @@ def _gmres_cycle_raw(apply_A, b, x0, m, tol_abs, precond, history):
             Z[k] = z
         w = apply_A(z).clone()
         if w.is_cuda and _COMM.size == 1 and k < 63 and w.dtype == torch.float64:
-            # CGS2 orthogonalisation + norm in one cluster kernel (tdb_krylov_arnoldi)
+            # CGS2 orthogonalisation + norm on the device (tdb_krylov_arnoldi)
             from . import _lib
 
             _lib.check(_lib.LIB.tdb_krylov_arnoldi(_ptr(V), n, n, k, _ptr(w), _ptr(hcol), None, None, 0, None,
@@ -332,7 +332,7 @@ def _cycle_fixed_device(apply_A, b: torch.Tensor, m: int, tol: float, precond, e
         if precond is not None:
             Z[k].copy_(precond(V[k]))
         w = apply_A(Z[k])
-        if fused:  # CGS2 + norm + Givens + V[k+1] = w / ||w|| in one cluster kernel
+        if fused:  # CGS2 + norm + Givens + V[k+1] = w / ||w|| (tdb_krylov_arnoldi)
             vnext = _ptr(V[k + 1]) if k + 1 < m else None
             _lib.check(L.tdb_krylov_arnoldi(_ptr(V), n, n, k, _ptr(w), _ptr(hcol), _ptr(st), _ptr(H), m, _ptr(cs),
                                             _ptr(sn), _ptr(g), vnext, stream), "krylov_arnoldi")
