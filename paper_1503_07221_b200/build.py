@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtdb.so")
 SOURCES = ["tdb_context.cu", "tdb_pair.cu", "tdb_assembly.cu", "tdb_matvec.cu", "tdb_krylov.cu", "tdb_band.cu", "tdb_potential.cu", "tdb_rhs.cu", "tdb_tables.cu"]
-HEADERS = ["tdb_common.cuh", "tdb_internal.h", "tdb_band.h", "tdb_async.cuh", "tdb_geometry.cuh", "tdb_basis.cuh", os.path.join("..", "..", "include", "tdb.h")]
+HEADERS = ["tdb_common.cuh", "tdb_quad_cells.cuh", "tdb_internal.h", "tdb_band.h", "tdb_async.cuh", "tdb_geometry.cuh", "tdb_basis.cuh", os.path.join("..", "..", "include", "tdb.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

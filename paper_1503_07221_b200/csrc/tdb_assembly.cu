@@ -296,6 +296,7 @@ __global__ void k_fill_items(long long E2, const long long* __restrict__ item_ba
 struct QFam {
   int nsub, fold, coeff_off, coef_global, deg, khead, tail_off;
   int npos, delta_off;      // positions; offset of the delta table in the smem copy
+  int cell_M, cell_kappa;   // cell-owner kernel: dt spans of the support; s = floor(r / dt) + kappa - span
   unsigned sp_neg, sn_neg;  // bit t: sign of table t is -1 for a >= 0 / a < 0 (fold)
   double lo, w, inv_w, amin, amax;
   const double* delta;
@@ -325,6 +326,13 @@ struct QuadArgs {
   const int* units;
   double* part;
   unsigned long long* n_in;
+  // split with k_quad_cells (tdb_quad_cells.cuh): bit fi of cell_mask = family fi of
+  // this launch is integrated there for the regular pairs; k_quad then takes its work
+  // items `batch` at a time and drops the regular pairs that have nothing else
+  const unsigned char* pcase;
+  unsigned cell_mask;
+  int batch;
+  double dt, inv_dt;
 };
 
 #ifndef TDB_QW
@@ -633,11 +641,30 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
   unsigned long long my_in = 0;
   const unsigned lanemask_lt = (1u << lane) - 1u;
 
+  // work items are taken `batch` at a time; with the regular pairs' main families on
+  // k_quad_cells (cell_mask), lane b first checks whether item b has anything left here
+  long long it0 = 0;
+  unsigned pend = 0u;
   while (true) {
-    long long it;
-    if (lane == 0) it = (long long)atomicAdd(a.work, 1ULL);
-    it = __shfl_sync(0xffffffffu, it, 0);
-    if (it >= a.nitems) break;
+    if (pend == 0u) {
+      if (lane == 0) it0 = (long long)atomicAdd(a.work, (unsigned long long)a.batch);
+      it0 = __shfl_sync(0xffffffffu, it0, 0);
+      if (it0 >= a.nitems) break;
+      bool todo = lane < a.batch && it0 + lane < a.nitems;
+      if (todo && a.cell_mask != 0u) {
+        const int Pq = a.items[it0 + lane].x;
+        if (a.pcase[Pq] == 0) {
+          todo = false;
+          for (int fi = 0; fi < a.fam_count; ++fi)
+            if (!((a.cell_mask >> fi) & 1u) && (a.frange[(long long)a.fam_ids[fi] * E2 + Pq].lo_cnt >> 16) != 0)
+              todo = true;
+        }
+      }
+      pend = __ballot_sync(0xffffffffu, todo);
+      continue;
+    }
+    const long long it = it0 + (__ffs(pend) - 1);
+    pend &= pend - 1u;
     const int2 item = a.items[it];
     const int Pp = item.x, grp = item.y;
     // admissible position ranges of the launch's families: lane fi holds family fi's
@@ -647,6 +674,7 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
     const int ey = a.tt[Pp / a.E], ex = Pp % a.E;
     int lx[3], ly[3];
     const int cs = pair_topology(a.tri, ex, ey, lx, ly);
+    const unsigned fam_skip = cs == 0 ? a.cell_mask : 0u;  // done by k_quad_cells
     const RuleDev& R = a.rules[cs];
     const V3 X0 = corner(a.corners, ex, lx[0]), X1 = corner(a.corners, ex, lx[1]),
              X2 = corner(a.corners, ex, lx[2]);
@@ -756,7 +784,7 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
       fr.foff = __shfl_sync(0xffffffffu, my_fr.foff, fi);
       fr.lo_cnt = __shfl_sync(0xffffffffu, my_fr.lo_cnt, fi);
       const int cnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
-      if (cnt == 0) continue;
+      if (cnt == 0 || ((fam_skip >> fi) & 1u)) continue;
       const QFam& fd = a.fam[fi];
       // keep the shared-memory pointer provably shared (LDS, not generic LD)
       const double* cf_s = coef_base + fd.coeff_off;
@@ -813,6 +841,8 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
   for (int o = 16; o >= 1; o >>= 1) my_in += __shfl_xor_sync(0xffffffffu, my_in, o);
   if (lane == 0) atomicAdd(a.n_in, my_in);
 }
+
+#include "tdb_quad_cells.cuh"
 
 // ---------------------------------------------------------------------------
 // 4. singular pairs: sum item partials into item 0 (item order, deterministic)
@@ -1378,6 +1408,24 @@ struct AsmWorkspace {
     int blob_doubles = 0;
   };
   std::vector<Launch> launches;
+  // cell-owner launch (k_quad_cells): the regular pairs of the families whose tables sit
+  // on the dt-aligned 32-cell grid; cell_mask = their bits in launches[0]'s family order
+  struct CellFit {
+    bool ok = false;
+    int M = 0, kappa = 0;
+    double dt = 0.0;
+  };
+  std::vector<CellFit> cell_fit;  // per family
+  struct CellLaunch {
+    bool on = false;
+    std::vector<int> fams;
+    std::vector<QFam> qfam;
+    int delta_doubles = 0, blob_doubles = 0;
+    double* d_blob = nullptr;
+    size_t smem = 0;
+    double dt = 0.0;
+  } cell;
+  unsigned cell_mask = 0u;
   std::vector<int> s_chunk;
   int words = 0;
   // position batches (bounded partial buffer): batch b covers family f's positions
@@ -1422,6 +1470,7 @@ struct AsmWorkspace {
       dev_free(L.d_fam);
       dev_free(L.d_blob);
     }
+    dev_free(cell.d_blob);
     if (events)
       for (auto& e : ev) cudaEventDestroy(e);
   }
@@ -1577,6 +1626,40 @@ static int run_quad(TdbSystem* sys, cudaStream_t st, long long nitems) {
   const int p = sys->p;
   int rc = TDB_OK;
   int li = 0;
+  if (ws->cell.on) {  // regular pairs x grid families
+    const AsmWorkspace::CellLaunch& CL = ws->cell;
+    QuadArgs qa{};
+    qa.E = (int)sys->E;
+    qa.npair = ws->E2;
+    qa.tt = ws->tt;
+    qa.fam_count = (int)CL.fams.size();
+    for (int i = 0; i < qa.fam_count; ++i) qa.fam_ids[i] = CL.fams[i];
+    for (int i = 0; i < qa.fam_count; ++i) qa.fam[i] = CL.qfam[i];
+    qa.blob = CL.d_blob;
+    qa.blob_doubles = CL.blob_doubles;
+    qa.coef_in_smem = 1;
+    qa.delta_doubles = CL.delta_doubles;
+    qa.tri = sys->tri;
+    qa.corners = sys->corners;
+    qa.a2 = sys->a2;
+    for (int c = 0; c < 4; ++c) qa.rules[c] = ws->rules[c];
+    qa.items = ws->items;
+    qa.nitems = nitems;
+    qa.work = ws->counters + 33;
+    qa.frange = ws->frange;
+    qa.pair_base = ws->slots;
+    qa.units = ws->units;
+    qa.part = ws->part;
+    qa.n_in = ws->counters;
+    qa.pcase = ws->pcase;
+    qa.cell_mask = 0u;
+    qa.batch = 1;
+    qa.dt = CL.dt;
+    qa.inv_dt = 1.0 / CL.dt;
+    TDB_CUDA_CHECK(cudaFuncSetAttribute(k_quad_cells, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CL.smem));
+    k_quad_cells<<<ctx->num_sms, kCellWarps * 32, CL.smem, st>>>(qa);
+    TDB_CUDA_CHECK(cudaGetLastError());
+  }
   for (const auto& L : ws->launches) {
     QuadArgs qa;
     qa.E = (int)sys->E;
@@ -1601,6 +1684,10 @@ static int run_quad(TdbSystem* sys, cudaStream_t st, long long nitems) {
     qa.units = ws->units;
     qa.part = ws->part;
     qa.n_in = ws->counters;
+    qa.pcase = ws->pcase;
+    qa.cell_mask = li == 0 ? ws->cell_mask : 0u;
+    qa.batch = qa.cell_mask ? 32 : 1;
+    qa.dt = qa.inv_dt = 0.0;
     switch (p) {
       case 0: rc = launch_quad<0>(qa, L.smem, L.in_smem, ctx->num_sms, st); break;
       case 1: rc = launch_quad<1>(qa, L.smem, L.in_smem, ctx->num_sms, st); break;
@@ -1654,7 +1741,7 @@ int tdb_system_run_impl(TdbSystem* sys) {
   // groups, finalize, per family (count chunks + cub scan x 2 + fill chunks); per batch
   // the plan runs twice (counts, then values)
   const int NB = ws->nbatch;
-  long long nl = (long long)NB * (6 + (long long)ws->launches.size()) + (NB > 1 ? 6LL * NB : 0);
+  long long nl = (long long)NB * (6 + (long long)ws->launches.size() + (ws->cell.on ? 1 : 0)) + (NB > 1 ? 6LL * NB : 0);
   {
     bool multi_ = false;
     for (int c = 0; c < 4; ++c) multi_ |= ws->nitems_case[c] > 1;
@@ -2058,6 +2145,45 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
     sys->fam[f].split_R = R;
     sys->fam[f].split_D = D;
     sys->fam[f].split_K = K;
+    {  // does the family sit on the dt-aligned grid of the cell-owner kernel (tdb_quad_cells.cuh)?
+      AsmWorkspace::CellFit fit;
+      const double thi_ = fd.lo + fd.nsub * fd.w;
+      const double amin_ = fd.fold ? -thi_ : fd.lo, amax_ = thi_;
+      if (p == 0 && K == 7 && (D == 12 || D == 14 || D == 16) && hf.npos >= 2) {
+        const double dtf = (hf.delta[0] - hf.delta[hf.npos - 1]) / (double)(hf.npos - 1);
+        bool ok = dtf > 0.0;
+        for (int s = 0; ok && s < hf.npos; ++s) ok = std::fabs(hf.delta[s] - (hf.delta[0] - s * dtf)) <= 1e-9 * dtf;
+        ok = ok && std::fabs(kCellPerDt * fd.w - dtf) <= 1e-9 * dtf;
+        const double spans = (amax_ - amin_) / dtf, kap = (hf.delta[0] - amin_) / dtf;
+        const int M_ = (int)std::lround(spans), kap_ = (int)std::lround(kap);
+        ok = ok && std::fabs(spans - M_) <= 1e-9 && M_ >= 1 && M_ <= kCellSpans && std::fabs(kap - kap_) <= 1e-9;
+        // the tables must vanish at the support ends: a point within roundoff of an end
+        // may be attributed to the neighbouring (out-of-support) position
+        long double vmax = 0.0L, vend = 0.0L;
+        for (int t = 0; ok && t < nt; ++t) {
+          for (int k = 0; k < fd.nsub; ++k)
+            vmax = std::max(vmax, fabsl(mono_all[((size_t)t * fd.nsub + k) * (kDeg + 1)]));
+          const long double* mf = mono_all.data() + ((size_t)t * fd.nsub) * (kDeg + 1);
+          const long double* ml = mono_all.data() + ((size_t)t * fd.nsub + fd.nsub - 1) * (kDeg + 1);
+          long double v_first = 0.0L, v_last = 0.0L;
+          for (int c = 0; c <= D; ++c) {
+            v_first += (c & 1) ? -mf[c] : mf[c];
+            v_last += ml[c];
+          }
+          vend = std::max(vend, fabsl(v_last));
+          if (!fd.fold) vend = std::max(vend, fabsl(v_first));
+        }
+        ok = ok && vend <= 1e-9L * vmax;
+        fit.ok = ok;
+        fit.M = M_;
+        fit.kappa = kap_;
+        fit.dt = dtf;
+        if (std::getenv("TDB_VERBOSE"))
+          std::fprintf(stderr, "tdb: family %d cell grid: ok %d spans %d kappa %d dt %.17g end/max %.3Le\n", f,
+                       (int)ok, M_, kap_, dtf, vmax > 0 ? vend / vmax : 0.0L);
+      }
+      ws->cell_fit.push_back(fit);
+    }
     if (std::getenv("TDB_VERBOSE"))
       std::fprintf(stderr, "tdb: family %d npos %d nsub %d -> refine %d, degree %d, fp64 head %d\n", f,
                    hf.npos, nsub_ref, R, D, K);
@@ -2196,6 +2322,64 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
       L.smem = (L.bytes + 15) / 16 * 16 + (size_t)(L.delta_doubles + 1) / 2 * 16 + warp_bytes;
       ws->launches.push_back(std::move(L));
     }
+  }
+  // ---- cell-owner launch: regular pairs of the families on the 32-cell grid ----
+  {
+    const char* ev = std::getenv("TDB_CELLS");
+    bool want = p == 0 && !(ev && std::atoi(ev) == 0) && desc->rules[0].nq == kChunk;
+    if (want) {  // the regular rule must be a 16 x 16 tensor rule, x index slowest
+      const TdbRule& r = desc->rules[0];
+      for (int q = 0; want && q < kChunk; ++q)
+        want = r.xhat[2 * q] == r.xhat[2 * (q / 16 * 16)] && r.xhat[2 * q + 1] == r.xhat[2 * (q / 16 * 16) + 1] &&
+               r.yhat[2 * q] == r.yhat[2 * (q % 16)] && r.yhat[2 * q + 1] == r.yhat[2 * (q % 16) + 1];
+    }
+    AsmWorkspace::Launch& L0 = ws->launches[0];
+    AsmWorkspace::CellLaunch& CL = ws->cell;
+    std::vector<double> cb;
+    const size_t fixed = (size_t)kCellWarps * kCellScratchBytes + 64;
+    for (size_t fi = 0; want && fi < L0.fams.size(); ++fi) {
+      const int f = L0.fams[fi];
+      const AsmWorkspace::CellFit& fit = ws->cell_fit[f];
+      if (!fit.ok) continue;
+      if (CL.on && std::fabs(fit.dt - CL.dt) > 1e-12 * CL.dt) continue;
+      QFam q = L0.qfam[fi];
+      // one record per cell: 7 (psi, psi~) FP64 head pairs, D - 6 FP32 tail pairs, pad
+      const int rw = cell_row_words(q.deg), ntail = q.deg - 6, trow = tail_row_f2(q.deg, 7, 2);
+      const size_t need = (cb.size() + (size_t)rw * 2 * q.nsub) * 8 +
+                          (size_t)(CL.delta_doubles + sys->fam[f].npos + 2) * 8 + fixed;
+      if (need > (size_t)max_smem) continue;
+      q.coef_global = 0;
+      q.coeff_off = (int)cb.size();
+      {
+        const double* src = blob_all.data() + ws->fam_blob_off[f];
+        const float* tsrc = reinterpret_cast<const float*>(src + q.tail_off);
+        cb.resize(cb.size() + (size_t)rw * 2 * q.nsub, 0.0);
+        double* dstr = cb.data() + q.coeff_off;
+        for (int k = 0; k < q.nsub; ++k) {
+          double* rec = dstr + (size_t)k * rw * 2;
+          std::memcpy(rec, src + (size_t)k * 14, 14 * sizeof(double));
+          std::memcpy(rec + 14, tsrc + (size_t)k * 2 * trow, (size_t)ntail * 2 * sizeof(float));
+        }
+      }
+      q.delta_off = CL.delta_doubles;
+      CL.delta_doubles += sys->fam[f].npos;
+      q.cell_M = fit.M;
+      q.cell_kappa = fit.kappa;
+      CL.fams.push_back(f);
+      CL.qfam.push_back(q);
+      CL.dt = fit.dt;
+      CL.on = true;
+      ws->cell_mask |= 1u << fi;
+    }
+    if (CL.on) {
+      CL.blob_doubles = (int)cb.size();
+      if ((rc = dupload(&CL.d_blob, cb.data(), cb.size(), st))) return rc;
+      CL.smem = (size_t)(CL.blob_doubles + 1) / 2 * 16 + (size_t)(CL.delta_doubles + 1) / 2 * 16 +
+                (size_t)kCellWarps * kCellScratchBytes;
+    }
+    if (verbose)
+      std::fprintf(stderr, "tdb: cell-owner launch: %zu families, mask 0x%x, smem %zu\n", CL.fams.size(),
+                   ws->cell_mask, CL.smem);
   }
   if ((rc = dupload(&sys->famdev, sys->famdev_host.data(), F, st))) return rc;
 

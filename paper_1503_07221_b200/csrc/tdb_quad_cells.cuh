@@ -1,0 +1,361 @@
+// Regular (non-touching) pairs: "cell owner" quadrature.  Included by
+// tdb_assembly.cu after k_quad (uses its QuadArgs / QFam / reduce-scatter).
+//
+// Same integrand, rule points and table arithmetic as k_quad (the reference's
+// pair_block_contributions, _core.pyx:47-159, summed per pair and position), but the
+// work is laid out around the table instead of around the position:
+//
+//   * k_quad gathers one coefficient row per (point, position) evaluation from shared
+//     memory, ~180 B per evaluation: the LSU return path (128 B/clk/SM) runs at 75%
+//     while the FP64 pipe idles at 32% (profiles/r02/ncu_quad_cfg4_r02d_summary.txt).
+//   * Every table of a family lives on a dt-aligned grid of C = 32 cells per time step
+//     and the positions of a family are one time step apart, so a rule point at
+//     distance r sits in the same cell column j = floor(32 frac(r / dt)) at every
+//     position, one dt-span of the table support further per lag.
+//   * The pair's 256 points are sorted by column and cut into column-pure sub-runs of 4.
+//     Per dt span m of the support, every lane takes one sub-run, loads the coefficient
+//     row of its cell (m, j) into REGISTERS once and evaluates its 4 points against it
+//     (position s = floor(r / dt) + kappa - m).  Per evaluation the LSU delivers the
+//     point (12 B), the position's table offset (8 B), a quarter of a coefficient row
+//     (~50 B) and takes the two table values (16 B) instead of a 180 B row.
+//   * The values land in G[m][q] (q = rule point).  The regular rule is the tensor
+//     product of a 16-point triangle rule with itself, so the shape products are
+//     contracted per unit as shy_a * sum_ix (c g0)[ix, iy] shx_b[ix]: lane = (iy, half
+//     of ix), 8 fused multiply-adds per table per lane, then the warp reduce-scatter
+//     k_quad uses.  Summation order differs from k_quad's r-sorted order (deterministic,
+//     fixed per lane); everything else is the same arithmetic.
+//
+// Families that do not fit this grid (p > 0, a different cell count, non-uniform lags,
+// table values that do not vanish at the support ends) and the singular cases stay on
+// k_quad (QuadArgs::cell_mask tells it which (regular pair, family) work is done here).
+#pragma once
+
+constexpr int kCellWarps = 8;
+constexpr int kCellSpans = 4;   // dt spans of a table support (passes per family), max
+constexpr int kCellPerDt = 32;  // table cells per time step
+// The pair's points are sorted by cell column and cut into column-pure sub-runs of 4
+// (columns padded to a multiple of 4): at most (256 + 3 * 32) / 4 = 88 sub-runs, kept
+// transposed ([entry 0..3][sub-run], consecutive lanes read consecutive words).
+constexpr int kCellSub = 4;
+constexpr int kCellSubRuns = 96;
+// per-warp scratch: sorted r (FP64), sorted q | column << 8 | n << 13, G[span][q] = (psi, psi~), counters
+constexpr int kCellScratchBytes = kCellSub * kCellSubRuns * 12 + kCellSpans * kChunk * 16 + 32 * 4;
+static_assert(kChunk == 256, "the cell-owner kernel packs the rule point index in 8 bits");
+
+// Coefficient rows of the cell-owner launch: one 16-byte aligned record per table cell,
+// [7 x (psi, psi~) FP64 head][D - 6 x (psi, psi~) FP32 tail][pad], an odd number of
+// 16-byte words (rows of neighbouring cells start in different bank groups).
+__host__ __device__ constexpr int cell_row_words(int D) { return (7 + (D - 6 + 1) / 2) | 1; }
+
+template <int D>
+struct CellRow {
+  double2 a[7];
+  float2 b[D - 6];
+  double roww;
+  __device__ __forceinline__ void load(const double2* __restrict__ rows, int row, double w) {
+    const double2* p = rows + row * cell_row_words(D);
+#pragma unroll
+    for (int k = 0; k < 7; ++k) a[k] = p[k];
+#pragma unroll
+    for (int k = 0; k < (D - 6) / 2; ++k) {
+      const double2 t = p[7 + k];
+      b[2 * k] = make_float2(__int_as_float(__double2loint(t.x)), __int_as_float(__double2hiint(t.x)));
+      b[2 * k + 1] = make_float2(__int_as_float(__double2loint(t.y)), __int_as_float(__double2hiint(t.y)));
+    }
+    roww = (double)row * w;
+  }
+};
+
+// (psi, psi~) of one table pair from register-resident coefficients: the arithmetic of
+// eval_pair<2, ., D, 7> (Estrin FP64 head, packed FP32 Horner tail).
+template <int D>
+__device__ __forceinline__ void cell_poly(const CellRow<D>& c, double x, double& v0, double& v1) {
+  const double2(&a)[7] = c.a;
+  const double x2 = x * x, x4 = x2 * x2;
+  const double qa0 = fma(a[1].x, x, a[0].x), qa1 = fma(a[3].x, x, a[2].x), qa2 = fma(a[5].x, x, a[4].x);
+  const double qb0 = fma(a[1].y, x, a[0].y), qb1 = fma(a[3].y, x, a[2].y), qb2 = fma(a[5].y, x, a[4].y);
+  const double ra0 = fma(qa1, x2, qa0), ra1 = fma(a[6].x, x2, qa2);
+  const double rb0 = fma(qb1, x2, qb0), rb1 = fma(a[6].y, x2, qb2);
+  v0 = fma(ra1, x4, ra0);
+  v1 = fma(rb1, x4, rb0);
+  const float xf = (float)x;
+  const float2 xx = make_float2(xf, xf);
+  float2 tt = c.b[D - 7];
+#pragma unroll
+  for (int k = D - 8; k >= 0; --k) tt = ffma2(tt, xx, c.b[k]);
+  const double x7 = x4 * x2 * x;
+  v0 = fma(x7, (double)tt.x, v0);
+  v1 = fma(x7, (double)tt.y, v1);
+}
+
+// Stage 1 of one family: per dt span m of the support, round by round every lane takes
+// one column-pure sub-run of 4 points, loads the coefficient row of its (span, column)
+// cell into registers and evaluates the 4 points against it, two at a time.
+template <int D>
+__device__ __forceinline__ void cell_family(const QFam& fd, const double2* __restrict__ rows,
+                                            const double* __restrict__ sdel, const double* __restrict__ s_r,
+                                            const int* __restrict__ s_q, double2* __restrict__ G, int nsr,
+                                            int lane, int w_lo, unsigned ucnt, unsigned& n_act) {
+  const double amin = fd.amin, amax = fd.amax, lo = fd.lo, w = fd.w, inv_w = fd.inv_w;
+  const int nsub = fd.nsub, nspan = fd.cell_M;
+  const bool fold = fd.fold != 0;
+  const int abs_mask = fold ? 0x7fffffff : -1;  // |a| as a mask on the high word
+  const unsigned sp1 = (fd.sp_neg & 1u) << 31, sn1 = (fd.sn_neg & 1u) << 31;
+  for (int m = 0; m < nspan; ++m) {
+    const int koff = fd.cell_kappa - m - w_lo;
+    double2* Gm = G + m * kChunk;
+#pragma unroll 1
+    for (int u0 = 0; u0 < nsr; u0 += 32) {
+      const bool live = u0 + lane < nsr;
+      const int u = live ? u0 + lane : 0;
+      double r[kCellSub], delta[kCellSub];
+      int qi[kCellSub];
+      bool valid[kCellSub];
+#pragma unroll
+      for (int i = 0; i < kCellSub; ++i) {
+        r[i] = s_r[i * kCellSubRuns + u];
+        qi[i] = s_q[i * kCellSubRuns + u];
+      }
+      CellRow<D> cr;
+      {
+        const int c = m * kCellPerDt + ((qi[0] >> 8) & 31);  // cell on the a axis, from amin
+        cr.load(rows, fold ? (c < nsub ? nsub - 1 - c : c - nsub) : c, w);
+      }
+#pragma unroll
+      for (int i = 0; i < kCellSub; ++i) {
+        const unsigned sr = (unsigned)((qi[i] >> 13) + koff);  // position relative to the pair's window
+        valid[i] = sr < ucnt;
+        delta[i] = sdel[valid[i] ? sr : 0u];
+      }
+#pragma unroll
+      for (int i = 0; i < kCellSub; ++i) {
+        const double av = r[i] + delta[i];
+        const bool act = valid[i] && av >= amin && av <= amax;
+        n_act += (act && live) ? 1u : 0u;
+        const int avh = __double2hiint(av);
+        const double aa = __hiloint2double(avh & abs_mask, __double2loint(av));
+        // cheb_locate's local coordinate with the sub-run's row for idx (equal to it except
+        // within roundoff of a cell edge, where the two pieces agree to 1e-16)
+        const double x = 2.0 * (aa - lo - cr.roww) * inv_w - 1.0;
+        double v0, v1;
+        cell_poly<D>(cr, x, v0, v1);
+        const int sg = (int)(avh < 0 ? sn1 : sp1);
+        v0 = __hiloint2double(__double2hiint(v0) ^ sg, __double2loint(v0));
+        v1 = __hiloint2double(__double2hiint(v1) ^ sg, __double2loint(v1));
+        if (live && qi[i] >= 0) Gm[qi[i] & 255] = act ? make_double2(v0, v1) : make_double2(0.0, 0.0);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kCellWarps * 32, 1) k_quad_cells(QuadArgs a) {
+  constexpr int NACC = 10;
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(16) double smem[];
+  double* sblob = smem;
+  double* sdelta = sblob + (a.blob_doubles + 1) / 2 * 2;
+  char* swarp = reinterpret_cast<char*>(sdelta + (a.delta_doubles + 1) / 2 * 2);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  char* mine = swarp + (size_t)wid * kCellScratchBytes;
+  double2* G = reinterpret_cast<double2*>(mine);
+  double* s_r = reinterpret_cast<double*>(G + kCellSpans * kChunk);
+  int* s_q = reinterpret_cast<int*>(s_r + kCellSub * kCellSubRuns);
+  unsigned* bins = reinterpret_cast<unsigned*>(s_q + kCellSub * kCellSubRuns);
+  for (int i = threadIdx.x; i < a.blob_doubles; i += blockDim.x) sblob[i] = a.blob[i];
+  for (int fi = 0; fi < a.fam_count; ++fi)
+    for (int i = threadIdx.x; i < a.fam[fi].npos; i += blockDim.x)
+      sdelta[a.fam[fi].delta_off + i] = a.fam[fi].delta[i];
+  __syncthreads();
+
+  // rule constants of this lane's points q = lane + 32 k: x index 2 k + (lane >> 4), y index lane & 15
+  const RuleDev& R = a.rules[0];
+  const double y1 = R.y1[lane], y2 = R.y2[lane];
+  const double shy0 = 1.0 - y1, shy1 = y1 - y2, shy2 = y2;
+
+  const unsigned E = (unsigned)a.E;
+  const long long E2 = a.npair;
+  const double inv_dt = a.inv_dt;
+  unsigned long long my_in = 0;
+
+  // pair index two ahead, pair header (corners, plan entries) one ahead of the work
+  struct Header {
+    double d;  // lanes 0-8 / 9-17: corners of ex / ey, 18 / 19: twice their areas
+    FRange fr;
+    int units, cs;
+    long long base;
+  };
+  auto grab = [&]() {
+    long long v = 0;
+    if (lane == 0) v = (long long)atomicAdd(a.work, 1ULL);
+    return __shfl_sync(FULL, v, 0);
+  };
+  auto load_header = [&](long long Pp, Header& h) {
+    h.d = 0.0;
+    h.fr = FRange{0, 0};
+    h.units = 0;
+    h.cs = 0;
+    h.base = 0;
+    if (Pp < E2) {
+      h.units = a.units[Pp];
+      h.cs = a.pcase[Pp];
+      h.base = a.pair_base[Pp];
+      const unsigned ex = (unsigned)Pp % E;
+      const int ey = a.tt[(unsigned)Pp / E];
+      if (lane < 9) h.d = a.corners[9 * (long long)ex + lane];
+      else if (lane < 18) h.d = a.corners[9 * (long long)ey + lane - 9];
+      else if (lane == 18) h.d = a.a2[ex];
+      else if (lane == 19) h.d = a.a2[ey];
+      if (lane < a.fam_count) h.fr = a.frange[(long long)a.fam_ids[lane] * E2 + Pp];
+    }
+  };
+  long long P0 = grab();
+  Header pre;
+  load_header(P0, pre);
+  long long P1 = grab();
+
+  while (P0 < E2) {
+    const Header cur = pre;
+    P0 = P1;
+    load_header(P0, pre);
+    P1 = grab();
+    if (cur.units == 0 || cur.cs != 0) continue;
+    if (__ballot_sync(FULL, (cur.fr.lo_cnt >> 16) != 0) == 0u) continue;
+    V3 X0, X1, X2, Y0, Y1, Y2;
+    X0.x = __shfl_sync(FULL, cur.d, 0); X0.y = __shfl_sync(FULL, cur.d, 1); X0.z = __shfl_sync(FULL, cur.d, 2);
+    X1.x = __shfl_sync(FULL, cur.d, 3); X1.y = __shfl_sync(FULL, cur.d, 4); X1.z = __shfl_sync(FULL, cur.d, 5);
+    X2.x = __shfl_sync(FULL, cur.d, 6); X2.y = __shfl_sync(FULL, cur.d, 7); X2.z = __shfl_sync(FULL, cur.d, 8);
+    Y0.x = __shfl_sync(FULL, cur.d, 9); Y0.y = __shfl_sync(FULL, cur.d, 10); Y0.z = __shfl_sync(FULL, cur.d, 11);
+    Y1.x = __shfl_sync(FULL, cur.d, 12); Y1.y = __shfl_sync(FULL, cur.d, 13); Y1.z = __shfl_sync(FULL, cur.d, 14);
+    Y2.x = __shfl_sync(FULL, cur.d, 15); Y2.y = __shfl_sync(FULL, cur.d, 16); Y2.z = __shfl_sync(FULL, cur.d, 17);
+    const V3 e1 = sub(X1, X0), e2 = sub(X2, X1), f1 = sub(Y1, Y0), f2 = sub(Y2, Y1);
+    const double scale = kInv4Pi * __shfl_sync(FULL, cur.d, 18) * __shfl_sync(FULL, cur.d, 19);
+
+    // geometry of the lane's points (k_quad's arithmetic), their time-step index n and cell column j
+    double ck[kNK], rk[kNK];
+    int nj[kNK];  // column | n << 5
+    bins[lane] = 0u;
+    __syncwarp();
+    const double yx = Y0.x + y1 * f1.x + y2 * f2.x, yy = Y0.y + y1 * f1.y + y2 * f2.y,
+                 yz = Y0.z + y1 * f1.z + y2 * f2.z;
+#pragma unroll
+    for (int k = 0; k < kNK; ++k) {
+      const double x1 = R.x1[lane + 32 * k], x2 = R.x2[lane + 32 * k];
+      const double dx = (X0.x + x1 * e1.x + x2 * e2.x) - yx;
+      const double dy = (X0.y + x1 * e1.y + x2 * e2.y) - yy;
+      const double dz = (X0.z + x1 * e1.z + x2 * e2.z) - yz;
+      rk[k] = sqrt(dx * dx + dy * dy + dz * dz);
+      ck[k] = scale * R.w[lane + 32 * k] / rk[k];
+      const double u = rk[k] * inv_dt;
+      const int n = (int)u;
+      const int j = min(kCellPerDt - 1, (int)((u - (double)n) * (double)kCellPerDt));
+      nj[k] = j | (n << 5);
+      atomicAdd(bins + j, 1u);
+    }
+    __syncwarp();
+    int nsr;  // sub-runs of the pair
+    {  // columns -> column-pure sub-runs of 4 (the order inside a column is free: stage 1
+       // stores by rule point, stage 2 sums in rule-point order)
+      const int cnt = (int)bins[lane];
+      const int mine_sr = (cnt + kCellSub - 1) / kCellSub;
+      int incl = mine_sr;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += v;
+      }
+      nsr = __shfl_sync(FULL, incl, 31);
+      const int first = (incl - mine_sr) * kCellSub;  // first slot of column `lane`
+      __syncwarp();
+      bins[lane] = (unsigned)first;
+      for (int p = cnt; p < mine_sr * kCellSub; ++p) {  // pads of the column's last sub-run
+        const int slot = first + p;
+        s_q[(slot & 3) * kCellSubRuns + (slot >> 2)] = (int)0x80000000u | (lane << 8);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < kNK; ++k) {
+        const int slot = (int)atomicAdd(bins + (nj[k] & 31), 1u);
+        const int at = (slot & 3) * kCellSubRuns + (slot >> 2);
+        s_r[at] = rk[k];
+        s_q[at] = (nj[k] << 8) | (lane + 32 * k);
+      }
+      __syncwarp();
+    }
+
+    for (int fi = 0; fi < a.fam_count; ++fi) {
+      FRange fr;
+      fr.foff = __shfl_sync(FULL, cur.fr.foff, fi);
+      fr.lo_cnt = __shfl_sync(FULL, cur.fr.lo_cnt, fi);
+      const int ucnt = fr.lo_cnt >> 16, s_lo = fr.lo_cnt & 0xffff;
+      if (ucnt == 0) continue;
+      const QFam& fd = a.fam[fi];
+      const double2* rows = reinterpret_cast<const double2*>(sblob + fd.coeff_off);
+      const double* sdel = sdelta + fd.delta_off + s_lo;
+      unsigned n_act = 0;
+      if (fd.deg == 12)
+        cell_family<12>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, n_act);
+      else if (fd.deg == 14)
+        cell_family<14>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, n_act);
+      else
+        cell_family<16>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, n_act);
+      my_in += n_act;
+      __syncwarp();
+
+      // stage 2: per unit, contract the table values with the weights and shape functions
+      double cx[kNK][3];
+      int mk[kNK];  // span of point k at the window's first position
+#pragma unroll
+      for (int k = 0; k < kNK; ++k) {
+        const double x1 = R.x1[lane + 32 * k], x2 = R.x2[lane + 32 * k];
+        cx[k][0] = ck[k] * (1.0 - x1);
+        cx[k][1] = ck[k] * (x1 - x2);
+        cx[k][2] = ck[k] * x2;
+        mk[k] = (nj[k] >> 5) + fd.cell_kappa - s_lo;
+      }
+      const unsigned nspan = (unsigned)fd.cell_M;
+      double* dst = a.part + (cur.base + fr.foff) * NACC;
+      const double2* Gq = G + lane;
+      for (int si = 0; si < ucnt; si += 2) {
+        double tb[2][4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) tb[u][0] = tb[u][1] = tb[u][2] = tb[u][3] = 0.0;
+#pragma unroll
+        for (int k = 0; k < kNK; ++k) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const unsigned m = (unsigned)(mk[k] - si - u);
+            double2 g = make_double2(0.0, 0.0);
+            if (m < nspan) g = Gq[m * kChunk + 32 * k];
+            tb[u][0] = fma(g.x, cx[k][0], tb[u][0]);
+            tb[u][1] = fma(g.x, cx[k][1], tb[u][1]);
+            tb[u][2] = fma(g.x, cx[k][2], tb[u][2]);
+            tb[u][3] = fma(g.y, ck[k], tb[u][3]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (si + u >= ucnt) break;  // warp-uniform
+          double acc[NACC];
+          acc[0] = shy0 * tb[u][0];
+          acc[1] = shy0 * tb[u][1];
+          acc[2] = shy0 * tb[u][2];
+          acc[3] = shy1 * tb[u][0];
+          acc[4] = shy1 * tb[u][1];
+          acc[5] = shy1 * tb[u][2];
+          acc[6] = shy2 * tb[u][0];
+          acc[7] = shy2 * tb[u][1];
+          acc[8] = shy2 * tb[u][2];
+          acc[9] = tb[u][3];
+          double outv[RS<NACC>::H5];
+          int base, valid;
+          warp_reduce_scatter<NACC>(acc, lane, outv, base, valid);
+          if (valid > 0) dst[(long long)(si + u) * NACC + base] = outv[0];
+        }
+      }
+      __syncwarp();
+    }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) my_in += __shfl_xor_sync(FULL, my_in, o);
+  if (lane == 0) atomicAdd(a.n_in, my_in);
+}
