@@ -139,6 +139,10 @@ typedef struct TdbStats {
   int64_t launches;        /* kernel launches issued by the last tdb_system_run */
   int64_t units_primary;   /* units whose test triangle's first vertex is an owned row:
                               summed over row blocks = the global unit count */
+  /* share of the regular-pair kernel (k_quad_cells) in ms_quad / n_in, pairs it took */
+  double ms_quad_cells;
+  int64_t n_in_cells;
+  int64_t pairs_cells;
 } TdbStats;
 
 typedef struct TdbContext TdbContext;

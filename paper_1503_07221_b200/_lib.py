@@ -71,6 +71,7 @@ class TdbStats(C.Structure):
         ("ms_plan", C.c_double), ("ms_quad", C.c_double), ("ms_finalize", C.c_double),
         ("ms_pattern", C.c_double), ("ms_total", C.c_double),
         ("units_case", i64 * 4), ("pairs_case", i64 * 4), ("launches", i64), ("units_primary", i64),
+        ("ms_quad_cells", C.c_double), ("n_in_cells", i64), ("pairs_cells", i64),
     ]
 
     def as_dict(self) -> dict:

@@ -195,6 +195,7 @@ struct PlanArgs {
                                    // [8] units of pairs whose test triangle's first vertex is owned
   const unsigned char* owned;      // (V,) owned test-vertex rows of this system
   int wlo[kMaxFamilies], whi[kMaxFamilies];  // position batch: family f's positions [wlo, whi)
+  unsigned cell_fams;  // families whose regular pairs run on k_quad_cells (no k_quad work item)
 };
 
 __global__ void k_plan_pairs(PlanArgs a) {
@@ -230,7 +231,7 @@ __global__ void k_plan_pairs(PlanArgs a) {
     const int ey = a.tt[P / a.E], ex = (int)(P % a.E);
     double dmin, dmax;
     const int cs = pair_bounds(a.corners, a.tri, ex, ey, dmin, dmax);
-    int units = 0;
+    int units = 0, rest = 0;  // rest: units that k_quad_cells does not take
     for (int f = 0; f < a.F; ++f) {
       const int n = s_off[f + 1] - s_off[f];
       int s0 = max(a.wlo[f], first_geq(s_hi + s_off[f], n, dmin));  // shi >= tmin
@@ -241,12 +242,20 @@ __global__ void k_plan_pairs(PlanArgs a) {
       fr.lo_cnt = (cnt > 0 ? s0 : 0) | (cnt << 16);
       a.frange[(long long)f * E2 + P] = fr;
       units += cnt;
+      if (cs != 0 || !((a.cell_fams >> f) & 1u)) rest += cnt;
     }
     a.units[P] = units;
     a.pcase[P] = (unsigned char)cs;
-    const int ni = units > 0 ? a.nitems_case[cs] : 0;
-    a.slots[P] = (long long)units * ni;
+    // partial slots for every chunk group of the pair; k_quad work items only where
+    // something is left for it
+    const int ng = units > 0 ? a.nitems_case[cs] : 0;
+    const int ni = rest > 0 ? ng : 0;
+    a.slots[P] = (long long)units * ng;
     a.nitems[P] = ni;
+    if (P == E2 - 1) {  // the last pair's own counts (the scans are exclusive)
+      a.case_pairs[10] = (unsigned long long)units * ng;
+      a.case_pairs[11] = (unsigned long long)ni;
+    }
     if (units > 0) {
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -275,14 +284,13 @@ __global__ void k_plan_pairs(PlanArgs a) {
 }
 
 __global__ void k_fill_items(long long E2, const long long* __restrict__ item_base,
-                             const long long* __restrict__ item_end_excl_next,
-                             const int* __restrict__ units, const unsigned char* __restrict__ pcase,
-                             const int* nitems_case, int2* __restrict__ items) {
+                             const unsigned long long* __restrict__ last_counts,
+                             const int* __restrict__ units, int2* __restrict__ items) {
   for (long long P = blockIdx.x * (long long)blockDim.x + threadIdx.x; P < E2;
        P += (long long)gridDim.x * blockDim.x) {
     if (units[P] == 0) continue;
-    const int ni = nitems_case[pcase[P]];
     const long long b = item_base[P];
+    const int ni = (int)((P + 1 < E2 ? item_base[P + 1] : b + (long long)last_counts[11]) - b);
     for (int i = 0; i < ni; ++i) items[b + i] = make_int2((int)P, i);
   }
 }
@@ -327,11 +335,10 @@ struct QuadArgs {
   double* part;
   unsigned long long* n_in;
   // split with k_quad_cells (tdb_quad_cells.cuh): bit fi of cell_mask = family fi of
-  // this launch is integrated there for the regular pairs; k_quad then takes its work
-  // items `batch` at a time and drops the regular pairs that have nothing else
+  // this launch is integrated there for the regular pairs (the pair plan issues no
+  // k_quad work item for a regular pair with nothing else)
   const unsigned char* pcase;
   unsigned cell_mask;
-  int batch;
   double dt, inv_dt;
 };
 
@@ -641,30 +648,11 @@ __global__ void __launch_bounds__(kQuadWarps * 32, 1) k_quad(QuadArgs a) {
   unsigned long long my_in = 0;
   const unsigned lanemask_lt = (1u << lane) - 1u;
 
-  // work items are taken `batch` at a time; with the regular pairs' main families on
-  // k_quad_cells (cell_mask), lane b first checks whether item b has anything left here
-  long long it0 = 0;
-  unsigned pend = 0u;
   while (true) {
-    if (pend == 0u) {
-      if (lane == 0) it0 = (long long)atomicAdd(a.work, (unsigned long long)a.batch);
-      it0 = __shfl_sync(0xffffffffu, it0, 0);
-      if (it0 >= a.nitems) break;
-      bool todo = lane < a.batch && it0 + lane < a.nitems;
-      if (todo && a.cell_mask != 0u) {
-        const int Pq = a.items[it0 + lane].x;
-        if (a.pcase[Pq] == 0) {
-          todo = false;
-          for (int fi = 0; fi < a.fam_count; ++fi)
-            if (!((a.cell_mask >> fi) & 1u) && (a.frange[(long long)a.fam_ids[fi] * E2 + Pq].lo_cnt >> 16) != 0)
-              todo = true;
-        }
-      }
-      pend = __ballot_sync(0xffffffffu, todo);
-      continue;
-    }
-    const long long it = it0 + (__ffs(pend) - 1);
-    pend &= pend - 1u;
+    long long it;
+    if (lane == 0) it = (long long)atomicAdd(a.work, 1ULL);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= a.nitems) break;
     const int2 item = a.items[it];
     const int Pp = item.x, grp = item.y;
     // admissible position ranges of the launch's families: lane fi holds family fi's
@@ -1432,7 +1420,7 @@ struct AsmWorkspace {
   // [wlo[b][f], whi[b][f]); one batch = every position
   int nbatch = 1;
   std::vector<std::vector<int>> wlo, whi;
-  cudaEvent_t ev[6];
+  cudaEvent_t ev[8];  // [6], [7]: around k_quad_cells
   bool events = false;
   long long launch_count = 0;
   // pattern phase: the families' count -> scan -> fill chains run on their own
@@ -1520,6 +1508,8 @@ static PlanArgs plan_args(TdbSystem* sys, int b) {
   pa.nitems = ws->nitems;
   pa.pcase = ws->pcase;
   pa.case_pairs = ws->counters + 40;
+  pa.cell_fams = 0u;
+  for (int f : ws->cell.fams) pa.cell_fams |= 1u << f;
   return pa;
 }
 
@@ -1569,8 +1559,7 @@ static int run_plan(TdbSystem* sys, cudaStream_t st, int b = 0) {
   if ((rc = scan_inplace(ws, ws->slots, ws->E2, st))) return rc;
   if ((rc = scan_inplace(ws, ws->nitems, ws->E2, st))) return rc;
   if (ws->items) {
-    k_fill_items<<<(int)blocks, 256, 0, st>>>(ws->E2, ws->nitems, nullptr, ws->units, ws->pcase,
-                                              ws->d_nitems_case, ws->items);
+    k_fill_items<<<(int)blocks, 256, 0, st>>>(ws->E2, ws->nitems, ws->counters + 40, ws->units, ws->items);
     TDB_CUDA_CHECK(cudaGetLastError());
   }
   return TDB_OK;
@@ -1653,12 +1642,13 @@ static int run_quad(TdbSystem* sys, cudaStream_t st, long long nitems) {
     qa.n_in = ws->counters;
     qa.pcase = ws->pcase;
     qa.cell_mask = 0u;
-    qa.batch = 1;
     qa.dt = CL.dt;
     qa.inv_dt = 1.0 / CL.dt;
     TDB_CUDA_CHECK(cudaFuncSetAttribute(k_quad_cells, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CL.smem));
+    TDB_CUDA_CHECK(cudaEventRecord(ws->ev[6], st));
     k_quad_cells<<<ctx->num_sms, kCellWarps * 32, CL.smem, st>>>(qa);
     TDB_CUDA_CHECK(cudaGetLastError());
+    TDB_CUDA_CHECK(cudaEventRecord(ws->ev[7], st));
   }
   for (const auto& L : ws->launches) {
     QuadArgs qa;
@@ -1686,7 +1676,6 @@ static int run_quad(TdbSystem* sys, cudaStream_t st, long long nitems) {
     qa.n_in = ws->counters;
     qa.pcase = ws->pcase;
     qa.cell_mask = li == 0 ? ws->cell_mask : 0u;
-    qa.batch = qa.cell_mask ? 32 : 1;
     qa.dt = qa.inv_dt = 0.0;
     switch (p) {
       case 0: rc = launch_quad<0>(qa, L.smem, L.in_smem, ctx->num_sms, st); break;
@@ -1721,13 +1710,10 @@ static int plan_totals(AsmWorkspace* ws, cudaStream_t st, long long* slots, long
   int rc;
   if ((rc = read_ll(ws->slots + E2 - 1, &ex_s, st))) return rc;
   if ((rc = read_ll(ws->nitems + E2 - 1, &ex_i, st))) return rc;
-  int u_last = 0;
-  unsigned char c_last = 0;
-  TDB_CUDA_CHECK(cudaMemcpy(&u_last, ws->units + E2 - 1, sizeof(int), cudaMemcpyDeviceToHost));
-  TDB_CUDA_CHECK(cudaMemcpy(&c_last, ws->pcase + E2 - 1, 1, cudaMemcpyDeviceToHost));
-  const int ni = u_last > 0 ? ws->nitems_case[c_last] : 0;
-  *slots = ex_s + (long long)u_last * ni;
-  *items = ex_i + ni;
+  unsigned long long last[2] = {0, 0};  // the last pair's slots and work items (k_plan_pairs)
+  TDB_CUDA_CHECK(cudaMemcpy(last, ws->counters + 50, sizeof(last), cudaMemcpyDeviceToHost));
+  *slots = ex_s + (long long)last[0];
+  *items = ex_i + (long long)last[1];
   return TDB_OK;
 }
 
@@ -1792,6 +1778,7 @@ int tdb_system_run_impl(TdbSystem* sys) {
     TDB_CUDA_CHECK(cudaMemcpy(cnt, ws->counters, sizeof(cnt), cudaMemcpyDeviceToHost));
     sys->stats.ms_plan = elapsed(ws->ev[0], ws->ev[1]);
     sys->stats.ms_quad = elapsed(ws->ev[1], ws->ev[2]);
+    sys->stats.ms_quad_cells = ws->cell.on ? elapsed(ws->ev[6], ws->ev[7]) : 0.0;
     sys->stats.ms_finalize = elapsed(ws->ev[2], ws->ev[3]);
     sys->stats.ms_pattern = elapsed(ws->ev[3], ws->ev[4]);
   } else {
@@ -1806,7 +1793,7 @@ int tdb_system_run_impl(TdbSystem* sys) {
       if ((rc = run_pattern_count(sys, f, st, nullptr, 0, 0, true))) return rc;
     TDB_CUDA_CHECK(cudaEventRecord(ws->ev[1], st));
     std::memset(cnt, 0, sizeof(cnt));
-    float ms_quad = 0.f;
+    float ms_quad = 0.f, ms_cells = 0.f;
     for (int b = 0; b < NB; ++b) {
       if ((rc = run_plan(sys, st, b))) return rc;
       long long bs = 0, bi = 0;
@@ -1821,13 +1808,17 @@ int tdb_system_run_impl(TdbSystem* sys) {
       TDB_CUDA_CHECK(cudaMemcpyAsync(c, ws->counters, sizeof(c), cudaMemcpyDeviceToHost, st));
       TDB_CUDA_CHECK(cudaStreamSynchronize(st));
       ms_quad += elapsed(ws->ev[2], ws->ev[3]);
+      if (ws->cell.on) ms_cells += elapsed(ws->ev[6], ws->ev[7]);
       cnt[0] += c[0];
+      cnt[34] += c[34];
+      cnt[35] += c[35];
       for (int k = 40; k < 49; ++k) cnt[k] += c[k];
     }
     TDB_CUDA_CHECK(cudaEventRecord(ws->ev[4], st));
     TDB_CUDA_CHECK(cudaEventSynchronize(ws->ev[4]));
     sys->stats.ms_plan = elapsed(ws->ev[0], ws->ev[1]);  // batch plans + pattern counts
     sys->stats.ms_quad = ms_quad;
+    sys->stats.ms_quad_cells = ms_cells;
     sys->stats.ms_finalize = 0.0;
     sys->stats.ms_pattern = elapsed(ws->ev[1], ws->ev[4]) - ms_quad;
   }
@@ -1839,6 +1830,8 @@ int tdb_system_run_impl(TdbSystem* sys) {
   sys->stats.units_primary = (int64_t)cnt[48];
   sys->stats.launches = ws->launch_count;
   sys->stats.n_in = (int64_t)cnt[0];
+  sys->stats.n_in_cells = (int64_t)cnt[34];
+  sys->stats.pairs_cells = (int64_t)cnt[35];
   sys->stats.n_geom = n_geom;
   sys->stats.ms_total = elapsed(ws->ev[0], ws->ev[4]);
   return TDB_OK;
@@ -2177,7 +2170,9 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
         fit.ok = ok;
         fit.M = M_;
         fit.kappa = kap_;
-        fit.dt = dtf;
+        // the kernel's time step is the tables' (32 cells): the same bits whatever subset
+        // of the positions this system holds (lag-sharded systems bin points identically)
+        fit.dt = kCellPerDt * fd.w;
         if (std::getenv("TDB_VERBOSE"))
           std::fprintf(stderr, "tdb: family %d cell grid: ok %d spans %d kappa %d dt %.17g end/max %.3Le\n", f,
                        (int)ok, M_, kap_, dtf, vmax > 0 ? vend / vmax : 0.0L);
@@ -2589,7 +2584,7 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
                      (double)ms * NACC * 8 / 1e9, need / 1e9);
     }
   }
-  if ((rc = dalloc(&ws->items, ws->total_items))) return rc;
+  if ((rc = dalloc(&ws->items, std::max<long long>(1, ws->total_items)))) return rc;
   if ((rc = dalloc(&ws->part, (size_t)ws->total_slots * NACC))) return rc;
   // pattern sizing: counts -> scan -> nnz
   long long nnz_total = 0;

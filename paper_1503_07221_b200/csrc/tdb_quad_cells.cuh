@@ -12,7 +12,7 @@
 //     and the positions of a family are one time step apart, so a rule point at
 //     distance r sits in the same cell column j = floor(32 frac(r / dt)) at every
 //     position, one dt-span of the table support further per lag.
-//   * The pair's 256 points are sorted by column and cut into column-pure sub-runs of 4.
+//   * The pair's 256 points are sorted by column and cut into column-pure sub-runs of 5.
 //     Per dt span m of the support, every lane takes one sub-run, loads the coefficient
 //     row of its cell (m, j) into REGISTERS once and evaluates its 4 points against it
 //     (position s = floor(r / dt) + kappa - m).  Per evaluation the LSU delivers the
@@ -33,13 +33,18 @@
 constexpr int kCellWarps = 8;
 constexpr int kCellSpans = 4;   // dt spans of a table support (passes per family), max
 constexpr int kCellPerDt = 32;  // table cells per time step
-// The pair's points are sorted by cell column and cut into column-pure sub-runs of 4
-// (columns padded to a multiple of 4): at most (256 + 3 * 32) / 4 = 88 sub-runs, kept
-// transposed ([entry 0..3][sub-run], consecutive lanes read consecutive words).
-constexpr int kCellSub = 4;
-constexpr int kCellSubRuns = 96;
+// The pair's points are sorted by cell column and cut into column-pure sub-runs of
+// kCellSub (columns padded to a multiple of it): at most (256 + 5 * 32) / 6 = 69
+// sub-runs, kept transposed ([entry][sub-run], consecutive lanes read consecutive words).
+// Measured at config 4 (k_quad_cells ms): 4 -> 641, 5 -> 624, 6 -> 641, 8 -> 797: the time
+// follows the evaluation slots per lane (rounds x kCellSub: 12, 11.8, 12, 16).
+#ifndef TDB_CELL_SUB
+#define TDB_CELL_SUB 5
+#endif
+constexpr int kCellSub = TDB_CELL_SUB;
+constexpr int kCellSubRuns = (kChunk + (kCellSub - 1) * 32) / kCellSub + 1;
 // per-warp scratch: sorted r (FP64), sorted q | column << 8 | n << 13, G[span][q] = (psi, psi~), counters
-constexpr int kCellScratchBytes = kCellSub * kCellSubRuns * 12 + kCellSpans * kChunk * 16 + 32 * 4;
+constexpr int kCellScratchBytes = (kCellSub * kCellSubRuns * 12 + kCellSpans * kChunk * 16 + 32 * 4 + 15) / 16 * 16;
 static_assert(kChunk == 256, "the cell-owner kernel packs the rule point index in 8 bits");
 
 // Coefficient rows of the cell-owner launch: one 16-byte aligned record per table cell,
@@ -88,62 +93,93 @@ __device__ __forceinline__ void cell_poly(const CellRow<D>& c, double x, double&
   v1 = fma(x7, (double)tt.y, v1);
 }
 
+// Family constants of stage 1 (warp-uniform).
+struct CellFam {
+  double amin, amax, lo, inv_w2;  // inv_w2 = 2 / w
+  int abs_mask;        // |a| as a mask on the high word (fold families)
+  unsigned sp1, sn1;   // sign bit of the tables for a >= 0 / a < 0
+};
+
+// NE points of one sub-run (entries e0 .. e0 + NE - 1) against the row in `cr`.
+template <int D, int NE>
+__device__ __forceinline__ void cell_evals(const CellFam& cf, const CellRow<D>& cr, const double* __restrict__ sdel,
+                                           const double* __restrict__ s_r, const int* __restrict__ s_q,
+                                           double2* __restrict__ Gm, int u, int e0, bool live, int koff,
+                                           unsigned ucnt, int sg, unsigned& n_act) {
+  double r[NE], delta[NE];
+  int qi[NE];
+  bool valid[NE];
+#pragma unroll
+  for (int i = 0; i < NE; ++i) {
+    r[i] = s_r[(e0 + i) * kCellSubRuns + u];
+    qi[i] = live ? s_q[(e0 + i) * kCellSubRuns + u] : (int)0x80000000u;  // idle lanes: like a pad entry
+  }
+#pragma unroll
+  for (int i = 0; i < NE; ++i) {
+    const unsigned sr = (unsigned)((qi[i] >> 13) + koff);  // position relative to the pair's window
+    valid[i] = sr < ucnt;
+    delta[i] = sdel[valid[i] ? sr : 0u];
+  }
+#pragma unroll
+  for (int i = 0; i < NE; ++i) {
+    const double av = r[i] + delta[i];
+    const bool act = valid[i] && av >= cf.amin && av <= cf.amax;
+    n_act += act ? 1u : 0u;
+    const int avh = __double2hiint(av);
+    const double aa = __hiloint2double(avh & cf.abs_mask, __double2loint(av));
+    // cheb_locate's local coordinate with the sub-run's row for idx (equal to it except
+    // within roundoff of a cell edge, where the two pieces agree to 1e-16)
+    // (2 t) inv_w - 1 == fma(t, 2 inv_w, -1) bit for bit (the doubling is exact)
+    const double x = fma(aa - cf.lo - cr.roww, cf.inv_w2, -1.0);
+    double v0, v1;
+    cell_poly<D>(cr, x, v0, v1);
+    v0 = __hiloint2double(__double2hiint(v0) ^ sg, __double2loint(v0));
+    v1 = __hiloint2double(__double2hiint(v1) ^ sg, __double2loint(v1));
+    if (qi[i] >= 0) {
+      double2* g = Gm + (qi[i] & 255);
+      if (act) *g = make_double2(v0, v1);
+      else *g = make_double2(0.0, 0.0);
+    }
+  }
+}
+
 // Stage 1 of one family: per dt span m of the support, round by round every lane takes
-// one column-pure sub-run of 4 points, loads the coefficient row of its (span, column)
-// cell into registers and evaluates the 4 points against it, two at a time.
+// one column-pure sub-run of points, loads the coefficient row of its (span, column)
+// cell into registers and evaluates its points against it (independent evaluations,
+// interleaved by the compiler: the kernel runs two warps per scheduler and lives on
+// instruction-level parallelism).
 template <int D>
 __device__ __forceinline__ void cell_family(const QFam& fd, const double2* __restrict__ rows,
                                             const double* __restrict__ sdel, const double* __restrict__ s_r,
                                             const int* __restrict__ s_q, double2* __restrict__ G, int nsr,
-                                            int lane, int w_lo, unsigned ucnt, unsigned& n_act) {
-  const double amin = fd.amin, amax = fd.amax, lo = fd.lo, w = fd.w, inv_w = fd.inv_w;
+                                            int lane, int w_lo, unsigned ucnt, double dt, unsigned& n_act) {
+  CellFam cf;
+  cf.amin = fd.amin;
+  cf.amax = fd.amax;
+  cf.lo = fd.lo;
+  cf.inv_w2 = 2.0 * fd.inv_w;
+  const double w = fd.w;
   const int nsub = fd.nsub, nspan = fd.cell_M;
   const bool fold = fd.fold != 0;
-  const int abs_mask = fold ? 0x7fffffff : -1;  // |a| as a mask on the high word
-  const unsigned sp1 = (fd.sp_neg & 1u) << 31, sn1 = (fd.sn_neg & 1u) << 31;
+  cf.abs_mask = fold ? 0x7fffffff : -1;
+  cf.sp1 = (fd.sp_neg & 1u) << 31;
+  cf.sn1 = (fd.sn_neg & 1u) << 31;
   for (int m = 0; m < nspan; ++m) {
     const int koff = fd.cell_kappa - m - w_lo;
     double2* Gm = G + m * kChunk;
+    // sign of the tables on this span (a < 0 on the spans below zero; where a span meets
+    // a = 0 the two signs differ only for an odd table, which vanishes there)
+    const int sg = (int)(cf.amin + ((double)m + 0.5) * dt < 0.0 ? cf.sn1 : cf.sp1);
 #pragma unroll 1
     for (int u0 = 0; u0 < nsr; u0 += 32) {
       const bool live = u0 + lane < nsr;
       const int u = live ? u0 + lane : 0;
-      double r[kCellSub], delta[kCellSub];
-      int qi[kCellSub];
-      bool valid[kCellSub];
-#pragma unroll
-      for (int i = 0; i < kCellSub; ++i) {
-        r[i] = s_r[i * kCellSubRuns + u];
-        qi[i] = s_q[i * kCellSubRuns + u];
-      }
       CellRow<D> cr;
       {
-        const int c = m * kCellPerDt + ((qi[0] >> 8) & 31);  // cell on the a axis, from amin
+        const int c = m * kCellPerDt + ((s_q[u] >> 8) & 31);  // cell on the a axis, from amin
         cr.load(rows, fold ? (c < nsub ? nsub - 1 - c : c - nsub) : c, w);
       }
-#pragma unroll
-      for (int i = 0; i < kCellSub; ++i) {
-        const unsigned sr = (unsigned)((qi[i] >> 13) + koff);  // position relative to the pair's window
-        valid[i] = sr < ucnt;
-        delta[i] = sdel[valid[i] ? sr : 0u];
-      }
-#pragma unroll
-      for (int i = 0; i < kCellSub; ++i) {
-        const double av = r[i] + delta[i];
-        const bool act = valid[i] && av >= amin && av <= amax;
-        n_act += (act && live) ? 1u : 0u;
-        const int avh = __double2hiint(av);
-        const double aa = __hiloint2double(avh & abs_mask, __double2loint(av));
-        // cheb_locate's local coordinate with the sub-run's row for idx (equal to it except
-        // within roundoff of a cell edge, where the two pieces agree to 1e-16)
-        const double x = 2.0 * (aa - lo - cr.roww) * inv_w - 1.0;
-        double v0, v1;
-        cell_poly<D>(cr, x, v0, v1);
-        const int sg = (int)(avh < 0 ? sn1 : sp1);
-        v0 = __hiloint2double(__double2hiint(v0) ^ sg, __double2loint(v0));
-        v1 = __hiloint2double(__double2hiint(v1) ^ sg, __double2loint(v1));
-        if (live && qi[i] >= 0) Gm[qi[i] & 255] = act ? make_double2(v0, v1) : make_double2(0.0, 0.0);
-      }
+      cell_evals<D, kCellSub>(cf, cr, sdel, s_r, s_q, Gm, u, 0, live, koff, ucnt, sg, n_act);
     }
   }
 }
@@ -175,7 +211,7 @@ __global__ void __launch_bounds__(kCellWarps * 32, 1) k_quad_cells(QuadArgs a) {
   const unsigned E = (unsigned)a.E;
   const long long E2 = a.npair;
   const double inv_dt = a.inv_dt;
-  unsigned long long my_in = 0;
+  unsigned long long my_in = 0, my_pairs = 0;
 
   // pair index two ahead, pair header (corners, plan entries) one ahead of the work
   struct Header {
@@ -220,6 +256,7 @@ __global__ void __launch_bounds__(kCellWarps * 32, 1) k_quad_cells(QuadArgs a) {
     P1 = grab();
     if (cur.units == 0 || cur.cs != 0) continue;
     if (__ballot_sync(FULL, (cur.fr.lo_cnt >> 16) != 0) == 0u) continue;
+    my_pairs += lane == 0 ? 1ULL : 0ULL;
     V3 X0, X1, X2, Y0, Y1, Y2;
     X0.x = __shfl_sync(FULL, cur.d, 0); X0.y = __shfl_sync(FULL, cur.d, 1); X0.z = __shfl_sync(FULL, cur.d, 2);
     X1.x = __shfl_sync(FULL, cur.d, 3); X1.y = __shfl_sync(FULL, cur.d, 4); X1.z = __shfl_sync(FULL, cur.d, 5);
@@ -253,7 +290,7 @@ __global__ void __launch_bounds__(kCellWarps * 32, 1) k_quad_cells(QuadArgs a) {
     }
     __syncwarp();
     int nsr;  // sub-runs of the pair
-    {  // columns -> column-pure sub-runs of 4 (the order inside a column is free: stage 1
+    {  // columns -> column-pure sub-runs (the order inside a column is free: stage 1
        // stores by rule point, stage 2 sums in rule-point order)
       const int cnt = (int)bins[lane];
       const int mine_sr = (cnt + kCellSub - 1) / kCellSub;
@@ -269,13 +306,13 @@ __global__ void __launch_bounds__(kCellWarps * 32, 1) k_quad_cells(QuadArgs a) {
       bins[lane] = (unsigned)first;
       for (int p = cnt; p < mine_sr * kCellSub; ++p) {  // pads of the column's last sub-run
         const int slot = first + p;
-        s_q[(slot & 3) * kCellSubRuns + (slot >> 2)] = (int)0x80000000u | (lane << 8);
+        s_q[(slot % kCellSub) * kCellSubRuns + slot / kCellSub] = (int)0x80000000u | (lane << 8);
       }
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < kNK; ++k) {
         const int slot = (int)atomicAdd(bins + (nj[k] & 31), 1u);
-        const int at = (slot & 3) * kCellSubRuns + (slot >> 2);
+        const int at = (slot % kCellSub) * kCellSubRuns + slot / kCellSub;
         s_r[at] = rk[k];
         s_q[at] = (nj[k] << 8) | (lane + 32 * k);
       }
@@ -293,11 +330,11 @@ __global__ void __launch_bounds__(kCellWarps * 32, 1) k_quad_cells(QuadArgs a) {
       const double* sdel = sdelta + fd.delta_off + s_lo;
       unsigned n_act = 0;
       if (fd.deg == 12)
-        cell_family<12>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, n_act);
+        cell_family<12>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, a.dt, n_act);
       else if (fd.deg == 14)
-        cell_family<14>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, n_act);
+        cell_family<14>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, a.dt, n_act);
       else
-        cell_family<16>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, n_act);
+        cell_family<16>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, a.dt, n_act);
       my_in += n_act;
       __syncwarp();
 
@@ -315,41 +352,73 @@ __global__ void __launch_bounds__(kCellWarps * 32, 1) k_quad_cells(QuadArgs a) {
       const unsigned nspan = (unsigned)fd.cell_M;
       double* dst = a.part + (cur.base + fr.foff) * NACC;
       const double2* Gq = G + lane;
-      for (int si = 0; si < ucnt; si += 2) {
-        double tb[2][4];
+      // Four units per step.  Register set u of a lane holds unit si + (u ^ h), h = lane
+      // bits 4-3: the first two levels of the warp sum exchange whole sets (no selects),
+      // after them the 8 lanes sharing h hold the 10 partial values of unit si + h.
+      const int h = (lane >> 3) & 3;
+      for (int si = 0; si < ucnt; si += 4) {
+        double tb[4][4];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) tb[u][0] = tb[u][1] = tb[u][2] = tb[u][3] = 0.0;
+        for (int u = 0; u < 4; ++u) tb[u][0] = tb[u][1] = tb[u][2] = tb[u][3] = 0.0;
 #pragma unroll
         for (int k = 0; k < kNK; ++k) {
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const unsigned m = (unsigned)(mk[k] - si - u);
+          for (int u = 0; u < 4; ++u) {
+            const int unit = si + (u ^ h);
+            const unsigned m = (unsigned)(mk[k] - unit);
             double2 g = make_double2(0.0, 0.0);
-            if (m < nspan) g = Gq[m * kChunk + 32 * k];
+            if (m < nspan && unit < ucnt) g = Gq[m * kChunk + 32 * k];
             tb[u][0] = fma(g.x, cx[k][0], tb[u][0]);
             tb[u][1] = fma(g.x, cx[k][1], tb[u][1]);
             tb[u][2] = fma(g.x, cx[k][2], tb[u][2]);
             tb[u][3] = fma(g.y, ck[k], tb[u][3]);
           }
         }
+        double acc[4][NACC];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          if (si + u >= ucnt) break;  // warp-uniform
-          double acc[NACC];
-          acc[0] = shy0 * tb[u][0];
-          acc[1] = shy0 * tb[u][1];
-          acc[2] = shy0 * tb[u][2];
-          acc[3] = shy1 * tb[u][0];
-          acc[4] = shy1 * tb[u][1];
-          acc[5] = shy1 * tb[u][2];
-          acc[6] = shy2 * tb[u][0];
-          acc[7] = shy2 * tb[u][1];
-          acc[8] = shy2 * tb[u][2];
-          acc[9] = tb[u][3];
-          double outv[RS<NACC>::H5];
-          int base, valid;
-          warp_reduce_scatter<NACC>(acc, lane, outv, base, valid);
-          if (valid > 0) dst[(long long)(si + u) * NACC + base] = outv[0];
+        for (int u = 0; u < 4; ++u) {
+          // explicitly rounded products: a product fused into the first exchange's add
+          // would make the sum depend on which lane of a pair keeps the unit
+          acc[u][0] = __dmul_rn(shy0, tb[u][0]);
+          acc[u][1] = __dmul_rn(shy0, tb[u][1]);
+          acc[u][2] = __dmul_rn(shy0, tb[u][2]);
+          acc[u][3] = __dmul_rn(shy1, tb[u][0]);
+          acc[u][4] = __dmul_rn(shy1, tb[u][1]);
+          acc[u][5] = __dmul_rn(shy1, tb[u][2]);
+          acc[u][6] = __dmul_rn(shy2, tb[u][0]);
+          acc[u][7] = __dmul_rn(shy2, tb[u][1]);
+          acc[u][8] = __dmul_rn(shy2, tb[u][2]);
+          acc[u][9] = tb[u][3];
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int i = 0; i < NACC; ++i) acc[u][i] += __shfl_xor_sync(FULL, acc[u ^ 2][i], 16);
+#pragma unroll
+        for (int i = 0; i < NACC; ++i) acc[0][i] += __shfl_xor_sync(FULL, acc[1][i], 8);
+        // the 8 lanes of a group: reduce-scatter of the 10 values (5, 3, 2 per level)
+        double w1[5], w2[3], w3[2];
+        rs_level<NACC, 4>(acc[0], w1, lane & 4);
+        rs_level<5, 2>(w1, w2, lane & 2);
+        rs_level<3, 1>(w2, w3, lane & 1);
+        int base = 0, n = NACC;
+        {
+          const int H[3] = {5, 3, 2};
+#pragma unroll
+          for (int l = 0; l < 3; ++l) {
+            const bool hi = (lane >> (2 - l)) & 1;
+            if (hi) {
+              base += H[l];
+              n = n > H[l] ? n - H[l] : 0;
+            } else {
+              n = n < H[l] ? n : H[l];
+            }
+          }
+        }
+        const int unit = si + h;
+        if (unit < ucnt) {
+          if (n > 0) dst[(long long)unit * NACC + base] = w3[0];
+          if (n > 1) dst[(long long)unit * NACC + base + 1] = w3[1];
         }
       }
       __syncwarp();
@@ -357,5 +426,9 @@ __global__ void __launch_bounds__(kCellWarps * 32, 1) k_quad_cells(QuadArgs a) {
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) my_in += __shfl_xor_sync(FULL, my_in, o);
-  if (lane == 0) atomicAdd(a.n_in, my_in);
+  if (lane == 0) {
+    atomicAdd(a.n_in, my_in);
+    atomicAdd(a.n_in + 34, my_in);  // this kernel's share (TdbStats::n_in_cells)
+    atomicAdd(a.n_in + 35, my_pairs);
+  }
 }

@@ -414,3 +414,33 @@ def test_position_batches_bitwise(G, cfg1_mesh, monkeypatch):
     A2._dev.rerun()  # re-run from the resident inputs, still identical
     for f in range(A1._dev.num_families):
         assert np.array_equal(A1._dev.family_arrays(f)[2], A2._dev.family_arrays(f)[2])
+
+
+def test_cell_owner_kernel_matches_k_quad(G, cfg1_mesh, monkeypatch):
+    # the regular pairs of the dt-grid families run on k_quad_cells (csrc/tdb_quad_cells.cuh),
+    # the singular cases and the singleton families on k_quad; TDB_CELLS=0 (read at system
+    # creation) keeps everything on k_quad.  Same rule points, tables and arithmetic per
+    # evaluation, different summation order: the blocks agree to roundoff.
+    from paper_1503_07221_b200.temporal_basis import TimeGrid
+
+    grid = TimeGrid(T=3.9, N=40, p=0)
+    A1 = G[2].assemble_system(cfg1_mesh, grid)
+    monkeypatch.setenv("TDB_CELLS", "0")
+    A0 = G[2].assemble_system(cfg1_mesh, grid)
+    monkeypatch.delenv("TDB_CELLS")
+    s1, s0 = A1.stats(), A0.stats()
+    assert s1["pairs_cells"] > 0 and s1["n_in_cells"] > 0 and s1["ms_quad_cells"] > 0.0
+    assert s0["pairs_cells"] == 0 and s0["n_in_cells"] == 0
+    # every in-support (unit, point) evaluation is done exactly once by one of the kernels
+    assert s1["units"] == s0["units"] and s1["n_in"] == s0["n_in"]
+    assert 0 < s1["items"] < s0["items"]  # no k_quad work item for a fully covered regular pair
+    assert A1._dev.position_units() == A0._dev.position_units()
+    for f in range(A1._dev.num_families):
+        p1, i1, d1 = A1._dev.family_arrays(f)
+        p0, i0, d0 = A0._dev.family_arrays(f)
+        assert np.array_equal(p1, p0) and np.array_equal(i1, i0)
+        assert np.all(np.isfinite(d1))
+        assert np.abs(d1 - d0).max() <= 1e-13 * np.abs(d0).max()
+    # p = 1 tables are off the kernel's grid: everything stays on k_quad
+    A2 = G[2].assemble_system(cfg1_mesh, TimeGrid(T=1.0, N=5, p=1))
+    assert A2.stats()["pairs_cells"] == 0

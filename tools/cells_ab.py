@@ -63,7 +63,7 @@ def main():
             err = np.abs(da - db).max() / scale
             print(f"family {f}: nnz {da.size} max|diff|/max|a| {err:.3e} nan {int(np.isnan(da).sum())}")
             worst = max(worst, err)
-        keys = ("ms_plan", "ms_quad", "ms_finalize", "ms_pattern", "ms_total", "n_in", "units")
+        keys = ("ms_plan", "ms_quad", "ms_quad_cells", "n_in_cells", "pairs_cells", "ms_finalize", "ms_pattern", "ms_total", "n_in", "units")
         print("cells  ", {k: s1[k] for k in keys})
         print("k_quad ", {k: s0[k] for k in keys})
         print("worst", worst)
