@@ -303,6 +303,86 @@ __global__ void __launch_bounds__(kBandMaxWarps * 32) k_band_mv(BandMvArgs a) {
     if (t0 + u < a.nT) *reinterpret_cast<double2*>(yp + 8 * u) = make_double2(acc[u][0], acc[u][1]);
 }
 
+// Short plans (at most 6 time tiles, e.g. the 40-row ranges of the recursive
+// preconditioner): one warp = (row block J, part) covers every time tile, so each
+// record is read once by one warp, straight from global memory (coalesced 256-byte A
+// fragment + broadcast header), four records in flight per warp, no shared-memory ring
+// and no barriers.  Same DMMA sequence per accumulator as k_band_mv<TT> with W = 1.
+#ifndef TDB_DIRECT_UNROLL
+#define TDB_DIRECT_UNROLL 3
+#endif
+constexpr int kDirectWarps = 4;   // independent warps per CTA
+constexpr int kDirectUnroll = TDB_DIRECT_UNROLL;  // records per step (the next step's are prefetched)
+template <int TT>
+__global__ void __launch_bounds__(kDirectWarps * 32) k_band_direct(BandMvArgs a) {
+  const int lane = threadIdx.x & 31;
+  const long long unit = (long long)blockIdx.x * kDirectWarps + (threadIdx.x >> 5);
+  if (unit >= (long long)a.nRB * a.P) return;
+  const int J = (int)(unit / a.P), part = (int)(unit % a.P);
+  const long long r0 = __ldg(a.rbptr + J), r1 = __ldg(a.rbptr + J + 1);
+  const long long q0 = r0 + (r1 - r0) * part / a.P, q1 = r0 + (r1 - r0) * (part + 1) / a.P;
+  const int g = lane >> 2, k = lane & 3;
+  double acc[TT][2];
+#pragma unroll
+  for (int u = 0; u < TT; ++u) acc[u][0] = acc[u][1] = 0.0;
+  const double* xl = a.xt + (a.off0 - k + g);
+  // software pipeline: the next batch's headers and A fragments are in flight during this
+  // batch's B loads and DMMAs
+  int4 hn[kDirectUnroll];
+  double an[kDirectUnroll];
+  auto fetch = [&](long long i) {
+#pragma unroll
+    for (int v = 0; v < kDirectUnroll; ++v) {
+      const BandTile* T = a.tiles + (i + v < q1 ? i + v : q1 - 1);
+      hn[v] = __ldg(reinterpret_cast<const int4*>(&T->l));
+      an[v] = __ldg(&T->v[lane]);
+    }
+  };
+  if (q0 < q1) fetch(q0);
+  for (long long i = q0; i < q1; i += kDirectUnroll) {
+    int lo[kDirectUnroll], hi[kDirectUnroll];
+    double av[kDirectUnroll], b[kDirectUnroll][TT];
+#pragma unroll
+    for (int v = 0; v < kDirectUnroll; ++v) {
+      const int4 h = hn[v];
+      lo[v] = h.z & 0xff;
+      hi[v] = i + v < q1 ? (h.z >> 8) : -1;
+      av[v] = an[v];
+      const double* x = xl + (long long)h.x * a.xs - h.y;
+#pragma unroll
+      for (int u = 0; u < TT; ++u) b[v][u] = __ldg(x + 8 * u);
+      // the light-cone tie lag: only the block rows of its logical mask (per lane / row)
+      if (a.s_irr >= h.y && a.s_irr < h.y + 4) {  // warp-uniform
+        if (k == a.s_irr - h.y) {
+#pragma unroll
+          for (int u = 0; u < TT; ++u) {
+            const int r = 8 * u + g;
+            if (!((a.irr_mask[r >> 5] >> (r & 31)) & 1u)) b[v][u] = 0.0;
+          }
+        }
+      }
+    }
+    if (i + kDirectUnroll < q1) fetch(i + kDirectUnroll);
+#pragma unroll
+    for (int v = 0; v < kDirectUnroll; ++v)
+#pragma unroll
+      for (int u = 0; u < TT; ++u)
+        if (u >= lo[v] && u <= hi[v]) dmma884(acc[u][0], acc[u][1], av[v], b[v][u]);
+  }
+  double* yp = a.ypart + ((long long)part * a.nRB * 8 + 8LL * J + g) * a.ldy + 2 * k;
+#pragma unroll
+  for (int u = 0; u < TT; ++u)
+    if (u < a.nT) *reinterpret_cast<double2*>(yp + 8 * u) = make_double2(acc[u][0], acc[u][1]);
+}
+
+template <int TT>
+int launch_direct(const BandMvArgs& a, cudaStream_t st) {
+  const long long units = (long long)a.nRB * a.P;
+  k_band_direct<TT><<<(unsigned)((units + kDirectWarps - 1) / kDirectWarps), kDirectWarps * 32, 0, st>>>(a);
+  TDB_CUDA_CHECK(cudaGetLastError());
+  return TDB_OK;
+}
+
 // y[(kt - rlo) nrows + j] += sum over parts (in part order) for kt in the band rows
 __global__ void k_band_reduce(BandMvArgs a) {
   const long long total = (long long)a.nrows * a.nkt;
@@ -513,6 +593,16 @@ int band_view(TdbSystem* sys, int f, const std::vector<unsigned>& act, int dt0, 
 }
 
 int band_mv_tiles(const BandMvArgs& a, cudaStream_t st) {
+  if (a.direct) {  // W == 1, TT == nT <= 6
+    switch (a.TT) {
+      case 1: return launch_direct<1>(a, st);
+      case 2: return launch_direct<2>(a, st);
+      case 3: return launch_direct<3>(a, st);
+      case 4: return launch_direct<4>(a, st);
+      case 5: return launch_direct<5>(a, st);
+      default: return launch_direct<6>(a, st);
+    }
+  }
   switch (a.TT) {
     case 1: return launch_tt<1>(a, st);
     case 2: return launch_tt<2>(a, st);

@@ -19,6 +19,7 @@ struct BandMvArgs {
   int nRB, P, nT, TT, W;  // row blocks, parts per row block, 8-step time tiles, tiles per warp, warps per CTA
   int nrows, act_words;   // owned rows, words of the active-position bit set
   int chunk;              // tile records per pipeline stage
+  int direct;             // short plan: k_band_direct (one warp per (row block, part), no smem ring)
   int ktlo, nkt, rlo;     // band rows kt in [ktlo, ktlo + nkt); y row index kt - rlo
   int off0, xs;           // xt column of (kt = ktlo, lag d_0) and row stride
   int dt0, dt1;           // itlo + d_0 - ktlo, ithi + d_0 - ktlo: valid rows of lag d_0 + s are

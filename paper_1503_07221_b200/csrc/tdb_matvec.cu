@@ -843,8 +843,15 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
     const char* e = std::getenv("TDB_BAND_TT");
     return e ? std::max(1, std::min(6, std::atoi(e))) : 0;
   }();
+  // short plans (<= 6 time tiles): one warp covers every time tile and reads its records
+  // straight from global memory (k_band_direct); TDB_BAND_DIRECT=0 keeps the ring kernel
+  static const bool direct_env = [] {
+    const char* e = std::getenv("TDB_BAND_DIRECT");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const bool direct = direct_env && nT <= 6 && !tt_env;
   const int tt_target = tt_env ? tt_env : (nT <= 6 ? 3 : 5);
-  const int W = std::max(1, std::min(kBandMaxWarps, (nT + tt_target - 1) / tt_target));
+  const int W = direct ? 1 : std::max(1, std::min(kBandMaxWarps, (nT + tt_target - 1) / tt_target));
   const int TT = (nT + W - 1) / W;
   if (TT > 6) {  // more than 384 block rows: not instantiated
     tdb_matvec_plan_destroy(p);
@@ -868,9 +875,17 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   const int band_ctas = band_ctas_env ? band_ctas_env
                                       : std::max(1, std::min(16, (int)((200 * 1024) / band_smem_bytes((npos + 31) / 32 + 1, chunk))));
   // one wave: nRB * P <= SMs x resident CTAs (a partial second wave is a pure tail)
-  const int P = (int)std::max<long long>(
-      1, std::min<long long>({64LL, ((long long)sys->ctx->num_sms * band_ctas) / std::max(1, nRB),
-                              tiles_per_rb / (2 * chunk)}));
+  // (direct plans: ~32 warps per SM, at least 16 records per warp)
+  static const int direct_wps = [] {  // direct plans: warps per SM the parts are sized for
+    const char* e = std::getenv("TDB_BAND_DIRECT_WPS");
+    return e ? std::max(1, std::atoi(e)) : 48;  // config 4 quarter range: 16 -> 0.320, 32 -> 0.285, 48 -> 0.280 ms
+  }();
+  const int P = direct ? (int)std::max<long long>(
+                             1, std::min<long long>({64LL, ((long long)sys->ctx->num_sms * direct_wps) / std::max(1, nRB),
+                                                     tiles_per_rb / 16}))
+                       : (int)std::max<long long>(
+                             1, std::min<long long>({64LL, ((long long)sys->ctx->num_sms * band_ctas) / std::max(1, nRB),
+                                                     tiles_per_rb / (2 * chunk)}));
   const int ldy = 8 * W * TT;
   cudaStream_t st = sys->ctx->stream;
   const size_t xt_n = (size_t)V * xs;
@@ -901,6 +916,7 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   ba.nrows = sys->nrows;
   ba.act_words = act_words;
   ba.chunk = chunk;
+  ba.direct = direct ? 1 : 0;
   ba.ktlo = ktlo;
   ba.nkt = nkt;
   ba.rlo = d->rlo;

@@ -153,7 +153,8 @@ template <int D>
 __device__ __forceinline__ void cell_family(const QFam& fd, const double2* __restrict__ rows,
                                             const double* __restrict__ sdel, const double* __restrict__ s_r,
                                             const int* __restrict__ s_q, double2* __restrict__ G, int nsr,
-                                            int lane, int w_lo, unsigned ucnt, double dt, unsigned& n_act) {
+                                            int lane, int w_lo, unsigned ucnt, double dt, int n_min, int n_max,
+                                            unsigned& n_act) {
   CellFam cf;
   cf.amin = fd.amin;
   cf.amax = fd.amax;
@@ -167,6 +168,9 @@ __device__ __forceinline__ void cell_family(const QFam& fd, const double2* __res
   cf.sn1 = (fd.sn_neg & 1u) << 31;
   for (int m = 0; m < nspan; ++m) {
     const int koff = fd.cell_kappa - m - w_lo;
+    // no point of the pair has its span-m position inside the window (position batches,
+    // lag-sharded systems): nothing of this span is read by stage 2
+    if (n_max + koff < 0 || n_min + koff >= (int)ucnt) continue;
     double2* Gm = G + m * kChunk;
     // sign of the tables on this span (a < 0 on the spans below zero; where a span meets
     // a = 0 the two signs differ only for an odd table, which vanishes there)
@@ -290,6 +294,17 @@ __global__ void __launch_bounds__(kCellWarps * 32, 1) k_quad_cells(QuadArgs a) {
       atomicAdd(bins + j, 1u);
     }
     __syncwarp();
+    int n_min = nj[0] >> 5, n_max = n_min;  // time-step range of the pair's points
+#pragma unroll
+    for (int k = 1; k < kNK; ++k) {
+      n_min = min(n_min, nj[k] >> 5);
+      n_max = max(n_max, nj[k] >> 5);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      n_min = min(n_min, __shfl_xor_sync(FULL, n_min, o));
+      n_max = max(n_max, __shfl_xor_sync(FULL, n_max, o));
+    }
     int nsr;  // sub-runs of the pair
     {  // columns -> column-pure sub-runs (the order inside a column is free: stage 1
        // stores by rule point, stage 2 sums in rule-point order)
@@ -331,11 +346,11 @@ __global__ void __launch_bounds__(kCellWarps * 32, 1) k_quad_cells(QuadArgs a) {
       const double* sdel = sdelta + fd.delta_off + s_lo;
       unsigned n_act = 0;
       if (fd.deg == 12)
-        cell_family<12>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, a.dt, n_act);
+        cell_family<12>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, a.dt, n_min, n_max, n_act);
       else if (fd.deg == 14)
-        cell_family<14>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, a.dt, n_act);
+        cell_family<14>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, a.dt, n_min, n_max, n_act);
       else
-        cell_family<16>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, a.dt, n_act);
+        cell_family<16>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, a.dt, n_min, n_max, n_act);
       my_in += n_act;
       __syncwarp();
 
