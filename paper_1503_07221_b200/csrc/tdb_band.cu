@@ -303,20 +303,22 @@ __global__ void __launch_bounds__(kBandMaxWarps * 32) k_band_mv(BandMvArgs a) {
     if (t0 + u < a.nT) *reinterpret_cast<double2*>(yp + 8 * u) = make_double2(acc[u][0], acc[u][1]);
 }
 
-// Short plans (at most 6 time tiles, e.g. the 40-row ranges of the recursive
-// preconditioner): one warp = (row block J, part) covers every time tile, so each
-// record is read once by one warp, straight from global memory (coalesced 256-byte A
-// fragment + broadcast header), four records in flight per warp, no shared-memory ring
-// and no barriers.  Same DMMA sequence per accumulator as k_band_mv<TT> with W = 1.
+// Direct variant: a unit = (row block J, part) is W adjacent warps, each covering TT of
+// the time tiles; every warp reads the unit's records straight from global memory
+// (coalesced 256-byte A fragment + broadcast header; the other warps of the unit hit
+// L1), the next step's records prefetched during this step's B loads and DMMAs.  No
+// shared-memory ring, no barriers.  Same DMMA sequence per accumulator as k_band_mv<TT>.
 #ifndef TDB_DIRECT_UNROLL
 #define TDB_DIRECT_UNROLL 3
 #endif
-constexpr int kDirectWarps = 4;   // independent warps per CTA
+constexpr int kDirectWarps = 8;   // warps per CTA: 8 / W units of W warps (W = 1, 2, 4, 8 time groups)
 constexpr int kDirectUnroll = TDB_DIRECT_UNROLL;  // records per step (the next step's are prefetched)
 template <int TT>
 __global__ void __launch_bounds__(kDirectWarps * 32) k_band_direct(BandMvArgs a) {
-  const int lane = threadIdx.x & 31;
-  const long long unit = (long long)blockIdx.x * kDirectWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // the W warps of a unit (adjacent in the CTA) read the same records (L1) for their own time tiles
+  const long long unit = (long long)blockIdx.x * (kDirectWarps / a.W) + wid / a.W;
+  const int t0 = (wid % a.W) * TT;
   if (unit >= (long long)a.nRB * a.P) return;
   const int J = (int)(unit / a.P), part = (int)(unit % a.P);
   const long long r0 = __ldg(a.rbptr + J), r1 = __ldg(a.rbptr + J + 1);
@@ -325,7 +327,7 @@ __global__ void __launch_bounds__(kDirectWarps * 32) k_band_direct(BandMvArgs a)
   double acc[TT][2];
 #pragma unroll
   for (int u = 0; u < TT; ++u) acc[u][0] = acc[u][1] = 0.0;
-  const double* xl = a.xt + (a.off0 - k + g);
+  const double* xl = a.xt + (a.off0 - k + g + 8 * t0);
   // software pipeline: the next batch's headers and A fragments are in flight during this
   // batch's B loads and DMMAs
   int4 hn[kDirectUnroll];
@@ -345,8 +347,8 @@ __global__ void __launch_bounds__(kDirectWarps * 32) k_band_direct(BandMvArgs a)
 #pragma unroll
     for (int v = 0; v < kDirectUnroll; ++v) {
       const int4 h = hn[v];
-      lo[v] = h.z & 0xff;
-      hi[v] = i + v < q1 ? (h.z >> 8) : -1;
+      lo[v] = (h.z & 0xff) - t0;
+      hi[v] = i + v < q1 ? (h.z >> 8) - t0 : -1;
       av[v] = an[v];
       const double* x = xl + (long long)h.x * a.xs - h.y;
 #pragma unroll
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(kDirectWarps * 32) k_band_direct(BandMvArgs a)
         if (k == a.s_irr - h.y) {
 #pragma unroll
           for (int u = 0; u < TT; ++u) {
-            const int r = 8 * u + g;
+            const int r = 8 * (t0 + u) + g;
             if (!((a.irr_mask[r >> 5] >> (r & 31)) & 1u)) b[v][u] = 0.0;
           }
         }
@@ -369,16 +371,16 @@ __global__ void __launch_bounds__(kDirectWarps * 32) k_band_direct(BandMvArgs a)
       for (int u = 0; u < TT; ++u)
         if (u >= lo[v] && u <= hi[v]) dmma884(acc[u][0], acc[u][1], av[v], b[v][u]);
   }
-  double* yp = a.ypart + ((long long)part * a.nRB * 8 + 8LL * J + g) * a.ldy + 2 * k;
+  double* yp = a.ypart + ((long long)part * a.nRB * 8 + 8LL * J + g) * a.ldy + 8 * t0 + 2 * k;
 #pragma unroll
   for (int u = 0; u < TT; ++u)
-    if (u < a.nT) *reinterpret_cast<double2*>(yp + 8 * u) = make_double2(acc[u][0], acc[u][1]);
+    if (t0 + u < a.nT) *reinterpret_cast<double2*>(yp + 8 * u) = make_double2(acc[u][0], acc[u][1]);
 }
 
 template <int TT>
 int launch_direct(const BandMvArgs& a, cudaStream_t st) {
-  const long long units = (long long)a.nRB * a.P;
-  k_band_direct<TT><<<(unsigned)((units + kDirectWarps - 1) / kDirectWarps), kDirectWarps * 32, 0, st>>>(a);
+  const long long units = (long long)a.nRB * a.P, per_cta = kDirectWarps / a.W;
+  k_band_direct<TT><<<(unsigned)((units + per_cta - 1) / per_cta), kDirectWarps * 32, 0, st>>>(a);
   TDB_CUDA_CHECK(cudaGetLastError());
   return TDB_OK;
 }
@@ -593,7 +595,7 @@ int band_view(TdbSystem* sys, int f, const std::vector<unsigned>& act, int dt0, 
 }
 
 int band_mv_tiles(const BandMvArgs& a, cudaStream_t st) {
-  if (a.direct) {  // W == 1, TT == nT <= 6
+  if (a.direct) {  // W in {1, 2, 4, 8}, TT <= 6
     switch (a.TT) {
       case 1: return launch_direct<1>(a, st);
       case 2: return launch_direct<2>(a, st);

@@ -849,9 +849,17 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
     const char* e = std::getenv("TDB_BAND_DIRECT");
     return !(e && std::atoi(e) == 0);
   }();
-  const bool direct = direct_env && nT <= 6 && !tt_env;
+  static const int direct_max_nt = [] {  // direct kernel up to this many time tiles (0: never)
+    const char* e = std::getenv("TDB_BAND_DIRECT_NT");
+    // config 4: longer plans are faster on the ring kernel (half range 1.09 vs 1.29 ms,
+    // full 2.42 vs 3.05 ms); the short ones on the direct kernel (quarter 0.28 vs 0.33 ms)
+    return e ? std::atoi(e) : 6;
+  }();
+  const bool direct = direct_env && nT <= direct_max_nt && nT <= 48 && !tt_env;
   const int tt_target = tt_env ? tt_env : (nT <= 6 ? 3 : 5);
-  const int W = direct ? 1 : std::max(1, std::min(kBandMaxWarps, (nT + tt_target - 1) / tt_target));
+  // direct units: the fewest warps (1, 2, 4, 8) with at most 6 time tiles each
+  const int Wd = nT <= 6 ? 1 : (nT <= 12 ? 2 : (nT <= 24 ? 4 : 8));
+  const int W = direct ? Wd : std::max(1, std::min(kBandMaxWarps, (nT + tt_target - 1) / tt_target));
   const int TT = (nT + W - 1) / W;
   if (TT > 6) {  // more than 384 block rows: not instantiated
     tdb_matvec_plan_destroy(p);
@@ -881,7 +889,7 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
     return e ? std::max(1, std::atoi(e)) : 48;  // config 4 quarter range: 16 -> 0.320, 32 -> 0.285, 48 -> 0.280 ms
   }();
   const int P = direct ? (int)std::max<long long>(
-                             1, std::min<long long>({64LL, ((long long)sys->ctx->num_sms * direct_wps) / std::max(1, nRB),
+                             1, std::min<long long>({64LL, ((long long)sys->ctx->num_sms * direct_wps) / std::max(1, nRB * W),
                                                      tiles_per_rb / 16}))
                        : (int)std::max<long long>(
                              1, std::min<long long>({64LL, ((long long)sys->ctx->num_sms * band_ctas) / std::max(1, nRB),
