@@ -374,6 +374,13 @@ def test_tiled_vs_csr_only_plan_agree(G, cfg1_mesh, tmp_path):
     yc = np.load(tmp_path / "y.npy")
     assert np.linalg.norm(ys[0] - yc[0]) <= 1e-13 * np.linalg.norm(yc[0])
     assert np.linalg.norm(ys[1] - yc[1][: 20 * M]) <= 1e-13 * np.linalg.norm(yc[1][: 20 * M])
+    # these 40-row plans run on k_band_direct (<= 6 time tiles); TDB_BAND_DIRECT=0 puts them
+    # on the shared-memory ring kernel k_band_mv: same records, same DMMA order per part
+    code2 = code.replace("tiled_terms == 0", "tiled_terms > 0")
+    subprocess.run([sys.executable, "-c", code2], check=True, env=dict(os.environ, TDB_BAND_DIRECT="0"), cwd=root)
+    yr = np.load(tmp_path / "y.npy")
+    assert np.linalg.norm(ys[0] - yr[0]) <= 1e-13 * np.linalg.norm(yr[0])
+    assert np.linalg.norm(ys[1] - yr[1][: 20 * M]) <= 1e-13 * np.linalg.norm(yr[1][: 20 * M])
 
 
 def test_matvec_long_time_axis_row_chunks(G, ico):
