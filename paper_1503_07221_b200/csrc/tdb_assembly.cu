@@ -2339,7 +2339,11 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
       if (CL.on && std::fabs(fit.dt - CL.dt) > 1e-12 * CL.dt) continue;
       QFam q = L0.qfam[fi];
       // one record per cell: 7 (psi, psi~) FP64 head pairs, D - 6 FP32 tail pairs, pad
-      const int rw = cell_row_words(q.deg), ntail = q.deg - 6, trow = tail_row_f2(q.deg, 7, 2);
+      // every grid family runs the degree-16 instantiation (missing tail coefficients are
+      // zeros: the same values bit for bit, one stage-1 loop body in the instruction cache)
+      const int ntail = q.deg - 6, trow = tail_row_f2(q.deg, 7, 2);
+      q.deg = 16;
+      const int rw = cell_row_words(q.deg);
       const size_t need = (cb.size() + (size_t)rw * 2 * q.nsub) * 8 +
                           (size_t)(CL.delta_doubles + sys->fam[f].npos + 2) * 8 + fixed;
       if (need > (size_t)max_smem) continue;

@@ -345,12 +345,8 @@ __global__ void __launch_bounds__(kCellWarps * 32, 1) k_quad_cells(QuadArgs a) {
       const double2* rows = reinterpret_cast<const double2*>(sblob + fd.coeff_off);
       const double* sdel = sdelta + fd.delta_off + s_lo;
       unsigned n_act = 0;
-      if (fd.deg == 12)
-        cell_family<12>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, a.dt, n_min, n_max, n_act);
-      else if (fd.deg == 14)
-        cell_family<14>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, a.dt, n_min, n_max, n_act);
-      else
-        cell_family<16>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, a.dt, n_min, n_max, n_act);
+      // (every grid family is stored with degree-16 rows: one loop body in the instruction cache)
+      cell_family<16>(fd, rows, sdel, s_r, s_q, G, nsr, lane, s_lo, (unsigned)ucnt, a.dt, n_min, n_max, n_act);
       my_in += n_act;
       __syncwarp();
 
