@@ -858,7 +858,12 @@ extern "C" int tdb_matvec_plan_create(TdbSystem* sys, const TdbMatvecDesc* d, Td
   const bool direct = direct_env && nT <= direct_max_nt && nT <= 48 && !tt_env;
   const int tt_target = tt_env ? tt_env : (nT <= 6 ? 3 : 5);
   // direct units: the fewest warps (1, 2, 4, 8) with at most 6 time tiles each
-  const int Wd = nT <= 6 ? 1 : (nT <= 12 ? 2 : (nT <= 24 ? 4 : 8));
+  static const int direct_tt = [] {  // most time tiles per direct warp
+    const char* e = std::getenv("TDB_BAND_DIRECT_TT");
+    return e ? std::max(1, std::min(6, std::atoi(e))) : 6;
+  }();
+  int Wd = 1;
+  while (Wd < 8 && (nT + Wd - 1) / Wd > direct_tt) Wd *= 2;
   const int W = direct ? Wd : std::max(1, std::min(kBandMaxWarps, (nT + tt_target - 1) / tt_target));
   const int TT = (nT + W - 1) / W;
   if (TT > 6) {  // more than 384 block rows: not instantiated
