@@ -177,14 +177,21 @@ __device__ __forceinline__ void cell_family(const QFam& fd, const double2* __res
     const int sg = (int)(cf.amin + ((double)m + 0.5) * dt < 0.0 ? cf.sn1 : cf.sp1);
 #pragma unroll 1
     for (int u0 = 0; u0 < nsr; u0 += 32) {
-      const bool live = u0 + lane < nsr;
-      const int u = live ? u0 + lane : 0;
+      // a last round of at most 6 sub-runs (a third of the pairs end on 1-2 of them) is
+      // spread one point per lane instead of one sub-run per lane
+      const bool wide = u0 > 0 && nsr - u0 <= 32 / kCellSub;  // warp-uniform
+      const int mine = wide ? u0 + lane / kCellSub : u0 + lane;
+      const bool live = mine < nsr;
+      const int u = live ? mine : 0;
       CellRow<D> cr;
       {
         const int c = m * kCellPerDt + ((s_q[u] >> 8) & 31);  // cell on the a axis, from amin
         cr.load(rows, fold ? (c < nsub ? nsub - 1 - c : c - nsub) : c, w);
       }
-      cell_evals<D, kCellSub>(cf, cr, sdel, s_r, s_q, Gm, u, 0, live, koff, ucnt, sg, n_act);
+      if (wide)
+        cell_evals<D, 1>(cf, cr, sdel, s_r, s_q, Gm, u, lane % kCellSub, live, koff, ucnt, sg, n_act);
+      else
+        cell_evals<D, kCellSub>(cf, cr, sdel, s_r, s_q, Gm, u, 0, live, koff, ucnt, sg, n_act);
     }
   }
 }
