@@ -2142,8 +2142,12 @@ int tdb_system_create_impl(TdbContext* ctx, const TdbMesh* mesh, const TdbAssemb
       AsmWorkspace::CellFit fit;
       const double thi_ = fd.lo + fd.nsub * fd.w;
       const double amin_ = fd.fold ? -thi_ : fd.lo, amax_ = thi_;
-      if (p == 0 && K == 7 && (D == 12 || D == 14 || D == 16) && hf.npos >= 2) {
-        const double dtf = (hf.delta[0] - hf.delta[hf.npos - 1]) / (double)(hf.npos - 1);
+      if (p == 0 && K == 7 && (D == 12 || D == 14 || D == 16)) {
+        // (a lag-sharded system may hold a single position of a family: the grid test must
+        // not depend on how many it holds, or the shard would run another kernel than the
+        // single-GPU system and lose bitwise equality)
+        const double dtf = hf.npos >= 2 ? (hf.delta[0] - hf.delta[hf.npos - 1]) / (double)(hf.npos - 1)
+                                        : kCellPerDt * fd.w;
         bool ok = dtf > 0.0;
         for (int s = 0; ok && s < hf.npos; ++s) ok = std::fabs(hf.delta[s] - (hf.delta[0] - s * dtf)) <= 1e-9 * dtf;
         ok = ok && std::fabs(kCellPerDt * fd.w - dtf) <= 1e-9 * dtf;

@@ -451,3 +451,36 @@ def test_cell_owner_kernel_matches_k_quad(G, cfg1_mesh, monkeypatch):
     # p = 1 tables are off the kernel's grid: everything stays on k_quad
     A2 = G[2].assemble_system(cfg1_mesh, TimeGrid(T=1.0, N=5, p=1))
     assert A2.stats()["pairs_cells"] == 0
+
+
+def test_lag_subsets_bitwise_equal_full_system(G, cfg1_mesh):
+    # a system that holds only a lag range of every family (lag-sharded ranks, position
+    # batches) must produce the same bits as the full system, whatever the range: the
+    # pair windows are clipped at the range ends, families may shrink to one position
+    # (kernel selection and the k_quad_cells summation order must not depend on either)
+    from paper_1503_07221_b200 import _lib
+    from paper_1503_07221_b200.assembly import DeviceAssembly, build_plan
+    from paper_1503_07221_b200.block_system import canonical_positions
+    from paper_1503_07221_b200.distributed import partition_lags
+    from paper_1503_07221_b200.kernel_weights import tables_for
+    from paper_1503_07221_b200.temporal_basis import TimeGrid
+
+    grid = TimeGrid(T=3.9, N=40, p=0)
+    tables = tables_for(grid)
+    pos = canonical_positions(grid, cfg1_mesh.diameter)
+    ctx = _lib.default_context(None)
+    full = DeviceAssembly(cfg1_mesh, build_plan(cfg1_mesh, grid, tables, pos), ctx)
+    ref = {p: full.position_blocks(*p)[0][0] for p in full.plan.where}
+    seen = set()
+    for groups, picks in ((2, (0, 1)), (5, (1, 4)), (24, (0, 7, 23))):
+        parts = partition_lags(grid, pos, groups)
+        for lg in picks:
+            if not parts[lg]:
+                continue
+            d = DeviceAssembly(cfg1_mesh, build_plan(cfg1_mesh, grid, tables, parts[lg]), ctx)
+            for p in d.plan.where:
+                a, b = d.position_blocks(*p)[0][0], ref[p]
+                assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices), (groups, lg, p)
+                assert np.array_equal(a.data, b.data), (groups, lg, p)
+                seen.add(p)
+    assert len(seen) > len(ref) // 2
