@@ -14,16 +14,18 @@
 //     position, one dt-span of the table support further per lag.
 //   * The pair's 256 points are sorted by column and cut into column-pure sub-runs of 5.
 //     Per dt span m of the support, every lane takes one sub-run, loads the coefficient
-//     row of its cell (m, j) into REGISTERS once and evaluates its 4 points against it
+//     row of its cell (m, j) into REGISTERS once and evaluates its 5 points against it
 //     (position s = floor(r / dt) + kappa - m).  Per evaluation the LSU delivers the
-//     point (12 B), the position's table offset (8 B), a quarter of a coefficient row
-//     (~50 B) and takes the two table values (16 B) instead of a 180 B row.
+//     point (12 B), the position's table offset (8 B), a fifth of a coefficient row
+//     (~40 B) and takes the two table values (16 B) instead of a 180 B row.
 //   * The values land in G[m][q] (q = rule point).  The regular rule is the tensor
 //     product of a 16-point triangle rule with itself, so the shape products are
 //     contracted per unit as shy_a * sum_ix (c g0)[ix, iy] shx_b[ix]: lane = (iy, half
-//     of ix), 8 fused multiply-adds per table per lane, then the warp reduce-scatter
-//     k_quad uses.  Summation order differs from k_quad's r-sorted order (deterministic,
-//     fixed per lane); everything else is the same arithmetic.
+//     of ix), 8 fused multiply-adds per table per lane, four units per step; the warp sum
+//     exchanges whole register sets in its first two levels (set u of a lane holds unit
+//     si + (u ^ lane bits 4-3): no selects) and ends with an 8-lane reduce-scatter.
+//     Summation order differs from k_quad's r-sorted order (deterministic, fixed per lane,
+//     independent of the pair's position window); everything else is the same arithmetic.
 //
 // Families that do not fit this grid (p > 0, a different cell count, non-uniform lags,
 // table values that do not vanish at the support ends) and the singular cases stay on
@@ -34,7 +36,7 @@ constexpr int kCellWarps = 8;
 constexpr int kCellSpans = 4;   // dt spans of a table support (passes per family), max
 constexpr int kCellPerDt = 32;  // table cells per time step
 // The pair's points are sorted by cell column and cut into column-pure sub-runs of
-// kCellSub (columns padded to a multiple of it): at most (256 + 5 * 32) / 6 = 69
+// kCellSub (columns padded to a multiple of it): at most (256 + 4 * 32) / 5 = 76
 // sub-runs, kept transposed ([entry][sub-run], consecutive lanes read consecutive words).
 // Measured at config 4 (k_quad_cells ms): 4 -> 641, 5 -> 624, 6 -> 641, 8 -> 797: the time
 // follows the evaluation slots per lane (rounds x kCellSub: 12, 11.8, 12, 16).
